@@ -1,0 +1,432 @@
+"""Seeded synthetic workloads shared by the oracle-side and GPU-side tests and
+by bench.py.
+
+This module holds NONE of the method's arithmetic (no marching, filtering,
+compositing, resampling or grid update).  It only builds inputs shaped like the
+paper's workloads (DESIGN.md §5 "input recipe"):
+
+* rays (pinhole cameras; NeRF-Synthetic-like hemisphere rigs, a Mip-NeRF-360-
+  like frame), fp32 origins and unit directions;
+* synthetic scenes standing in for the user's NeRF (Alg. 1 ``density_fn`` /
+  ``rgb_density_fn``): analytic primitives with a soft shell,
+  optionally seen through the Mip-NeRF-360 contraction, evaluated in fp64 at
+  arbitrary points, or baked onto a dense lattice for the GPU harness field;
+* occupancy inputs (a boolean per grid cell) derived from those scenes;
+* ragged packed-sample fuzz inputs (counts, contiguous intervals, σ, rgb).
+
+Everything is a pure function of its seed.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+SQRT3 = math.sqrt(3.0)
+
+
+# --------------------------------------------------------------------------- rays
+def look_at(cam_pos, target, up=(0.0, 0.0, 1.0)):
+    """Camera-to-world rotation (columns right, up, back) for a camera looking at target."""
+    cam_pos, target, up = (np.asarray(v, np.float64) for v in (cam_pos, target, up))
+    fwd = target - cam_pos
+    fwd /= np.linalg.norm(fwd)
+    right = np.cross(fwd, up)
+    if np.linalg.norm(right) < 1e-9:
+        right = np.cross(fwd, np.array([0.0, 1.0, 0.0]))
+    right /= np.linalg.norm(right)
+    true_up = np.cross(right, fwd)
+    return np.stack([right, true_up, -fwd], axis=1)
+
+
+def pinhole_rays(cam_pos, c2w, px, py, width, height, focal):
+    """Rays through pixel centres (px, py) (arrays); returns fp32 o, d (unit)."""
+    px, py = np.asarray(px, np.float64), np.asarray(py, np.float64)
+    dirs_cam = np.stack(
+        [(px + 0.5 - width / 2.0) / focal, -(py + 0.5 - height / 2.0) / focal, -np.ones_like(px)], -1
+    )
+    d = dirs_cam @ np.asarray(c2w).T
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    o = np.broadcast_to(np.asarray(cam_pos, np.float64), d.shape)
+    return o.astype(np.float32), d.astype(np.float32)
+
+
+def hemisphere_cameras(n, radius, centre, seed=0):
+    """n camera centres on the upper hemisphere (Fibonacci lattice)."""
+    i = np.arange(n) + 0.5
+    z = i / n  # upper hemisphere: cos(polar) in (0, 1)
+    phi = math.pi * (1.0 + math.sqrt(5.0)) * i
+    r = np.sqrt(1.0 - z * z)
+    pts = np.stack([r * np.cos(phi), r * np.sin(phi), z], -1) * radius + np.asarray(centre)
+    return pts
+
+
+# --------------------------------------------------------------------------- scenes
+def contract_points(x):
+    """Mip-NeRF-360 contraction x̂ = x (‖x‖ <= 1) else (2 - 1/‖x‖) x/‖x‖ (P:257
+    defers Φ to the cited works; reading #6).  Caller-side only."""
+    x = np.asarray(x, np.float64)
+    n = np.linalg.norm(x, axis=-1, keepdims=True)
+    nn = np.maximum(n, 1e-12)
+    return np.where(n <= 1.0, x, (2.0 - 1.0 / nn) * x / nn)
+
+
+@dataclasses.dataclass
+class Primitives:
+    """Soft-shelled analytic primitives: σ = σ_max·clamp(½ − sdf/w, 0, 1),
+    union by max; rgb = colour of the max-density primitive times a
+    gentle sinusoidal modulation.  With ``unbounded`` the coordinates are the
+    contracted ones and a ground slab plus a noisy background shell are added
+    (the Mip-NeRF-360-shaped CFG3/CFG4 scene).  Only used to bake lattices."""
+
+    kinds: np.ndarray  # 0 sphere, 1 box
+    centres: np.ndarray  # [P,3]
+    sizes: np.ndarray  # [P,3]
+    colours: np.ndarray  # [P,3]
+    sigma_max: float = 500.0
+    width: float = 1.0 / 128.0
+    unbounded: bool = False
+    noise_seed: int = 0
+
+    def sdf_min(self, x):
+        x = np.asarray(x, np.float64)
+        best = np.full(x.shape[0], np.inf)
+        arg = np.zeros(x.shape[0], np.int64)
+        for p in range(len(self.kinds)):
+            c, s = self.centres[p], self.sizes[p]
+            if self.kinds[p] == 1:
+                q = np.abs(x - c) - s
+                d = np.linalg.norm(np.maximum(q, 0.0), axis=-1) + np.minimum(q.max(-1), 0.0)
+            else:
+                d = np.linalg.norm(x - c, axis=-1) - s[0]
+            better = d < best
+            best = np.where(better, d, best)
+            arg = np.where(better, p, arg)
+        return best, arg
+
+    def _noise(self, xh, freq=6.0):
+        f = xh * freq
+        i0 = np.floor(f).astype(np.int64)
+        t = f - i0
+        acc = 0.0
+        for dx in (0, 1):
+            for dy in (0, 1):
+                for dz in (0, 1):
+                    h = ((i0[..., 0] + dx) * 73856093) ^ ((i0[..., 1] + dy) * 19349663) ^ ((i0[..., 2] + dz) * 83492791)
+                    h = (h ^ (self.noise_seed * 2654435761)) & 0xFFFFFFFF
+                    h = (h * 2246822519) & 0xFFFFFFFF
+                    h ^= h >> 13
+                    v = (h & 0xFFFF) / 65535.0
+                    wx = t[..., 0] if dx else 1 - t[..., 0]
+                    wy = t[..., 1] if dy else 1 - t[..., 1]
+                    wz = t[..., 2] if dz else 1 - t[..., 2]
+                    acc = acc + v * wx * wy * wz
+        return acc
+
+    def sigma_rgb(self, x):
+        x = np.asarray(x, np.float64).reshape(-1, 3)
+        d, arg = self.sdf_min(x)
+        sg = self.sigma_max * np.clip(0.5 - d / self.width, 0.0, 1.0)
+        col = self.colours[arg] * (0.75 + 0.25 * np.sin(40.0 * x.sum(-1)))[:, None]
+        if self.unbounded:
+            rn = np.linalg.norm(x, axis=-1)
+            ground = self.sigma_max * np.clip(0.5 - (np.abs(x[:, 2] + 0.60) - 0.02) / self.width, 0, 1)
+            ground = np.where(rn < 1.0, ground, 0.0)
+            shell = self.sigma_max * np.clip(0.5 - (np.abs(rn - 1.70) - 0.15) / (4 * self.width), 0, 1)
+            shell = shell * (self._noise(x) > 0.62)
+            scol = np.stack([0.3 + 0.4 * self._noise(x * 1.3), np.full(len(x), 0.5), np.full(len(x), 0.7)], -1)
+            col = np.where((ground > sg)[:, None], np.array([0.35, 0.3, 0.25]), col)
+            sg = np.maximum(sg, ground)
+            col = np.where((shell > sg)[:, None], scol, col)
+            sg = np.maximum(sg, shell)
+        return sg, np.clip(col, 0.0, 1.0)
+
+
+def random_primitives(seed, n_prims=24, lo=0.25, hi=0.75, size_lo=0.04, size_hi=0.15,
+                      unbounded=False, width=1.0 / 128.0):
+    rng = np.random.default_rng(seed)
+    kinds = rng.integers(0, 2, n_prims)
+    centres = rng.uniform(lo, hi, (n_prims, 3))
+    sizes = rng.uniform(size_lo, size_hi, (n_prims, 3))
+    sizes[kinds == 0, 1:] = sizes[kinds == 0, :1]
+    colours = rng.uniform(0.1, 0.9, (n_prims, 3))
+    return Primitives(kinds, centres, sizes, colours, unbounded=unbounded, noise_seed=seed, width=width)
+
+
+@dataclasses.dataclass
+class Lattice:
+    """Dense cell-centre lattice field: data[z,y,x] = (σ, r, g, b)
+    float32 over the box [lo, hi]^3, trilinear between cell centres, clamped
+    to the edge centres, 0 outside the box.  ``contracted`` queries it at the
+    contracted point.  This is the caller's NeRF stand-in (Alg. 1
+    density_fn/rgb_density_fn); the GPU harness field evaluates the
+    same lattice in fp32."""
+
+    data: np.ndarray  # [res,res,res,4] float32
+    lo: float
+    hi: float
+    contracted: bool = False
+
+    @property
+    def res(self):
+        return self.data.shape[0]
+
+    def sigma_rgb(self, x, chunk=1 << 21):
+        x = np.asarray(x, np.float64)
+        shp = x.shape[:-1]
+        x = x.reshape(-1, 3)
+        out = np.empty((x.shape[0], 4))
+        flat = self.data.reshape(-1, 4)
+        R = self.res
+        for s in range(0, x.shape[0], chunk):
+            xs = x[s : s + chunk]
+            if self.contracted:
+                xs = contract_points(xs)
+            inside = np.all((xs >= self.lo) & (xs <= self.hi), axis=-1)
+            u = (xs - self.lo) / (self.hi - self.lo) * R - 0.5
+            u = np.clip(u, 0.0, R - 1.0)
+            i0 = np.minimum(np.floor(u).astype(np.int64), R - 2)
+            f = u - i0
+            acc = np.zeros((xs.shape[0], 4))
+            for dz in (0, 1):
+                for dy in (0, 1):
+                    for dx in (0, 1):
+                        w = (f[:, 0] if dx else 1 - f[:, 0]) * (f[:, 1] if dy else 1 - f[:, 1]) * (f[:, 2] if dz else 1 - f[:, 2])
+                        idx = (i0[:, 0] + dx) + R * ((i0[:, 1] + dy) + R * (i0[:, 2] + dz))
+                        acc += w[:, None] * flat[idx]
+            acc[~inside] = 0.0
+            out[s : s + chunk] = acc
+        return out[:, 0].reshape(shp), out[:, 1:].reshape(shp + (3,))
+
+
+def bake_lattice(prims, res, lo, hi, contracted=False):
+    """Sample primitives at the res^3 cell-centre lattice."""
+    c = lo + (np.arange(res) + 0.5) / res * (hi - lo)
+    zz, yy, xx = np.meshgrid(c, c, c, indexing="ij")
+    pts = np.stack([xx, yy, zz], -1).reshape(-1, 3)
+    sig, rgb = prims.sigma_rgb(pts)
+    data = np.concatenate([sig[:, None], rgb], 1).astype(np.float32).reshape(res, res, res, 4)
+    return Lattice(data, float(lo), float(hi), contracted)
+
+
+def _maxpool3(a):
+    p = np.pad(a, 1)
+    out = np.zeros_like(a)
+    n = a.shape[0]
+    for dz in range(3):
+        for dy in range(3):
+            for dx in range(3):
+                out = np.maximum(out, p[dz : dz + n, dy : dy + n, dx : dx + n])
+    return out
+
+
+def occupancy_from_lattice(lat, levels, res, roi, sigma_thresh=5.0):
+    """Occupancy input (uint8 per cell, level-major, x fastest): for the bounded
+    lattice on the same 128^3 cells, the 3x3x3 max of lattice σ > threshold
+    (conservative for trilinear); for cascades, σ at the cell centre."""
+    roi = np.asarray(roi, np.float64)
+    ctr, half = (roi[:3] + roi[3:]) / 2, (roi[3:] - roi[:3]) / 2
+    out = []
+    if not lat.contracted and levels == 1 and lat.res == res and np.allclose(roi, [lat.lo] * 3 + [lat.hi] * 3):
+        return (_maxpool3(lat.data[..., 0]) > sigma_thresh).astype(np.uint8).ravel()
+    c = (np.arange(res) + 0.5) / res
+    zz, yy, xx = np.meshgrid(c, c, c, indexing="ij")
+    unit = np.stack([xx, yy, zz], -1).reshape(-1, 3)
+    for l in range(levels):
+        lo, hi = ctr - half * 2**l, ctr + half * 2**l
+        sig, _ = lat.sigma_rgb(lo + unit * (hi - lo))
+        out.append((sig > sigma_thresh).astype(np.uint8))
+    return np.concatenate(out)
+
+
+# --------------------------------------------------------------------------- configs
+@dataclasses.dataclass
+class MarchConfig:
+    name: str
+    levels: int
+    res: int
+    roi: tuple
+    rays_o: np.ndarray
+    rays_d: np.ndarray
+    occ: np.ndarray  # uint8 per cell
+    near: float
+    far: float
+    step: float
+    max_step: float = 1e10
+    cone_angle: float = 0.0
+    scene: object = None
+    eps: float = 1e-4
+
+
+def cfg1(seed=1001):
+    """CFG1 (configs[0]): 64 rays through a 32^3 grid in the unit box, analytic
+    sphere (c = 0.5, r = 0.3, σ0 = 20), step 1e-2."""
+    origin = np.array([0.5, 0.5, -0.5])
+    g = 0.5 + 0.45 * ((np.arange(8) + 0.5) / 4.0 - 1.0)
+    tx, ty = np.meshgrid(g, g, indexing="xy")
+    tgt = np.stack([tx.ravel(), ty.ravel(), np.full(64, 0.5)], -1)
+    d = tgt - origin
+    o = np.broadcast_to(origin, d.shape).copy()
+    for k, side in zip((0, 7, 56, 63), ((-1, -1), (1, -1), (-1, 1), (1, 1))):
+        d[k] = np.array([side[0] * 3.0, side[1] * 3.0, 1.0])  # corner rays miss the box
+    o[9], d[9] = [0.53, 0.47, -0.5], [0.0, 0.0, 1.0]  # axis-aligned ray
+    o[18], d[18] = [0.45, 0.55, 0.4], [0.3, 0.2, 1.0]  # origin inside the box
+    o[27], d[27] = [1.5, 0.52, 0.5], [-1.0, 0.0, 0.0]  # axis-aligned, -x
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    # conservative occupancy: cells whose closest point lies within the sphere (exact fp64)
+    res, c, r = 32, np.array([0.5, 0.5, 0.5]), 0.3
+    idx = np.arange(res)
+    zz, yy, xx = np.meshgrid(idx, idx, idx, indexing="ij")
+    lo = np.stack([xx, yy, zz], -1).reshape(-1, 3) / res
+    hi = lo + 1.0 / res
+    closest = np.clip(c, lo, hi)
+    occ = (np.linalg.norm(closest - c, axis=-1) <= r).astype(np.uint8)
+    return MarchConfig("cfg1", 1, 32, (0, 0, 0, 1, 1, 1), o.astype(np.float32), d.astype(np.float32),
+                       occ, 0.0, 1e10, float(np.float32(1e-2)))
+
+
+CFG1_SPHERE = dict(centre=(0.5, 0.5, 0.5), radius=0.3, sigma0=20.0, rgb=(0.9, 0.6, 0.3))
+
+
+def sphere_sigma_rgb(x, centre=(0.5, 0.5, 0.5), radius=0.3, sigma0=20.0, rgb=(0.9, 0.6, 0.3)):
+    x = np.asarray(x, np.float64)
+    inside = np.linalg.norm(x - np.asarray(centre), axis=-1) <= radius
+    sig = np.where(inside, sigma0, 0.0)
+    col = np.where(inside[..., None], np.asarray(rgb), 0.0)
+    return sig, col
+
+
+def cfg2_rays(n_rays, seed=1002, n_cams=100, width=800, height=800, focal=1111.1111, radius=1.35):
+    rng = np.random.default_rng(seed)
+    centre = np.array([0.5, 0.5, 0.5])
+    cams = hemisphere_cameras(n_cams, radius, centre)
+    cam = rng.integers(0, n_cams, n_rays)
+    px = rng.integers(0, width, n_rays)
+    py = rng.integers(0, height, n_rays)
+    o = np.empty((n_rays, 3), np.float32)
+    d = np.empty((n_rays, 3), np.float32)
+    for c in range(n_cams):
+        m = cam == c
+        if m.any():
+            oo, dd = pinhole_rays(cams[c], look_at(cams[c], centre), px[m], py[m], width, height, focal)
+            o[m], d[m] = oo, dd
+    return o, d
+
+
+def cfg2_lattice(seed=1002):
+    prims = random_primitives(seed)
+    return bake_lattice(prims, 128, 0.0, 1.0)
+
+
+def cfg2(n_rays=1 << 18, seed=1002, lattice=None):
+    """CFG2 (configs[1]): NeRF-Synthetic-shaped training batch, 2^18 rays,
+    128^3 grid over the unit box, step fp32(√3/1024), dense-lattice field."""
+    lat = lattice if lattice is not None else cfg2_lattice(seed)
+    o, d = cfg2_rays(n_rays, seed)
+    occ = occupancy_from_lattice(lat, 1, 128, (0, 0, 0, 1, 1, 1))
+    return MarchConfig("cfg2", 1, 128, (0, 0, 0, 1, 1, 1), o, d, occ, 0.0, 1e10,
+                       float(np.float32(SQRT3 / 1024.0)), scene=lat)
+
+
+def cfg3_lattice(seed=1003):
+    prims = random_primitives(seed, n_prims=24, lo=-0.35, hi=0.35, size_lo=0.04, size_hi=0.15,
+                              unbounded=True, width=1.0 / 64.0)
+    return bake_lattice(prims, 128, -2.0, 2.0, contracted=True)
+
+
+def cfg3(width=800, height=800, seed=1003, rays_subset=None, lattice=None):
+    """CFG3 (configs[2]): one 800x800 frame, 4-level cascaded 128^3 grid over
+    [-1,1]^3 .. [-8,8]^3, cone step c = 1/256, Δt_min = fp32(2√3/1024), near 0.2,
+    field = lattice over contracted [-2,2]^3."""
+    lat = lattice if lattice is not None else cfg3_lattice(seed)
+    cam = np.array([0.0, -0.75, 0.2])
+    py, px = np.meshgrid(np.arange(height), np.arange(width), indexing="ij")
+    px, py = px.ravel(), py.ravel()
+    if rays_subset is not None:
+        px, py = px[rays_subset], py[rays_subset]
+    o, d = pinhole_rays(cam, look_at(cam, (0.0, 0.0, 0.0)), px, py, width, height, 720.0)
+    occ = occupancy_from_lattice(lat, 4, 128, (-1, -1, -1, 1, 1, 1))
+    return MarchConfig("cfg3", 4, 128, (-1, -1, -1, 1, 1, 1), o, d, occ, 0.2, 1e10,
+                       float(np.float32(2.0 * SQRT3 / 1024.0)), max_step=1e10,
+                       cone_angle=float(np.float32(1.0 / 256.0)), scene=lat)
+
+
+@dataclasses.dataclass
+class PropConfig:
+    rays_o: np.ndarray
+    rays_d: np.ndarray
+    s_edges: np.ndarray  # [n, 257]
+    t_near: float
+    t_far: float
+    n_out: tuple
+    scene: object
+
+
+def cfg4(n_rays=1 << 16, seed=1004):
+    """CFG4 (configs[3]): proposal estimator, 2^16 rays, 256 -> 96 -> 48 intervals,
+    lindisp Φ with t_n = 0.2, t_f = 1000."""
+    rng = np.random.default_rng(seed)
+    ang = 2 * math.pi * (np.arange(16) + 0.5) / 16
+    cams = np.stack([0.75 * np.cos(ang), 0.75 * np.sin(ang), np.full(16, 0.2)], -1)
+    cam = rng.integers(0, 16, n_rays)
+    px = rng.integers(0, 800, n_rays)
+    py = rng.integers(0, 800, n_rays)
+    o = np.empty((n_rays, 3), np.float32)
+    d = np.empty((n_rays, 3), np.float32)
+    for c in range(16):
+        m = cam == c
+        if m.any():
+            o[m], d[m] = pinhole_rays(cams[c], look_at(cams[c], (0, 0, 0)), px[m], py[m], 800, 800, 720.0)
+    s = np.broadcast_to((np.arange(257) / 256.0).astype(np.float32), (n_rays, 257)).copy()
+    return PropConfig(o, d, s, 0.2, 1000.0, (96, 48), cfg3_lattice(seed - 1))
+
+
+def lindisp(s, tn, tf):
+    """Φ for building caller-side inputs only (midpoints to query the field)."""
+    s = np.asarray(s, np.float64)
+    return 1.0 / ((1.0 - s) / tn + s / tf)
+
+
+def field_at_intervals(scene_fn, rays_o, rays_d, t0, t1, ray_id):
+    """Caller-side field query at interval midpoints: σ, rgb as fp32."""
+    t0, t1 = np.asarray(t0, np.float64), np.asarray(t1, np.float64)
+    m = 0.5 * (t0 + t1)
+    o = np.asarray(rays_o, np.float64)[ray_id]
+    d = np.asarray(rays_d, np.float64)[ray_id]
+    sig, rgb = scene_fn(o + m[:, None] * d)
+    return sig.astype(np.float32), rgb.astype(np.float32)
+
+
+# --------------------------------------------------------------------------- fuzz inputs
+def ragged_samples(n_rays, seed, max_count=300, long_rays=(0,), long_count=1100, p_zero=0.15):
+    """Ragged packed samples: counts in [0, max_count] (some 0, a few > 1 tile),
+    contiguous ascending intervals with random widths, σ a mixture of empty
+    space, thin media and opaque spikes; rgb in [0,1]."""
+    rng = np.random.default_rng(seed)
+    counts = rng.integers(0, max_count + 1, n_rays)
+    counts[rng.random(n_rays) < p_zero] = 0
+    for r in long_rays:
+        if r < n_rays:
+            counts[r] = long_count
+    N = int(counts.sum())
+    start = np.zeros(n_rays, np.int64)
+    start[1:] = np.cumsum(counts)[:-1]
+    packed = np.stack([start, counts], 1).astype(np.int64)
+    ray_id = np.repeat(np.arange(n_rays, dtype=np.int32), counts)
+    widths = rng.uniform(1e-3, 2e-2, N).astype(np.float32)
+    t0 = np.empty(N, np.float32)
+    t1 = np.empty(N, np.float32)
+    for r in range(n_rays):
+        s, c = start[r], counts[r]
+        if c == 0:
+            continue
+        w = widths[s : s + c].astype(np.float64)
+        gaps = np.where(rng.random(c) < 0.1, rng.uniform(0, 0.05, c), 0.0)
+        edges = rng.uniform(0.05, 0.5) + np.concatenate([[0.0], np.cumsum(w + gaps)])
+        t0[s : s + c] = edges[:-1] + gaps
+        t1[s : s + c] = edges[1:]
+    kind = rng.random(N)
+    sigma = np.where(kind < 0.5, 0.0, np.where(kind < 0.85, rng.uniform(0, 5, N), rng.uniform(50, 500, N)))
+    rgb = rng.uniform(0, 1, (N, 3))
+    return packed, t0, t1, ray_id, sigma.astype(np.float32), rgb.astype(np.float32)
