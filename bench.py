@@ -1,0 +1,437 @@
+"""bench.py — throughput of the NerfAcc packed-sample hot path on B200.
+
+One step = one CFG2 training step (BASELINE.json configs[1], the config the
+metric is quoted on): march the occupancy grid (nacc_sampling_occgrid) ->
+caller's no-grad σ query (harness lattice field) -> no-gradient early-stop
+filter (nacc_filter_early_stop) -> caller's σ, rgb query -> render fwd
+(nacc_render_fwd) -> MSE gradient -> render bwd (nacc_render_bwd), plus the
+occupancy-grid update with its MAX all-reduce every 16 steps (points ->
+field -> all_reduce -> nacc_occgrid_update).  Rays are sharded across ranks
+(2^18 per GPU, weak scaling); the grid is replicated.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec (march+render fwd+bwd) and HBM GB/s vs 8 TB/s at 1/2/4/8 B200"
+UNIT = "samples/s"
+RAYS_PER_GPU = 1 << 18
+UPDATE_EVERY = 16
+EPS = 1e-4
+WORKLOAD = ("cfg2: NeRF-Synthetic-shaped training batch, 2^18 rays per GPU, 128^3 occupancy grid over the unit box, "
+            "step sqrt(3)/1024, early stop T<1e-4, dense-lattice trilinear sigma/rgb field, fwd+bwd, "
+            "grid EMA update + MAX all-reduce every 16 steps")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="nacc", choices=["nacc", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+# ----------------------------------------------------------------------------- clocks (NVML)
+class ClockSampler:
+    def __init__(self, index):
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake_slowdown",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- workload
+def make_inputs(rank, n_batches=4):
+    import workloads as W
+
+    rays = []
+    for b in range(n_batches):
+        o, d = W.cfg2_rays(RAYS_PER_GPU, seed=1002 + 1000 * rank + 17 * b)
+        rays.append((o, d))
+    lat = W.cfg2_lattice()
+    rng = np.random.default_rng(7 + rank)
+    gt = rng.uniform(0, 1, (RAYS_PER_GPU, 3)).astype(np.float32)
+    return rays, lat, gt
+
+
+class Pipeline:
+    """One CFG2 training step through the public API (paper_2305_04966_b200)."""
+
+    def __init__(self, rank, world, device):
+        import torch
+
+        import workloads as W
+        import paper_2305_04966_b200 as N
+        from paper_2305_04966_b200 import harness as H
+
+        self.N, self.H, self.torch = N, H, torch
+        self.rank, self.world, self.device = rank, world, device
+        rays, lat, gt = make_inputs(rank)
+        self.rays_host = rays
+        self.rays = [(torch.from_numpy(o).to(device), torch.from_numpy(d).to(device)) for o, d in rays]
+        self.gt = torch.from_numpy(gt).to(device)
+        self.field = H.LatticeField(torch.from_numpy(lat.data.reshape(-1, 4)).to(device), lat.lo, lat.hi)
+        self.spec = N.GridSpec(roi=(0, 0, 0, 1, 1, 1), res=128, levels=1)
+        self.step_size = float(np.float32(W.SQRT3 / 1024.0))
+        self.params = N.MarchParams(step=self.step_size)
+        self.grid = N.OccupancyGrid(self.spec, device=device, decay=0.95, threshold=0.01, seed=1234)
+        self.occ_fn = lambda x: self.field.at_points(x, self.step_size)  # v = σ·Δt
+        for k in range(16):  # warm the estimator (SPEC cmd_render W = 16), untimed
+            self.grid.update_every_n_steps(k * UPDATE_EVERY, self.occ_fn, n=UPDATE_EVERY)
+        self.capacity = None
+        self.k = 0
+        self.stats = {"pre": 0, "post": 0, "rays": 0}
+        self.events = []
+
+    def step(self, rays=None, timing=False):
+        N, H, torch = self.N, self.H, self.torch
+        o, d = rays if rays is not None else self.rays[self.k % len(self.rays)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
+        rec = (lambda i: ev[i].record()) if timing else (lambda i: None)
+        rec(0)
+        s = N.sampling_occgrid(o, d, self.spec, self.grid.bits, self.params, capacity=self.capacity)
+        self.capacity = int(s.n_samples * 1.15) + 1024
+        rec(1)
+        sigma, _ = self.field.at_samples(o, d, s.t0, s.t1, s.ray_id, want_rgb=False)
+        rec(2)
+        f = N.filter_early_stop(s, sigma, EPS)
+        rec(3)
+        sig2, rgb = self.field.at_samples(o, d, f.t0, f.t1, f.ray_id, want_rgb=True)
+        sig2.requires_grad_(True)
+        rgb.requires_grad_(True)
+        rec(4)
+        color, opacity, depth = N.rendering(f, sig2, rgb, eps=EPS)
+        rec(5)
+        g = H.mse_grad(color.detach(), self.gt)
+        rec(6)
+        color.backward(g)
+        rec(7)
+        self.grid.update_every_n_steps(self.k, self.occ_fn, n=UPDATE_EVERY)
+        rec(8)
+        self.k += 1
+        self.stats["pre"] += s.n_samples
+        self.stats["post"] += f.n_samples
+        self.stats["rays"] += s.n_rays
+        if timing:
+            self.events.append(ev)
+        return color, opacity, depth, f.n_samples
+
+    def stage_ms(self):
+        names = ["march", "field_sigma", "filter", "field_sigma_rgb", "render_fwd", "mse_grad", "render_bwd",
+                 "grid_update"]
+        acc = {n: 0.0 for n in names}
+        for ev in self.events:
+            for i, n in enumerate(names):
+                acc[n] += ev[i].elapsed_time(ev[i + 1])
+        k = max(len(self.events), 1)
+        return {n: v / k for n, v in acc.items()}
+
+
+def algorithmic_bytes(stage, pre, post, rays):
+    """SURVEY §8(d).4 / DESIGN.md §6: bytes the method must move, per launch."""
+    if stage == "march":
+        return rays * (24 + 16) + pre * 12
+    if stage == "filter":
+        return rays * 32 + post * 12 * 2 + rays * 16
+    if stage == "render_fwd":
+        return post * 24 + rays * (16 + 20 + 40)
+    if stage == "render_bwd":
+        return post * 40 + rays * (16 + 12 + 40)
+    return None
+
+
+# ----------------------------------------------------------------------------- oracle (CPU baseline)
+def oracle_sample(n_rays, seed_offset=0):
+    """A bounded sample of the CFG2 workload for the CPU oracle: n_rays rays,
+    with the caller's σ/rgb precomputed (numpy field, untimed)."""
+    import oracle as O
+    import workloads as W
+
+    lat = W.cfg2_lattice()
+    o, d = W.cfg2_rays(n_rays, seed=1002 + seed_offset)
+    occ = W.occupancy_from_lattice(lat, 1, 128, (0, 0, 0, 1, 1, 1))
+    step = float(np.float32(W.SQRT3 / 1024.0))
+    pk, t0, t1, rid = O.march(occ, 1, 128, (0, 0, 0, 1, 1, 1), o, d, step=step)
+    sig, _ = W.field_at_intervals(lat.sigma_rgb, o, d, t0, t1, rid)
+    L = -math.log(float(np.float32(EPS)))
+    pk2, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, sig, L)
+    s2, rgb = W.field_at_intervals(lat.sigma_rgb, o, d, a0, a1, r2)
+    gt = np.random.default_rng(0).uniform(0, 1, (n_rays, 3))
+    return dict(o=o, d=d, occ=occ, step=step, sig=sig, s2=s2, rgb=rgb, L=L, gt=gt)
+
+
+def oracle_step(inp):
+    """march -> filter -> render fwd -> render bwd on the CPU oracle (timed part)."""
+    import oracle as O
+
+    pk, t0, t1, rid = O.march(inp["occ"], 1, 128, (0, 0, 0, 1, 1, 1), inp["o"], inp["d"], step=inp["step"])
+    pk2, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, inp["sig"], inp["L"])
+    out = O.render_fwd(pk2, a0, a1, inp["s2"], inp["rgb"], neg_log_eps=inp["L"])
+    g = 2.0 * (out["color"] - inp["gt"]) / (3 * len(pk2))
+    O.render_bwd(pk2, a0, a1, inp["s2"], inp["rgb"], g, None, None, neg_log_eps=inp["L"])
+    return len(a0)
+
+
+def cpu_baseline(n_rays=1 << 15, reps=3):
+    import oracle as O
+
+    inp = oracle_sample(n_rays)
+    oracle_step(inp)
+    t = time.perf_counter()
+    post = 0
+    for _ in range(reps):
+        post += oracle_step(inp)
+    dt = time.perf_counter() - t
+    return {"value": post / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"{n_rays} CFG2 rays x {reps} reps (march+filter+render fwd+bwd; field precomputed)",
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+
+    # size each step so the whole --steps K --warmup W run stays within ~2 minutes
+    probe = oracle_sample(4096, seed_offset=5)
+    t = time.perf_counter()
+    oracle_step(probe)
+    per_ray = (time.perf_counter() - t) / 4096
+    budget = 90.0 / max(args.steps + args.warmup, 1)
+    n = int(min(1 << 16, max(256, budget / max(per_ray, 1e-9))))
+    n = 1 << int(math.floor(math.log2(n)))
+    inp = oracle_sample(n)
+    for _ in range(args.warmup):
+        oracle_step(inp)
+    t = time.perf_counter()
+    post = 0
+    for _ in range(args.steps):
+        post += oracle_step(inp)
+    dt = time.perf_counter() - t
+    value = post / dt
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "rays_per_step": n, "parallelism": "oracle on host cores (rank 0)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+                             "sample": f"{n} CFG2 rays per step (field precomputed, untimed)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- main arm
+def run_nacc(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    import paper_2305_04966_b200 as N
+    from paper_2305_04966_b200 import harness as H
+
+    pipe = Pipeline(rank, world, device)
+    for _ in range(max(args.warmup, 3)):
+        pipe.step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- device-timed region: inputs resident in HBM
+    pipe.stats = {"pre": 0, "post": 0, "rays": 0}
+    l0 = N.launch_count() + H.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            pipe.step(timing=not args.profile)
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    launches = N.launch_count() + H.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    stats = dict(pipe.stats)
+    stages = pipe.stage_ms() if not args.profile else {}
+    t = torch.tensor([ms, stats["post"], stats["pre"], stats["rays"]], dtype=torch.float64, device=device)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        t[0] = tmax[0]
+    ms_max, post_all, pre_all, rays_all = t.tolist()
+    value = post_all / (ms_max / 1e3)
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.profile:
+        pinned = [(torch.from_numpy(o).pin_memory(), torch.from_numpy(d).pin_memory()) for o, d in pipe.rays_host]
+        out_host = torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32).pin_memory()
+        k2 = max(args.steps // 4, 20)
+        post_e2e = 0
+        barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for i in range(k2):
+            ho, hd = pinned[i % len(pinned)]
+            o = ho.to(device, non_blocking=True)
+            d = hd.to(device, non_blocking=True)
+            color, opacity, depth, n_post = pipe.step(rays=(o, d))
+            res = torch.cat([color.detach(), opacity.detach()[:, None], depth.detach()[:, None]], 1)
+            out_host.copy_(res, non_blocking=True)
+            post_e2e += n_post
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms2 = f0.elapsed_time(f1)
+        t2 = torch.tensor([ms2, post_e2e], dtype=torch.float64, device=device)
+        if world > 1:
+            m = t2.clone()
+            dist.all_reduce(m[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t2[1:], op=dist.ReduceOp.SUM)
+            t2[0] = m[0]
+        e2e = {"value": t2[1].item() / (t2[0].item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": RAYS_PER_GPU * 24,
+               "d2h_bytes_per_step": RAYS_PER_GPU * 20, "steps": k2}
+
+    if rank == 0:
+        peak, peak_kind = measured_peaks()
+        K = args.steps
+        pre_pg, post_pg, rays_pg = stats["pre"] / K, stats["post"] / K, stats["rays"] / K
+        roof = None
+        if stages:
+            lib_stages = {k: v for k, v in stages.items() if algorithmic_bytes(k, 1, 1, 1) is not None}
+            dom = max(lib_stages, key=lib_stages.get)
+            byts = algorithmic_bytes(dom, pre_pg, post_pg, rays_pg)
+            achieved = byts / (lib_stages[dom] / 1e3) / 1e9
+            tr = ncu_traffic().get(dom)
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": tr, "kernel": dom, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": byts,
+                    "ms_per_launch": lib_stages[dom]}
+        cpu = None
+        if not args.no_cpu_baseline and not args.profile and world == 1:
+            cpu = cpu_baseline()
+        clocks = clk.summary()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "rays_per_gpu": RAYS_PER_GPU, "global_rays_per_step": rays_all / K,
+                           "grid": "1x128^3", "parallelism": f"dp{world} (ray-sharded, replicated grid)",
+                           "l2": "inputs larger than L2 (march output ~0.25 GB/step/GPU; 4 rotating ray batches)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+                "samples_pre_filter_per_step_per_gpu": pre_pg, "samples_post_filter_per_step_per_gpu": post_pg,
+                "pre_filter_samples_per_s": pre_all / (ms_max / 1e3), "rays_per_s": rays_all / (ms_max / 1e3),
+                "stage_ms": stages,
+                "library_ms_per_step": sum(v for k, v in stages.items() if algorithmic_bytes(k, 1, 1, 1) is not None)
+                if stages else None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_nacc(args)
+
+
+if __name__ == "__main__":
+    main()

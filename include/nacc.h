@@ -1,0 +1,243 @@
+/*
+ * nacc.h — C ABI of the B200-native packed-sample volume-rendering core
+ * (the data-parallel hot path of NerfAcc, arXiv 2305.04966).
+ *
+ * The calls mirror Algorithm 1 of the paper:
+ *   t0, t1, r_id = nerfacc.sampling(r_o, r_d, estimator, density_fn)
+ *       -> nacc_sampling_occgrid (+ caller evaluates σ) -> nacc_filter_early_stop
+ *   color, opacity, depth, aux = nerfacc.rendering(t0, t1, r_id, ...)
+ *       -> nacc_render_fwd / nacc_render_bwd (fused), or the granular
+ *          nacc_render_weights_fwd/bwd + nacc_accumulate_along_rays(_bwd)
+ *   estimator.update_every_n_steps(...)
+ *       -> nacc_occgrid_points (+ caller evaluates σ, all-reduces MAX)
+ *          -> nacc_occgrid_update
+ *   proposal-network estimator -> nacc_importance_sample
+ * The library never calls the radiance field: Alg. 1's density_fn /
+ * rgb_density_fn are evaluated by the caller between calls.
+ *
+ * Conventions (apply to every call unless stated):
+ *  - Pointers are DEVICE pointers unless named *_host.  The caller owns and
+ *    allocates every buffer; the library never allocates, frees, retains
+ *    pointers past stream completion, or keeps global state (except the
+ *    thread-local error string and a launch counter).
+ *  - Every call is asynchronous on `stream` and never synchronises.  Counts
+ *    that size later buffers (`total`) are written to device int64s.
+ *  - Host-side validation runs before any launch.  On invalid arguments the
+ *    call returns NACC_ERR_INVALID_ARGUMENT and writes nothing.  n_rays == 0
+ *    returns NACC_OK without launching (totals are set to 0 with a memset).
+ *    CUDA launch errors return NACC_ERR_CUDA; nacc_last_error() (thread-local)
+ *    holds the message.  Nothing aborts, exits or throws across the ABI.
+ *  - Device preconditions are NOT checked: σ >= 0 and finite;
+ *    ‖d‖ ≈ 1; per-ray intervals ascending and non-overlapping.
+ *  - Layout ("sample as interval", "packed tensor"): samples are SoA
+ *    t0[N], t1[N], sigma[N] fp32, rgb[N][3] fp32, ray_id[N] int32, ordered by
+ *    ray then ascending t; packed_info[n_rays][2] int64 = (start, count).
+ *    Arrays must be 4-byte aligned; packed_info / ctx 8-byte aligned.
+ *  - Occupancy bitfield layout (public): cell q = l*R^3 + x + R*(y + R*z) of
+ *    level l is bit (q & 31) of uint32 word (q >> 5).  Density arrays use the
+ *    same cell order (level-major, x fastest; reading #27).
+ */
+#ifndef NACC_H
+#define NACC_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NACC_ABI_VERSION 1
+
+typedef enum {
+  NACC_OK = 0,
+  NACC_ERR_INVALID_ARGUMENT = 1,
+  NACC_ERR_INSUFFICIENT_CAPACITY = 2, /* reported through *status_out of one-shot calls */
+  NACC_ERR_CUDA = 3,
+  NACC_ERR_UNSUPPORTED = 4
+} nacc_status;
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *nacc_last_error(void);
+int nacc_abi_version(void);
+/* Number of kernels this library has launched in this process (all threads). */
+uint64_t nacc_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Occupancy grid ("Spatial Skipping"; Instant-NGP cascade,         */
+/* DESIGN.md reading #4): level l covers centre ± half·2^l of `roi`, l < levels */
+/* (1..8), res^3 cells per level, levels*res^3 < 2^31.                          */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t levels;
+  int32_t res;
+  float roi[6]; /* lo_x, lo_y, lo_z, hi_x, hi_y, hi_z of level 0; lo < hi */
+} nacc_grid;
+
+/* Ray-marching parameters ("follow the original paper's implementation";
+ * P:158 marching step Δt; P:257 coarser steps with distance). */
+typedef struct {
+  float near_plane; /* lattice anchor when t_min == NULL (reading #1) */
+  float far_plane;  /* interval k is emitted only if its midpoint < far */
+  float step;       /* Δt (uniform lattice) or Δt_min (cone lattice); > 0 finite */
+  float max_step;   /* Δt_max for the cone lattice; >= step */
+  float cone_angle; /* c >= 0; 0 = uniform lattice t_k = near + kΔt (reading #5) */
+  int32_t stratified; /* jitter each ray's anchor by ξ_r·Δt, ξ_r = Philox(seed,(r,0,0,0)) */
+  uint64_t seed;
+} nacc_march;
+
+/* Bytes of the bitfield for `grid`: 4*ceil(levels*res^3/32). 0 if invalid. */
+size_t nacc_grid_bits_bytes(const nacc_grid *grid);
+
+/* Workspace for nacc_sampling_occgrid / _fill with n_rays rays. */
+size_t nacc_sampling_occgrid_workspace_bytes(const nacc_grid *grid, const nacc_march *params,
+                                             int64_t n_rays);
+
+/* Alg. 1 nerfacc.sampling with the occupancy-grid estimator.
+ * For every ray r, interval k of the lattice (uniform t_k = near_r + kΔt, or
+ * the cone recurrence t_{k+1} = t_k + clamp(t_k·c, Δt_min, Δt_max)) is emitted
+ * iff its midpoint m_k < far_r lies in an occupied cell of the finest level
+ * whose box holds it (readings #1-#3; the fp32 op sequence there is
+ * normative).  Emitted intervals are packed: t0 = t_k, t1 = t_{k+1},
+ * ray_id = r, in ray then k order.
+ *   bits          occupancy bitfield (layout above), nacc_grid_bits_bytes()
+ *   rays_o/_d     [n_rays][3] fp32 origins / unit directions
+ *   t_min, t_max  optional per-ray near/far [n_rays] (NULL = params' planes);
+ *                 the cone lattice requires t_min == NULL and stratified == 0
+ *                 (shared anchor), else NACC_ERR_UNSUPPORTED
+ *   packed_info   [n_rays][2] int64 out, always written
+ *   total         device int64 out: Σ counts, always written
+ *   t0,t1,ray_id  [capacity] out; written only if total <= capacity, else the
+ *                 device int32 *status_out (NULL allowed) is set to
+ *                 NACC_ERR_INSUFFICIENT_CAPACITY (else NACC_OK) and the caller
+ *                 re-allocates and calls nacc_sampling_occgrid_fill.
+ *   ws            workspace of nacc_sampling_occgrid_workspace_bytes() bytes. */
+nacc_status nacc_sampling_occgrid(const nacc_grid *grid, const uint32_t *bits,
+                                  const nacc_march *params, const float *rays_o,
+                                  const float *rays_d, const float *t_min, const float *t_max,
+                                  int64_t n_rays, int64_t *packed_info, float *t0, float *t1,
+                                  int32_t *ray_id, int64_t capacity, int64_t *total,
+                                  int32_t *status_out, void *ws, size_t ws_bytes,
+                                  cudaStream_t stream);
+
+/* Writes the samples described by a packed_info produced by
+ * nacc_sampling_occgrid with the same inputs (the capacity-retry path). */
+nacc_status nacc_sampling_occgrid_fill(const nacc_grid *grid, const uint32_t *bits,
+                                       const nacc_march *params, const float *rays_o,
+                                       const float *rays_d, const float *t_min,
+                                       const float *t_max, int64_t n_rays,
+                                       const int64_t *packed_info, float *t0, float *t1,
+                                       int32_t *ray_id, void *ws, size_t ws_bytes,
+                                       cudaStream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* §4.2 "No Gradient Filtering": drop samples whose ENTERING            */
+/* transmittance T_i = exp(-Σ_{j<i} σ_j δ_j) is below ε, i.e. keep the prefix   */
+/* with S_i <= neg_log_eps (reading #9; S_i accumulated in fp64).               */
+/*   sigma         [n_samples] σ from the caller's no-grad density query        */
+/*   neg_log_eps   -ln ε computed by the caller in fp64 (+inf disables)         */
+/*   packed_info_out [n_rays][2], total out (device int64), always written;     */
+/*   t0_out, t1_out, ray_id_out [capacity] written iff total <= capacity        */
+/*   (capacity >= n_samples always suffices).                                   */
+/* ------------------------------------------------------------------------ */
+size_t nacc_filter_workspace_bytes(int64_t n_rays);
+nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, const float *t0,
+                                   const float *t1, const float *sigma, int64_t n_samples,
+                                   double neg_log_eps, int64_t *packed_info_out, float *t0_out,
+                                   float *t1_out, int32_t *ray_id_out, int64_t capacity,
+                                   int64_t *total, void *ws, size_t ws_bytes,
+                                   cudaStream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Transmittance estimator and compositing (Eq. 2, discretised as   */
+/* P:246 with the index typo read as σ(t_j), reading #11):                     */
+/*   δ_i = t1_i - t0_i, s_i = σ_i δ_i, S_i = Σ_{j<i} s_j (fp64),               */
+/*   T_i = exp(-S_i), α_i = 1 - exp(-s_i), w_i = T_i α_i (0 once S_i > -ln ε). */
+/* ------------------------------------------------------------------------ */
+/* weights/trans/alphas [n_samples] out; trans and alphas may be NULL. */
+nacc_status nacc_render_weights_fwd(const int64_t *packed_info, int64_t n_rays, const float *t0,
+                                    const float *t1, const float *sigma, int64_t n_samples,
+                                    double neg_log_eps, float *weights, float *trans,
+                                    float *alphas, cudaStream_t stream);
+/* g_sigma_i = δ_i (g_w_i T_i (1-α_i)[live] - Σ_{j>i} g_w_j w_j - Σ_{j>i} g_T_j T_j);
+ * g_trans may be NULL (= 0). */
+nacc_status nacc_render_weights_bwd(const int64_t *packed_info, int64_t n_rays, const float *t0,
+                                    const float *t1, const float *sigma, int64_t n_samples,
+                                    double neg_log_eps, const float *g_weights,
+                                    const float *g_trans, float *g_sigma, cudaStream_t stream);
+
+/* accumulate_along_rays: out[r][c] = Σ_i w_i v_i[c]; values == NULL means ones
+ * (opacity, C must be 1).  1 <= C <= 64. */
+nacc_status nacc_accumulate_along_rays(const int64_t *packed_info, int64_t n_rays,
+                                       const float *weights, const float *values, int32_t C,
+                                       int64_t n_samples, float *out, cudaStream_t stream);
+/* g_weights_i = Σ_c g_out[r][c] v_i[c]; g_values_i = w_i g_out[r] (NULL = skip). */
+nacc_status nacc_accumulate_along_rays_bwd(const int64_t *packed_info, int64_t n_rays,
+                                           const float *weights, const float *values, int32_t C,
+                                           int64_t n_samples, const float *g_out,
+                                           float *g_weights, float *g_values,
+                                           cudaStream_t stream);
+
+/* Fused render (Alg. 1 nerfacc.rendering): per ray
+ *   color = Σ w rgb, opacity = Σ w, depth = Σ w m / max(opacity, 1e-10),
+ *   m = (t0+t1)/2 (reading #12).  ctx [n_rays][5] fp64 out (may be NULL) keeps
+ *   (C_r, C_g, C_b, O, N) for the backward. */
+nacc_status nacc_render_fwd(const int64_t *packed_info, int64_t n_rays, const float *t0,
+                            const float *t1, const float *sigma, const float *rgb,
+                            int64_t n_samples, double neg_log_eps, float *color, float *opacity,
+                            float *depth, double *ctx, cudaStream_t stream);
+/* Backward of nacc_render_fwd (t detached): given upstream
+ * g_color [n][3], g_opacity [n], g_depth [n] (each may be NULL = 0), writes
+ * g_sigma [N] and g_rgb [N][3].  ctx from the forward (NULL = recompute). */
+nacc_status nacc_render_bwd(const int64_t *packed_info, int64_t n_rays, const float *t0,
+                            const float *t1, const float *sigma, const float *rgb,
+                            int64_t n_samples, double neg_log_eps, const double *ctx,
+                            const float *g_color, const float *g_opacity, const float *g_depth,
+                            float *g_sigma, float *g_rgb, cudaStream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Proposal estimator: inverse-transform resampling (Eq. 1) of the  */
+/* CDF F = 1 - T (Eq. 3, "compute the CDF directly using 1 - T(t)", */
+/* P:220) in s-space.  Per ray, edges e_0..e_m (ascending, in s) and   */
+/* either sigma [m] (F_j = 1 - exp(-Σ_{i<j} σ_i (Φ(e_{i+1}) - Φ(e_i)))) or a    */
+/* given cdf [m+1]; F̂ = F normalised to [0,1] (uniform if the mass <= 1e-12,   */
+/* reading #16).  Output edges s_i = F̂^{-1}(u_i), u_i = i/n_out (i = 0..n_out) */
+/* or stratified u_i = (i + ξ_{r,i})/(n_out+1) with ξ = Philox(seed,(r,i,1)),   */
+/* linear within each bin; t_out = Φ(s_out) (may be NULL).                      */
+/* ------------------------------------------------------------------------ */
+typedef enum { NACC_MAP_IDENTITY = 0, NACC_MAP_LINDISP = 1 } nacc_map;
+nacc_status nacc_importance_sample(int64_t n_rays, int32_t n_in, const float *s_edges,
+                                   const float *sigma, const float *cdf, nacc_map map,
+                                   double t_near, double t_far, int32_t n_out,
+                                   int32_t stratified, uint64_t seed, float *s_out, float *t_out,
+                                   cudaStream_t stream);
+
+/* ------------------------------------------------------------------------ */
+/* Occupancy-grid estimator update (EMA σ^k = γσ^{k-1} + (1-γ)σ_q,  */
+/* binarise σ̂ = 1[σ > τ]; readings #20-#23).                                  */
+/* ------------------------------------------------------------------------ */
+typedef enum { NACC_UPDATE_EMA = 0, NACC_UPDATE_MAX_DECAY = 1 } nacc_update_rule;
+typedef enum { NACC_THRESH_FIXED = 0, NACC_THRESH_MIN_MEAN = 1 } nacc_thresh_rule;
+
+/* Query points for cells [cell_begin, cell_begin+cell_count): level l, index
+ * (i,j,k): x = lo_l + (i + ξ)(hi_l - lo_l)/R in fp64, rounded once; ξ from
+ * Philox(seed, (cell_in_level, step, l, 2)) or 1/2 when jitter == 0.
+ * xyz [cell_count][3] out. */
+nacc_status nacc_occgrid_points(const nacc_grid *grid, uint64_t seed, int64_t step,
+                                int32_t jitter, int64_t cell_begin, int64_t cell_count,
+                                float *xyz, cudaStream_t stream);
+size_t nacc_occgrid_workspace_bytes(const nacc_grid *grid);
+/* density [levels*res^3] in/out (fp32 state, updated with fp64 arithmetic,
+ * rounded once); fresh [levels*res^3] = the caller's σ(x)·Δt at the points
+ * (after the MAX all-reduce across ranks); bits out; mean (device double,
+ * NULL allowed) = mean of the updated density. */
+nacc_status nacc_occgrid_update(const nacc_grid *grid, float *density, const float *fresh,
+                                nacc_update_rule rule, float decay, float threshold,
+                                nacc_thresh_rule thresh_rule, uint32_t *bits, double *mean,
+                                void *ws, size_t ws_bytes, cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NACC_H */

@@ -1,0 +1,376 @@
+"""Thin PyTorch binding of libnacc (include/nacc.h), named after Algorithm 1
+of the paper.  Argument marshalling only: every step of the path
+runs in the library's CUDA kernels; torch provides device memory, streams and
+the process group.  Non-CUDA tensors are rejected (no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+from typing import Callable, Optional
+
+import torch
+
+from . import _lib as L
+from ._lib import check
+
+NEG_LOG_EPS_DEFAULT = -math.log(float(torch.tensor(1e-4, dtype=torch.float32)))  # P:86, ε = 1e-4 (fp32)
+
+
+def neg_log_eps(eps: Optional[float]) -> float:
+    """-ln ε in fp64 on the host (reading #9); None or 0 disables early stop."""
+    if eps is None or eps <= 0.0:
+        return math.inf
+    return -math.log(float(torch.tensor(eps, dtype=torch.float32)))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _req(t: torch.Tensor, dtype, name: str, numel: Optional[int] = None) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (there is no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        t = t.contiguous()
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} must have {numel} elements, got {t.numel()}")
+    return t
+
+
+def _ws(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=device)
+
+
+# ----------------------------------------------------------------------------- specs
+@dataclasses.dataclass
+class GridSpec:
+    """Occupancy grid: `levels` cascaded boxes centre ± half·2^l of
+    `roi`, `res`^3 cells each (reading #4)."""
+    roi: tuple = (0.0, 0.0, 0.0, 1.0, 1.0, 1.0)
+    res: int = 128
+    levels: int = 1
+
+    def c(self) -> L.Grid:
+        g = L.Grid()
+        g.levels, g.res = int(self.levels), int(self.res)
+        for i in range(6):
+            g.roi[i] = float(self.roi[i])
+        return g
+
+    @property
+    def n_cells(self) -> int:
+        return self.levels * self.res ** 3
+
+
+@dataclasses.dataclass
+class MarchParams:
+    """Ray-marching parameters (readings #1, #5)."""
+    step: float
+    near_plane: float = 0.0
+    far_plane: float = 1e10
+    max_step: float = 1e10
+    cone_angle: float = 0.0
+    stratified: bool = False
+    seed: int = 0
+
+    def c(self) -> L.March:
+        m = L.March()
+        m.near_plane, m.far_plane, m.step = self.near_plane, self.far_plane, self.step
+        m.max_step, m.cone_angle = self.max_step, self.cone_angle
+        m.stratified, m.seed = int(bool(self.stratified)), int(self.seed)
+        return m
+
+
+@dataclasses.dataclass
+class PackedSamples:
+    """Sample-as-interval packed tensor: t0, t1 fp32 [N], ray_id
+    int32 [N], packed_info int64 [n_rays, 2] = (start, count)."""
+    packed_info: torch.Tensor
+    t0: torch.Tensor
+    t1: torch.Tensor
+    ray_id: torch.Tensor
+
+    @property
+    def n_rays(self) -> int:
+        return self.packed_info.shape[0]
+
+    @property
+    def n_samples(self) -> int:
+        return self.t0.numel()
+
+
+# ----------------------------------------------------------------------------- sampling
+def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec, bits: torch.Tensor,
+                     params: MarchParams, t_min: Optional[torch.Tensor] = None,
+                     t_max: Optional[torch.Tensor] = None, capacity: Optional[int] = None) -> PackedSamples:
+    """Alg. 1 ``nerfacc.sampling`` with the occupancy-grid estimator.
+    ``capacity`` (optional) enables the one-shot count+scan+fill; the exact
+    path (count+scan, read the total, fill) is used otherwise or on overflow."""
+    lib = L.lib()
+    n = rays_o.shape[0]
+    dev = rays_o.device
+    rays_o = _req(rays_o, torch.float32, "rays_o", 3 * n)
+    rays_d = _req(rays_d, torch.float32, "rays_d", 3 * n)
+    bits = _req(bits, torch.int32, "bits")
+    if t_min is not None:
+        t_min = _req(t_min, torch.float32, "t_min", n)
+    if t_max is not None:
+        t_max = _req(t_max, torch.float32, "t_max", n)
+    g, p = grid.c(), params.c()
+    ws = _ws(lib.nacc_sampling_occgrid_workspace_bytes(C.byref(g), C.byref(p), n), dev)
+    packed = torch.empty((n, 2), dtype=torch.int64, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    cap = int(capacity) if capacity is not None else 0
+    t0 = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+    t1 = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+    rid = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    with_out = cap > 0
+    check(lib.nacc_sampling_occgrid(C.byref(g), _ptr(bits), C.byref(p), _ptr(rays_o), _ptr(rays_d), _ptr(t_min),
+                                    _ptr(t_max), n, _ptr(packed), _ptr(t0) if with_out else None,
+                                    _ptr(t1) if with_out else None, _ptr(rid) if with_out else None, cap,
+                                    _ptr(total), None, _ptr(ws), ws.numel(), _stream()), "nacc_sampling_occgrid")
+    N = int(total.item())
+    if N > cap:
+        t0 = torch.empty(max(N, 1), dtype=torch.float32, device=dev)
+        t1 = torch.empty(max(N, 1), dtype=torch.float32, device=dev)
+        rid = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
+        check(lib.nacc_sampling_occgrid_fill(C.byref(g), _ptr(bits), C.byref(p), _ptr(rays_o), _ptr(rays_d),
+                                             _ptr(t_min), _ptr(t_max), n, _ptr(packed), _ptr(t0), _ptr(t1),
+                                             _ptr(rid), _ptr(ws), ws.numel(), _stream()),
+              "nacc_sampling_occgrid_fill")
+    return PackedSamples(packed, t0[:N], t1[:N], rid[:N])
+
+
+def filter_early_stop(samples: PackedSamples, sigma: torch.Tensor, eps: Optional[float] = 1e-4) -> PackedSamples:
+    """§4.2 no-gradient filtering: keep each ray's prefix with entering
+    transmittance >= ε.  ``sigma`` comes from the caller's no-grad density query."""
+    lib = L.lib()
+    n, N = samples.n_rays, samples.n_samples
+    dev = samples.packed_info.device
+    sigma = _req(sigma.detach(), torch.float32, "sigma", N)
+    ws = _ws(lib.nacc_filter_workspace_bytes(n), dev)
+    packed = torch.empty((n, 2), dtype=torch.int64, device=dev)
+    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    cap = max(N, 1)
+    t0 = torch.empty(cap, dtype=torch.float32, device=dev)
+    t1 = torch.empty(cap, dtype=torch.float32, device=dev)
+    rid = torch.empty(cap, dtype=torch.int32, device=dev)
+    check(lib.nacc_filter_early_stop(_ptr(samples.packed_info), n, _ptr(samples.t0), _ptr(samples.t1), _ptr(sigma),
+                                     N, neg_log_eps(eps), _ptr(packed), _ptr(t0), _ptr(t1), _ptr(rid), cap,
+                                     _ptr(total), _ptr(ws), ws.numel(), _stream()), "nacc_filter_early_stop")
+    M = int(total.item())
+    return PackedSamples(packed, t0[:M], t1[:M], rid[:M])
+
+
+# ----------------------------------------------------------------------------- rendering
+class _RenderFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, packed_info, t0, t1, sigma, rgb, nle):
+        n, N = packed_info.shape[0], t0.numel()
+        dev = t0.device
+        color = torch.empty((n, 3), dtype=torch.float32, device=dev)
+        opacity = torch.empty(n, dtype=torch.float32, device=dev)
+        depth = torch.empty(n, dtype=torch.float32, device=dev)
+        cx = torch.empty((n, 5), dtype=torch.float64, device=dev)
+        check(L.lib().nacc_render_fwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), _ptr(rgb), N, nle,
+                                      _ptr(color), _ptr(opacity), _ptr(depth), _ptr(cx), _stream()),
+              "nacc_render_fwd")
+        ctx.save_for_backward(packed_info, t0, t1, sigma, rgb, cx)
+        ctx.nle = nle
+        return color, opacity, depth
+
+    @staticmethod
+    def backward(ctx, g_color, g_opacity, g_depth):
+        packed_info, t0, t1, sigma, rgb, cx = ctx.saved_tensors
+        n, N = packed_info.shape[0], t0.numel()
+        g_sigma = torch.empty_like(sigma)
+        g_rgb = torch.empty_like(rgb)
+        gc = None if g_color is None else g_color.contiguous().float()
+        go = None if g_opacity is None else g_opacity.contiguous().float()
+        gd = None if g_depth is None else g_depth.contiguous().float()
+        check(L.lib().nacc_render_bwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), _ptr(rgb), N, ctx.nle,
+                                      _ptr(cx), _ptr(gc), _ptr(go), _ptr(gd), _ptr(g_sigma), _ptr(g_rgb),
+                                      _stream()), "nacc_render_bwd")
+        return None, None, None, g_sigma, g_rgb, None
+
+
+def rendering(samples: PackedSamples, sigma: torch.Tensor, rgb: torch.Tensor, eps: Optional[float] = None):
+    """Alg. 1 ``nerfacc.rendering`` on caller-evaluated σ and rgb:
+    returns (color [n,3], opacity [n], depth [n]), differentiable w.r.t. σ and rgb."""
+    N = samples.n_samples
+    sigma = _req(sigma, torch.float32, "sigma", N)
+    rgb = _req(rgb, torch.float32, "rgb", 3 * N)
+    return _RenderFn.apply(samples.packed_info, samples.t0, samples.t1, sigma, rgb.view(N, 3), neg_log_eps(eps))
+
+
+class _WeightsFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, packed_info, t0, t1, sigma, nle):
+        n, N = packed_info.shape[0], t0.numel()
+        w = torch.empty_like(sigma)
+        T = torch.empty_like(sigma)
+        a = torch.empty_like(sigma)
+        check(L.lib().nacc_render_weights_fwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, nle,
+                                              _ptr(w), _ptr(T), _ptr(a), _stream()), "nacc_render_weights_fwd")
+        ctx.save_for_backward(packed_info, t0, t1, sigma)
+        ctx.nle = nle
+        ctx.mark_non_differentiable(a)
+        return w, T, a
+
+    @staticmethod
+    def backward(ctx, g_w, g_T, g_a):
+        packed_info, t0, t1, sigma = ctx.saved_tensors
+        n, N = packed_info.shape[0], t0.numel()
+        g_sigma = torch.empty_like(sigma)
+        gw = torch.zeros_like(sigma) if g_w is None else g_w.contiguous().float()
+        gT = None if g_T is None else g_T.contiguous().float()
+        check(L.lib().nacc_render_weights_bwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, ctx.nle,
+                                              _ptr(gw), _ptr(gT), _ptr(g_sigma), _stream()),
+              "nacc_render_weights_bwd")
+        return None, None, None, g_sigma, None
+
+
+def render_weights(samples: PackedSamples, sigma: torch.Tensor, eps: Optional[float] = None):
+    """Transmittance estimator (Eq. 2): returns (weights, trans, alphas) per sample."""
+    sigma = _req(sigma, torch.float32, "sigma", samples.n_samples)
+    return _WeightsFn.apply(samples.packed_info, samples.t0, samples.t1, sigma, neg_log_eps(eps))
+
+
+class _AccumFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, packed_info, weights, values, C_):
+        n, N = packed_info.shape[0], weights.numel()
+        out = torch.empty((n, C_), dtype=torch.float32, device=weights.device)
+        check(L.lib().nacc_accumulate_along_rays(_ptr(packed_info), n, _ptr(weights), _ptr(values), C_, N, _ptr(out),
+                                                 _stream()), "nacc_accumulate_along_rays")
+        ctx.save_for_backward(packed_info, weights, values)
+        ctx.C = C_
+        ctx.has_values = values is not None
+        return out
+
+    @staticmethod
+    def backward(ctx, g_out):
+        packed_info, weights, values = ctx.saved_tensors
+        n, N = packed_info.shape[0], weights.numel()
+        g_w = torch.empty_like(weights)
+        g_v = torch.empty_like(values) if ctx.has_values else None
+        g_out = g_out.contiguous().float()
+        check(L.lib().nacc_accumulate_along_rays_bwd(_ptr(packed_info), n, _ptr(weights),
+                                                     _ptr(values if ctx.has_values else None), ctx.C, N,
+                                                     _ptr(g_out), _ptr(g_w), _ptr(g_v), _stream()),
+              "nacc_accumulate_along_rays_bwd")
+        return None, g_w, g_v, None
+
+
+def accumulate_along_rays(samples: PackedSamples, weights: torch.Tensor, values: Optional[torch.Tensor] = None):
+    """Segmented sums out[r] = Σ_i w_i v_i (values None = ones, i.e. opacity)."""
+    N = samples.n_samples
+    weights = _req(weights, torch.float32, "weights", N)
+    if values is None:
+        return _AccumFn.apply(samples.packed_info, weights, None, 1)
+    values = _req(values, torch.float32, "values")
+    C_ = values.numel() // max(N, 1) if N else (values.shape[-1] if values.dim() > 1 else 1)
+    return _AccumFn.apply(samples.packed_info, weights, values.view(N, C_) if N else values, C_)
+
+
+# ----------------------------------------------------------------------------- proposal resampling
+MAP_IDENTITY, MAP_LINDISP = 0, 1
+
+
+def importance_sample(s_edges: torch.Tensor, n_out: int, sigma: Optional[torch.Tensor] = None,
+                      cdf: Optional[torch.Tensor] = None, map_kind: int = MAP_LINDISP, t_near: float = 0.2,
+                      t_far: float = 1000.0, stratified: bool = False, seed: int = 0):
+    """Inverse-CDF resampling of interval edges (Eq. 1 + Eq. 3; s-space
+    P:257).  s_edges [n, m+1]; returns (s_out, t_out) [n, n_out+1]."""
+    n, m1 = s_edges.shape
+    s_edges = _req(s_edges, torch.float32, "s_edges")
+    if sigma is not None:
+        sigma = _req(sigma.detach(), torch.float32, "sigma", n * (m1 - 1))
+    if cdf is not None:
+        cdf = _req(cdf.detach(), torch.float32, "cdf", n * m1)
+    s_out = torch.empty((n, n_out + 1), dtype=torch.float32, device=s_edges.device)
+    t_out = torch.empty_like(s_out)
+    check(L.lib().nacc_importance_sample(n, m1 - 1, _ptr(s_edges), _ptr(sigma), _ptr(cdf), int(map_kind),
+                                         float(t_near), float(t_far), int(n_out), int(bool(stratified)), int(seed),
+                                         _ptr(s_out), _ptr(t_out), _stream()), "nacc_importance_sample")
+    return s_out, t_out
+
+
+# ----------------------------------------------------------------------------- occupancy grid
+def owner_slab(n_cells: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous owner slab of cells for `rank` (reading #25)."""
+    return n_cells * rank // world, n_cells * (rank + 1) // world
+
+
+class OccupancyGrid:
+    """The occupancy-grid transmittance estimator (P:240-241, P:26 ``nerfacc.
+    TransmittanceEstimator``): fp32 cached density + public bitfield, updated
+    with EMA (or max-decay) every n steps."""
+
+    def __init__(self, spec: GridSpec, device="cuda", decay: float = 0.95, threshold: float = 0.01,
+                 rule: int = 0, thresh_rule: int = 0, seed: int = 0):
+        self.spec = spec
+        self.device = torch.device(device)
+        self.density = torch.zeros(spec.n_cells, dtype=torch.float32, device=self.device)
+        nb = L.lib().nacc_grid_bits_bytes(C.byref(spec.c()))
+        self.bits = torch.zeros(nb // 4, dtype=torch.int32, device=self.device)
+        self.decay, self.threshold, self.rule, self.thresh_rule, self.seed = decay, threshold, rule, thresh_rule, seed
+        self.mean = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self._ws = _ws(L.lib().nacc_occgrid_workspace_bytes(C.byref(spec.c())), self.device)
+
+    def points(self, step: int, jitter: bool = True, cell_begin: int = 0, cell_count: Optional[int] = None):
+        if cell_count is None:
+            cell_count = self.spec.n_cells - cell_begin
+        xyz = torch.empty((cell_count, 3), dtype=torch.float32, device=self.device)
+        g = self.spec.c()
+        check(L.lib().nacc_occgrid_points(C.byref(g), self.seed, int(step), int(bool(jitter)), int(cell_begin),
+                                          int(cell_count), _ptr(xyz), _stream()), "nacc_occgrid_points")
+        return xyz
+
+    def update(self, fresh: torch.Tensor):
+        fresh = _req(fresh, torch.float32, "fresh", self.spec.n_cells)
+        g = self.spec.c()
+        check(L.lib().nacc_occgrid_update(C.byref(g), _ptr(self.density), _ptr(fresh), int(self.rule),
+                                          float(self.decay), float(self.threshold), int(self.thresh_rule),
+                                          _ptr(self.bits), _ptr(self.mean), _ptr(self._ws), self._ws.numel(),
+                                          _stream()), "nacc_occgrid_update")
+
+    def update_every_n_steps(self, step: int, occ_eval_fn: Callable[[torch.Tensor], torch.Tensor], n: int = 16,
+                             jitter: bool = True, process_group=None) -> bool:
+        """Alg. 1 ``estimator.update_every_n_steps``: every n steps,
+        owner-computes the fresh values σ(x)·Δt on this rank's cell slab,
+        merges them with a MAX all-reduce over the process group (the path's
+        one collective; non-owners contribute 0 since σ >= 0) and applies
+        the identical update on every rank."""
+        if step % n != 0:
+            return False
+        world, rank = 1, 0
+        if process_group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
+            world = torch.distributed.get_world_size(process_group)
+            rank = torch.distributed.get_rank(process_group)
+        C_ = self.spec.n_cells
+        lo, hi = owner_slab(C_, rank, world)
+        fresh = torch.zeros(C_, dtype=torch.float32, device=self.device)
+        if hi > lo:
+            xyz = self.points(step, jitter, lo, hi - lo)
+            fresh[lo:hi] = occ_eval_fn(xyz).reshape(-1).float()
+        if world > 1:
+            torch.distributed.all_reduce(fresh, op=torch.distributed.ReduceOp.MAX, group=process_group)
+        self.update(fresh)
+        return True
+
+    def state_dict(self):
+        return {"density": self.density.clone(), "spec": dataclasses.asdict(self.spec), "decay": self.decay,
+                "threshold": self.threshold, "rule": self.rule, "thresh_rule": self.thresh_rule, "seed": self.seed}
+
+
+def launch_count() -> int:
+    return int(L.lib().nacc_launch_count())

@@ -1,0 +1,116 @@
+// common.cuh — shared device helpers of libnacc (sm_100a).  Product code:
+// nothing here is shared with oracle/ (which is plain C with its own Philox).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cmath>
+#include <string>
+
+#include "nacc.h"
+
+namespace nacc {
+
+// ---------------------------------------------------------------- error state
+void set_error(const std::string &msg);
+void clear_error();
+void count_launch(int n = 1);
+
+#define NACC_REQUIRE(cond, msg)                                   \
+  do {                                                            \
+    if (!(cond)) {                                                \
+      ::nacc::set_error(std::string(__func__) + ": " + (msg));     \
+      return NACC_ERR_INVALID_ARGUMENT;                           \
+    }                                                             \
+  } while (0)
+
+#define NACC_CHECK_LAUNCH()                                                        \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess) {                                                       \
+      ::nacc::set_error(std::string(__func__) + ": " + cudaGetErrorString(e_));     \
+      return NACC_ERR_CUDA;                                                        \
+    }                                                                              \
+  } while (0)
+
+#define NACC_CUDA(call)                                                            \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      ::nacc::set_error(std::string(__func__) + ": " + cudaGetErrorString(e_));     \
+      return NACC_ERR_CUDA;                                                        \
+    }                                                                              \
+  } while (0)
+
+inline bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------- Philox4x32-10
+struct u32x4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = u32x4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+// 24-bit uniform in [0,1) as an exact double
+__device__ __forceinline__ double u24(uint32_t x) { return (double)(x >> 8) * (1.0 / 16777216.0); }
+
+// ---------------------------------------------------------------- warp scans
+__device__ __forceinline__ double warp_incl_scan(double v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double n = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_sumf(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+__device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t n = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
+}
+
+// ---------------------------------------------------------------- launch helpers
+inline int grid_for(int64_t work_items, int per_block, int64_t cap = (1ll << 31) - 1) {
+  int64_t g = ceil_div(work_items, per_block);
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+// exclusive scan of int32 counts -> packed_info (start, count) and *total.
+// Workspace: scan_workspace_bytes(n).  Launches 3 kernels (2 if n small).
+size_t scan_workspace_bytes(int64_t n);
+cudaError_t scan_counts_to_packed(const int32_t *counts, int64_t n, int64_t *packed_info,
+                                  int64_t *total, void *ws, cudaStream_t stream);
+
+}  // namespace nacc

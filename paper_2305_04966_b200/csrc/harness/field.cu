@@ -1,0 +1,124 @@
+// field.cu — bench/test harness: the synthetic stand-in for the user's NeRF
+// (Alg. 1 density_fn / rgb_density_fn).  Not part of libnacc.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "nacc_harness.h"
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+
+__device__ __forceinline__ float4 lattice_at(const float4 *__restrict__ lat, int R, float lo, float hi, int contracted,
+                                             float x, float y, float z) {
+  if (contracted) {
+    const float n = sqrtf(x * x + y * y + z * z);
+    if (n > 1.0f) {
+      const float s = (2.0f - 1.0f / n) / n;
+      x *= s;
+      y *= s;
+      z *= s;
+    }
+  }
+  if (!(x >= lo && x <= hi && y >= lo && y <= hi && z >= lo && z <= hi)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const float sc = (float)R / (hi - lo);
+  float u[3] = {(x - lo) * sc - 0.5f, (y - lo) * sc - 0.5f, (z - lo) * sc - 0.5f};
+  int i0[3];
+  float f[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    u[a] = fminf(fmaxf(u[a], 0.0f), (float)(R - 1));
+    i0[a] = min((int)floorf(u[a]), R - 2);
+    f[a] = u[a] - (float)i0[a];
+  }
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+    const float w = (dx ? f[0] : 1.f - f[0]) * (dy ? f[1] : 1.f - f[1]) * (dz ? f[2] : 1.f - f[2]);
+    const float4 v = __ldg(lat + (i0[0] + dx) + R * ((i0[1] + dy) + R * (i0[2] + dz)));
+    acc.x += w * v.x;
+    acc.y += w * v.y;
+    acc.z += w * v.z;
+    acc.w += w * v.w;
+  }
+  return acc;
+}
+
+__global__ void field_samples_kernel(const float4 *__restrict__ lat, int R, float lo, float hi, int contracted,
+                                     const float *__restrict__ o, const float *__restrict__ d,
+                                     const float *__restrict__ t0, const float *__restrict__ t1,
+                                     const int32_t *__restrict__ rid, int64_t n, float *__restrict__ sigma,
+                                     float *__restrict__ rgb) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = __ldg(rid + i);
+  const float m = 0.5f * (__ldg(t0 + i) + __ldg(t1 + i));
+  const float x = __ldg(o + 3 * r) + m * __ldg(d + 3 * r);
+  const float y = __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1);
+  const float z = __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2);
+  const float4 v = lattice_at(lat, R, lo, hi, contracted, x, y, z);
+  sigma[i] = v.x;
+  if (rgb) {
+    rgb[3 * i] = v.y;
+    rgb[3 * i + 1] = v.z;
+    rgb[3 * i + 2] = v.w;
+  }
+}
+
+__global__ void field_points_kernel(const float4 *__restrict__ lat, int R, float lo, float hi, int contracted,
+                                    const float *__restrict__ xyz, int64_t n, float scale, float *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 v = lattice_at(lat, R, lo, hi, contracted, xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+  out[i] = scale * v.x;
+}
+
+__global__ void mse_grad_kernel(const float *__restrict__ c, const float *__restrict__ gt, int64_t n3, float k,
+                                float *__restrict__ g) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n3) g[i] = k * (c[i] - gt[i]);
+}
+
+inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }
+}  // namespace
+
+extern "C" {
+
+nacc_status naccx_field_at_samples(const float *lattice, int32_t res, float lo, float hi, int32_t contracted,
+                                   const float *rays_o, const float *rays_d, const float *t0, const float *t1,
+                                   const int32_t *ray_id, int64_t n, float *sigma, float *rgb, cudaStream_t stream) {
+  if (n < 0 || res < 2 || !(hi > lo)) return NACC_ERR_INVALID_ARGUMENT;
+  if (n == 0) return NACC_OK;
+  if (!lattice || !rays_o || !rays_d || !t0 || !t1 || !ray_id || !sigma) return NACC_ERR_INVALID_ARGUMENT;
+  field_samples_kernel<<<blocks_for(n), 256, 0, stream>>>(reinterpret_cast<const float4 *>(lattice), res, lo, hi,
+                                                          contracted, rays_o, rays_d, t0, t1, ray_id, n, sigma, rgb);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
+}
+
+nacc_status naccx_field_at_points(const float *lattice, int32_t res, float lo, float hi, int32_t contracted,
+                                  const float *xyz, int64_t n, float scale, float *out, cudaStream_t stream) {
+  if (n < 0 || res < 2 || !(hi > lo)) return NACC_ERR_INVALID_ARGUMENT;
+  if (n == 0) return NACC_OK;
+  if (!lattice || !xyz || !out) return NACC_ERR_INVALID_ARGUMENT;
+  field_points_kernel<<<blocks_for(n), 256, 0, stream>>>(reinterpret_cast<const float4 *>(lattice), res, lo, hi,
+                                                         contracted, xyz, n, scale, out);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
+}
+
+nacc_status naccx_mse_grad(const float *color, const float *gt, int64_t n_rays, float *g_color, cudaStream_t stream) {
+  if (n_rays < 0) return NACC_ERR_INVALID_ARGUMENT;
+  if (n_rays == 0) return NACC_OK;
+  if (!color || !gt || !g_color) return NACC_ERR_INVALID_ARGUMENT;
+  mse_grad_kernel<<<blocks_for(3 * n_rays), 256, 0, stream>>>(color, gt, 3 * n_rays, 2.0f / (3.0f * (float)n_rays),
+                                                              g_color);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
+}
+
+uint64_t naccx_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+// resample.cu — the proposal estimator's inverse-transform sampling
+// (Eq. 1) of the CDF F = 1 - T (Eq. 3; "compute
+// the CDF directly using 1 - T(t)"), piecewise linear in s (P:257,
+// readings #16-#19).  One warp per ray; the ray's normalised CDF lives in
+// shared memory, each lane inverts 1/32 of the output edges by binary search.
+#include "common.cuh"
+
+namespace nacc {
+
+__device__ __forceinline__ double phi(int map, double s, double tn, double inv_tn, double inv_tf, double tf) {
+  if (map == NACC_MAP_IDENTITY) return tn + s * (tf - tn);
+  return 1.0 / ((1.0 - s) * inv_tn + s * inv_tf);
+}
+
+constexpr int kResampleWarps = 4;
+
+__global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
+    int64_t n_rays, int n_in, const float *__restrict__ s_edges, const float *__restrict__ sigma,
+    const float *__restrict__ cdf, int map, double tn, double tf, int n_out, int stratified, uint32_t key0,
+    uint32_t key1, float *__restrict__ s_out, float *__restrict__ t_out) {
+  extern __shared__ float smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * kResampleWarps + warp;
+  if (r >= n_rays) return;
+  float *e = smem + (size_t)warp * 2 * (n_in + 1);
+  float *F = e + (n_in + 1);
+  const double inv_tn = 1.0 / tn, inv_tf = isinf(tf) ? 0.0 : 1.0 / tf;
+  const float *er = s_edges + r * (int64_t)(n_in + 1);
+  for (int j = lane; j <= n_in; j += 32) e[j] = __ldg(er + j);
+  __syncwarp();
+  bool uniform = false;
+  if (sigma) {
+    const float *sr = sigma + r * (int64_t)n_in;
+    double carry = 0.0;
+    for (int base = 0; base < n_in; base += 32) {
+      const int j = base + lane;
+      double s = 0.0;
+      if (j < n_in) {
+        const double ta = phi(map, (double)e[j], tn, inv_tn, inv_tf, tf);
+        const double tb = phi(map, (double)e[j + 1], tn, inv_tn, inv_tf, tf);
+        s = (double)__ldg(sr + j) * (tb - ta);
+      }
+      const double incl = warp_incl_scan(s);
+      if (j < n_in) F[j + 1] = -expm1f(-(float)(carry + incl));
+      carry += __shfl_sync(kFull, incl, 31);
+    }
+    if (lane == 0) F[0] = 0.f;
+    uniform = !(-expm1(-carry) > 1e-12);
+    __syncwarp();
+    if (!uniform) {
+      const float Fm = F[n_in];
+      for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(F[j], Fm);
+    }
+  } else {
+    const float *cr = cdf + r * (int64_t)(n_in + 1);
+    const float c0 = __ldg(cr), cm = __ldg(cr + n_in);
+    uniform = !((double)cm - (double)c0 > 1e-12);
+    if (!uniform) {
+      const float den = __fsub_rn(cm, c0);
+      for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(__fsub_rn(__ldg(cr + j), c0), den);
+    }
+  }
+  if (uniform) {
+    const float e0 = e[0], den = __fsub_rn(e[n_in], e0);
+    for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(__fsub_rn(e[j], e0), den);
+  }
+  __syncwarp();
+  float *so = s_out + r * (int64_t)(n_out + 1);
+  float *to = t_out ? t_out + r * (int64_t)(n_out + 1) : nullptr;
+  for (int i = lane; i <= n_out; i += 32) {
+    double u;
+    if (stratified) {
+      const u32x4 rnd = philox4x32_10(u32x4{(uint32_t)(uint64_t)r, (uint32_t)((uint64_t)r >> 32), (uint32_t)i, 1u},
+                                      key0, key1);
+      u = ((double)i + u24(rnd.x)) / (double)(n_out + 1);
+    } else {
+      u = (double)i / (double)n_out;
+    }
+    double s;
+    if (u >= 1.0) {
+      // smallest j in [0, n_in-1] with F[j+1] >= 1
+      int lo = 0, hi = n_in - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (F[mid + 1] >= 1.0f) hi = mid;
+        else lo = mid + 1;
+      }
+      s = (double)e[lo + 1];
+    } else {
+      // largest j in [0, n_in-1] with F[j] <= u
+      int lo = 0, hi = n_in - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((double)F[mid] <= u) lo = mid;
+        else hi = mid - 1;
+      }
+      const double Fj = (double)F[lo], Fj1 = (double)F[lo + 1];
+      const double ej = (double)e[lo], ej1 = (double)e[lo + 1];
+      s = ej + (u - Fj) / (Fj1 - Fj) * (ej1 - ej);
+    }
+    so[i] = (float)s;
+    if (to) to[i] = (float)phi(map, s, tn, inv_tn, inv_tf, tf);
+  }
+}
+
+}  // namespace nacc
+
+using namespace nacc;
+
+extern "C" {
+
+nacc_status nacc_importance_sample(int64_t n_rays, int32_t n_in, const float *s_edges, const float *sigma,
+                                   const float *cdf, nacc_map map, double t_near, double t_far, int32_t n_out,
+                                   int32_t stratified, uint64_t seed, float *s_out, float *t_out,
+                                   cudaStream_t stream) {
+  clear_error();
+  NACC_REQUIRE(n_rays >= 0, "n_rays must be >= 0");
+  NACC_REQUIRE(n_in >= 1 && n_out >= 1, "n_in and n_out must be >= 1");
+  NACC_REQUIRE((sigma != nullptr) != (cdf != nullptr), "exactly one of sigma / cdf must be non-NULL");
+  NACC_REQUIRE(map == NACC_MAP_IDENTITY || map == NACC_MAP_LINDISP, "unknown map");
+  NACC_REQUIRE(std::isfinite(t_near) && t_near > 0.0 && t_far > t_near, "need 0 < t_near < t_far");
+  NACC_REQUIRE(map == NACC_MAP_LINDISP || std::isfinite(t_far), "identity map needs a finite t_far");
+  if (n_rays == 0) return NACC_OK;
+  NACC_REQUIRE(s_edges && s_out, "s_edges and s_out must be non-NULL");
+  const size_t smem = (size_t)kResampleWarps * 2 * (n_in + 1) * sizeof(float);
+  if (smem > 227 * 1024) {
+    set_error("nacc_importance_sample: n_in too large for shared memory");
+    return NACC_ERR_UNSUPPORTED;
+  }
+  if (smem > 48 * 1024)
+    NACC_CUDA(cudaFuncSetAttribute(importance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  importance_kernel<<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
+      n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, n_out, stratified, (uint32_t)(seed & 0xffffffffu),
+      (uint32_t)(seed >> 32), s_out, t_out);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+"""Bench/test harness bindings (include/nacc_harness.h): the synthetic stand-in
+for the user's NeRF (Alg. 1 density_fn / rgb_density_fn) and the MSE
+gradient of Alg. 1 line 48.  Not part of the product path."""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+from .api import _ptr, _req, _stream
+
+
+class LatticeField:
+    """Dense cell-centre lattice (σ, r, g, b) over [lo, hi]^3, trilinear
+    (S:121-126), optionally queried through the scene contraction."""
+
+    def __init__(self, data: torch.Tensor, lo: float, hi: float, contracted: bool = False):
+        self.data = _req(data.float(), torch.float32, "lattice")
+        self.res = int(round((self.data.numel() // 4) ** (1.0 / 3.0)))
+        assert self.res ** 3 * 4 == self.data.numel()
+        self.lo, self.hi, self.contracted = float(lo), float(hi), int(bool(contracted))
+
+    def at_samples(self, rays_o, rays_d, t0, t1, ray_id, want_rgb=True):
+        n = t0.numel()
+        sigma = torch.empty(n, dtype=torch.float32, device=t0.device)
+        rgb = torch.empty((n, 3), dtype=torch.float32, device=t0.device) if want_rgb else None
+        st = L.harness().naccx_field_at_samples(_ptr(self.data), self.res, self.lo, self.hi, self.contracted,
+                                                _ptr(rays_o), _ptr(rays_d), _ptr(t0), _ptr(t1), _ptr(ray_id), n,
+                                                _ptr(sigma), _ptr(rgb), _stream())
+        if st != 0:
+            raise L.NaccError(st, "naccx_field_at_samples")
+        return sigma, rgb
+
+    def at_points(self, xyz, scale=1.0):
+        n = xyz.shape[0]
+        out = torch.empty(n, dtype=torch.float32, device=xyz.device)
+        st = L.harness().naccx_field_at_points(_ptr(self.data), self.res, self.lo, self.hi, self.contracted,
+                                               _ptr(xyz), n, float(scale), _ptr(out), _stream())
+        if st != 0:
+            raise L.NaccError(st, "naccx_field_at_points")
+        return out
+
+
+def mse_grad(color: torch.Tensor, gt: torch.Tensor) -> torch.Tensor:
+    n = color.shape[0]
+    g = torch.empty_like(color)
+    st = L.harness().naccx_mse_grad(_ptr(color), _ptr(gt), n, _ptr(g), _stream())
+    if st != 0:
+        raise L.NaccError(st, "naccx_mse_grad")
+    return g
+
+
+def launch_count() -> int:
+    return int(L.harness().naccx_launch_count())

@@ -1,0 +1,118 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol that
+include/nacc.h declares, and host-side validation rejects bad arguments
+before any launch (no GPU needed)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(naccx?_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2305_04966_b200 import _lib as L
+
+    return L.lib()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_2305_04966_b200 import _lib as L
+
+    names = declared("nacc.h")
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in L.SIGNATURES, f"binding lacks {n}"
+    hnames = declared("nacc_harness.h")
+    h = L.harness()
+    for n in hnames:
+        assert hasattr(h, n), n
+
+
+def test_exports_are_exactly_the_abi(lib):
+    """No stray C symbols: every exported nacc_* function is declared."""
+    import subprocess
+
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_2305_04966_b200", "libnacc.so")],
+                         capture_output=True, text=True).stdout
+    exported = sorted(set(re.findall(r"\bT (nacc_[a-z0-9_]+)\b", out)))
+    assert exported == declared("nacc.h")
+
+
+def test_version_and_sizes(lib):
+    from paper_2305_04966_b200 import GridSpec, MarchParams
+
+    assert lib.nacc_abi_version() == 1
+    g = GridSpec(res=128, levels=4).c()
+    assert lib.nacc_grid_bits_bytes(C.byref(g)) == 4 * 128**3 // 8
+    g.levels = 0
+    assert lib.nacc_grid_bits_bytes(C.byref(g)) == 0
+    g = GridSpec(res=128).c()
+    p = MarchParams(step=0.01).c()
+    assert lib.nacc_sampling_occgrid_workspace_bytes(C.byref(g), C.byref(p), 1 << 18) >= 4 << 18
+    assert lib.nacc_filter_workspace_bytes(1000) >= 4000
+
+
+def test_host_validation_rejects_before_launch(lib):
+    """Invalid arguments return NACC_ERR_INVALID_ARGUMENT and set the thread-local message."""
+    from paper_2305_04966_b200 import GridSpec, MarchParams
+
+    g = GridSpec(res=16).c()
+    bad_steps = [MarchParams(step=0.0), MarchParams(step=float("nan")), MarchParams(step=0.01, cone_angle=-1.0)]
+    fake = C.c_void_p(4096)
+    for p in bad_steps:
+        pc = p.c()
+        st = lib.nacc_sampling_occgrid(C.byref(g), fake, C.byref(pc), fake, fake, None, None, 10, fake, None, None,
+                                       None, 0, fake, None, fake, 1 << 20, None)
+        assert st == 1
+        assert b"step" in lib.nacc_last_error() or b"cone" in lib.nacc_last_error()
+    gl = GridSpec(res=16, levels=9).c()
+    pc = MarchParams(step=0.01).c()
+    st = lib.nacc_sampling_occgrid(C.byref(gl), fake, C.byref(pc), fake, fake, None, None, 10, fake, None, None, None,
+                                   0, fake, None, fake, 1 << 20, None)
+    assert st == 1 and b"levels" in lib.nacc_last_error()
+    # workspace too small
+    st = lib.nacc_sampling_occgrid(C.byref(g), fake, C.byref(pc), fake, fake, None, None, 10, fake, None, None, None,
+                                   0, fake, None, fake, 8, None)
+    assert st == 1 and b"workspace" in lib.nacc_last_error()
+    # cone marching with per-ray anchors is unsupported
+    pcone = MarchParams(step=0.01, cone_angle=0.01, max_step=1.0).c()
+    st = lib.nacc_sampling_occgrid(C.byref(g), fake, C.byref(pcone), fake, fake, fake, None, 10, fake, None, None,
+                                   None, 0, fake, None, fake, 1 << 24, None)
+    assert st == 4
+    assert lib.nacc_render_fwd(None, 5, None, None, None, None, 3, 1.0, None, None, None, None, None) == 1
+    assert lib.nacc_render_fwd(fake, -1, None, None, None, None, 3, 1.0, None, None, None, None, None) == 1
+    assert lib.nacc_accumulate_along_rays(fake, 3, fake, None, 3, 5, fake, None) == 1  # values NULL needs C == 1
+    assert lib.nacc_importance_sample(4, 8, fake, fake, fake, 1, 0.2, 1000.0, 4, 0, 0, fake, None, None) == 1
+    assert lib.nacc_importance_sample(4, 8, fake, fake, None, 0, 0.2, float("inf"), 4, 0, 0, fake, None, None) == 1
+    assert lib.nacc_occgrid_update(C.byref(g), fake, fake, 0, 1.5, 0.01, 0, fake, None, fake, 1 << 20, None) == 1
+    assert lib.nacc_occgrid_points(C.byref(g), 0, 0, 1, 0, 16**3 + 1, fake, None) == 1
+    assert lib.nacc_filter_early_stop(fake, 4, fake, fake, fake, 10, float("nan"), fake, fake, fake, fake, 10, fake,
+                                      fake, 1 << 20, None) == 1
+
+
+def test_product_has_no_oracle_dependency():
+    """The product package never imports, includes or links the oracle (task rule ③)."""
+    pkg = os.path.join(ROOT, "paper_2305_04966_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                s = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", s, flags=re.M), f
+                assert not re.search(r"#include\s+[<\"].*oracle", s), f
+                assert "liboracle" not in s, f
+    import subprocess
+
+    out = subprocess.run(["ldd", os.path.join(pkg, "libnacc.so")], capture_output=True, text=True).stdout
+    assert "oracle" not in out

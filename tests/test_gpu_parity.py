@@ -1,0 +1,462 @@
+"""GPU parity: the CUDA path (through the C ABI via the thin binding) against
+the fp64 oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star):
+  counts, packed_info, ray_id: bit-exact;  t0/t1: bit-exact (<= 1 ulp allowed);
+  early-stop cut: bit-exact outside the tie band |S - L| < 1e-9 L;
+  T, α, w: abs 1e-5;  color/opacity/depth: |Δ| <= 1e-4 |ref| + 1e-6;
+  g_σ, g_rgb: |Δ| <= 1e-3 (|ref| + 1e-3 max_ray |ref|);
+  resampled edges: backward error <= 1e-6, monotone, |Δs| <= 1e-5 where the
+  CDF slope >= 1e-2;  grid density and bits: bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+L_EPS = -math.log(float(np.float32(1e-4)))
+
+
+@pytest.fixture(scope="module")
+def N():
+    import torch
+
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2305_04966_b200 as N
+
+    torch.cuda.init()
+    return N
+
+
+def cuda(a, dtype=None):
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def gpu_march(N, occ, levels, res, roi, o, d, **kw):
+    bits = cuda(W.pack_bits(occ).view(np.int32))
+    t_min = kw.pop("t_min", None)
+    t_max = kw.pop("t_max", None)
+    capacity = kw.pop("capacity", None)
+    grid = N.GridSpec(roi=tuple(roi), res=res, levels=levels)
+    p = N.MarchParams(**kw)
+    s = N.sampling_occgrid(cuda(o), cuda(d), grid, bits, p, None if t_min is None else cuda(t_min),
+                           None if t_max is None else cuda(t_max), capacity=capacity)
+    return (s.packed_info.cpu().numpy(), s.t0.cpu().numpy(), s.t1.cpu().numpy(), s.ray_id.cpu().numpy())
+
+
+def assert_march_equal(gpu, ref):
+    pg, g0, g1, gr = gpu
+    pr, r0, r1, rr = ref
+    assert np.array_equal(pg, pr), f"packed_info differs in {np.sum(np.any(pg != pr, axis=1))} rays"
+    assert np.array_equal(gr, rr)
+    assert np.array_equal(g0, r0) and np.array_equal(g1, r1)
+
+
+def random_rays(n, rng, lo=-0.5, hi=0.5):
+    c, w = (lo + hi) / 2, hi - lo
+    o = c + rng.normal(size=(n, 3)) * w * 1.5
+    d = c + rng.uniform(-0.6, 0.6, (n, 3)) * w - o
+    o[0], d[0] = [lo - 0.5 * w, c + 0.1 * w, c], [1, 0, 0]
+    o[1], d[1] = [c, c, c], [0.3, -0.5, 0.8]
+    o[2], d[2] = [lo - 0.5 * w, lo, c], [1, 0, 0]
+    o[3], d[3] = [lo - 0.5 * w, hi, c], [1, 0, 0]
+    o[4], d[4] = [c, c, hi + w], [0, 0, -1]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return o.astype(np.float32), d.astype(np.float32)
+
+
+# ============================================================================ march
+def test_march_cfg1(N):
+    c = W.cfg1()
+    ref = O.march(c.occ, c.levels, c.res, c.roi, c.rays_o, c.rays_d, step=c.step)
+    assert_march_equal(gpu_march(N, c.occ, c.levels, c.res, c.roi, c.rays_o, c.rays_d, step=c.step), ref)
+
+
+@pytest.mark.parametrize("levels,res,cone,strat,tminmax", [
+    (1, 4, 0, 0, 0), (1, 16, 0, 1, 0), (2, 8, 0, 0, 1), (3, 13, 0, 1, 1), (1, 8, 1, 0, 0), (3, 8, 1, 0, 0),
+    (4, 16, 1, 0, 1)])
+def test_march_random_grids(N, levels, res, cone, strat, tminmax):
+    rng = np.random.default_rng(10 * levels + res + cone + 100 * strat)
+    o, d = random_rays(3000, rng)
+    occ = (rng.random(levels * res**3) < 0.3).astype(np.uint8)
+    kw = dict(step=float(np.float32(0.0071)), stratified=strat, seed=1234)
+    if cone:
+        kw.update(cone_angle=float(np.float32(1 / 128)), max_step=float(np.float32(0.05)), near=0.02)
+    t_min = t_max = None
+    if tminmax:
+        t_max = rng.uniform(0.5, 3.0, len(o)).astype(np.float32)
+        if not cone:
+            t_min = rng.uniform(0.0, 0.5, len(o)).astype(np.float32)
+    roi = (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5)
+    ref = O.march(occ, levels, res, roi, o, d, t_min=t_min, t_max=t_max, **kw)
+    kw_g = dict(kw)
+    if "near" in kw_g:
+        kw_g["near_plane"] = kw_g.pop("near")
+    got = gpu_march(N, occ, levels, res, roi, o, d, t_min=t_min, t_max=t_max, **kw_g)
+    assert_march_equal(got, ref)
+    assert ref[0][:, 1].sum() > 1000
+
+
+def test_march_edge_cases(N):
+    rng = np.random.default_rng(1)
+    o, d = random_rays(500, rng)
+    roi = (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5)
+    empty = np.zeros(8**3, np.uint8)
+    pk, t0, _, _ = gpu_march(N, empty, 1, 8, roi, o, d, step=0.01)  # all-empty grid
+    assert pk[:, 1].sum() == 0 and len(t0) == 0 and np.all(pk[:, 0] == 0)
+    # all rays miss
+    om = o + np.array([10, 10, 10], np.float32)
+    pk, t0, _, _ = gpu_march(N, np.ones(8**3, np.uint8), 1, 8, roi, om, d, step=0.01)
+    assert pk[:, 1].sum() == 0
+    # zero rays
+    pk, t0, _, _ = gpu_march(N, np.ones(8**3, np.uint8), 1, 8, roi, o[:0], d[:0], step=0.01)
+    assert pk.shape == (0, 2) and len(t0) == 0
+    # one-shot with a too-small capacity falls back to the fill path
+    full = np.ones(8**3, np.uint8)
+    ref = O.march(full, 1, 8, roi, o, d, step=0.01)
+    got = gpu_march(N, full, 1, 8, roi, o, d, step=0.01, capacity=17)
+    assert_march_equal(got, ref)
+    got = gpu_march(N, full, 1, 8, roi, o, d, step=0.01, capacity=len(ref[1]) + 5)
+    assert_march_equal(got, ref)
+    # long rays spanning many warp iterations (tiny step)
+    ref = O.march(full, 1, 8, roi, o[:50], d[:50], step=1e-4)
+    assert ref[0][:, 1].max() > 5000
+    assert_march_equal(gpu_march(N, full, 1, 8, roi, o[:50], d[:50], step=1e-4), ref)
+
+
+def test_march_deterministic(N):
+    rng = np.random.default_rng(2)
+    o, d = random_rays(4000, rng)
+    occ = (rng.random(16**3) < 0.4).astype(np.uint8)
+    a = gpu_march(N, occ, 1, 16, (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5), o, d, step=0.003, stratified=1, seed=9)
+    b = gpu_march(N, occ, 1, 16, (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5), o, d, step=0.003, stratified=1, seed=9)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    c = W.cfg2()
+    ref = O.march(c.occ, 1, 128, c.roi, c.rays_o, c.rays_d, step=c.step)
+    return c, ref
+
+
+def test_march_cfg2_full(N, cfg2):
+    """CFG2 at full size (2^18 rays, 128^3), every ray compared bit-exactly."""
+    c, ref = cfg2
+    assert_march_equal(gpu_march(N, c.occ, 1, 128, c.roi, c.rays_o, c.rays_d, step=c.step), ref)
+
+
+def test_march_cfg3_full(N):
+    """CFG3 at full size (640k rays, 4-level cascade, cone steps)."""
+    c = W.cfg3()
+    ref = O.march(c.occ, 4, 128, c.roi, c.rays_o, c.rays_d, near=c.near, step=c.step, cone_angle=c.cone_angle,
+                  max_step=c.max_step)
+    got = gpu_march(N, c.occ, 4, 128, c.roi, c.rays_o, c.rays_d, near_plane=c.near, step=c.step,
+                    cone_angle=c.cone_angle, max_step=c.max_step)
+    assert_march_equal(got, ref)
+    assert ref[0][:, 1].mean() > 100
+
+
+# ============================================================================ filter
+def gpu_filter(N, pk, t0, t1, sig, eps=1e-4):
+    import torch
+
+    s = N.PackedSamples(cuda(pk), cuda(t0), cuda(t1), cuda(np.zeros(len(t0), np.int32)))
+    f = N.filter_early_stop(s, cuda(sig), eps)
+    torch.cuda.synchronize()
+    return f.packed_info.cpu().numpy(), f.t0.cpu().numpy(), f.t1.cpu().numpy(), f.ray_id.cpu().numpy()
+
+
+def check_filter(gpu, ref, margin, L):
+    pg, g0, g1, gr = gpu
+    pr, r0, r1, rr, _ = ref
+    tie = margin < 1e-9 * L
+    diff = pg[:, 1] != pr[:, 1]
+    assert not np.any(diff & ~tie), f"{np.sum(diff & ~tie)} cuts differ outside the tie band"
+    if not diff.any():
+        assert np.array_equal(pg, pr) and np.array_equal(g0, r0) and np.array_equal(g1, r1) and np.array_equal(gr, rr)
+    return int(tie.sum())
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_filter_ragged(N, seed):
+    pk, t0, t1, _, sig, _ = W.ragged_samples(3000, seed=seed, long_rays=(0, 5, 77))
+    for eps in (1e-4, 1e-2, 0.0):
+        L = -math.log(float(np.float32(eps))) if eps > 0 else math.inf
+        ref = O.filter_early_stop(pk, t0, t1, sig, L)
+        n_tie = check_filter(gpu_filter(N, pk, t0, t1, sig, eps), ref, ref[4], L)
+        assert n_tie == 0
+
+
+def test_filter_cfg2_full(N, cfg2):
+    c, (pk, t0, t1, rid) = cfg2
+    sig, _ = W.field_at_intervals(c.scene.sigma_rgb, c.rays_o, c.rays_d, t0, t1, rid)
+    ref = O.filter_early_stop(pk, t0, t1, sig, L_EPS)
+    check_filter(gpu_filter(N, pk, t0, t1, sig), ref, ref[4], L_EPS)
+    assert len(ref[1]) * 2 < len(t0)  # the filter removes most samples
+
+
+# ============================================================================ render
+def gpu_render(N, pk, t0, t1, sig, rgb, g_color, g_opacity, g_depth, eps=None):
+    import torch
+
+    s = N.PackedSamples(cuda(pk), cuda(t0), cuda(t1), cuda(np.zeros(len(t0), np.int32)))
+    sg = cuda(sig).requires_grad_()
+    cg = cuda(rgb).requires_grad_()
+    color, opacity, depth = N.rendering(s, sg, cg, eps=eps)
+    loss = (color * cuda(g_color)).sum() + (opacity * cuda(g_opacity)).sum() + (depth * cuda(g_depth)).sum()
+    loss.backward()
+    torch.cuda.synchronize()
+    return (color.detach().cpu().numpy(), opacity.detach().cpu().numpy(), depth.detach().cpu().numpy(),
+            sg.grad.cpu().numpy(), cg.grad.cpu().numpy())
+
+
+def close_rel(got, ref, rel=1e-4, floor=1e-6):
+    return np.abs(got - ref) <= rel * np.abs(ref) + floor
+
+
+def grad_ok(got, ref, pk, comps=1):
+    ref = ref.reshape(len(ref), -1)
+    got = got.reshape(len(got), -1)
+    ray_max = np.zeros(len(ref))
+    for (s, c) in pk:
+        if c:
+            ray_max[s : s + c] = np.abs(ref[s : s + c]).max()
+    return np.abs(got - ref) <= 1e-3 * (np.abs(ref) + 1e-3 * ray_max[:, None])
+
+
+def run_render_parity(N, pk, t0, t1, sig, rgb, seed, eps=None):
+    rng = np.random.default_rng(seed)
+    n = len(pk)
+    gC, gO, gD = rng.normal(size=(n, 3)).astype(np.float32), rng.normal(size=n).astype(np.float32), \
+        rng.normal(size=n).astype(np.float32)
+    L = math.inf if eps is None else -math.log(float(np.float32(eps)))
+    got = gpu_render(N, pk, t0, t1, sig, rgb, gC, gO, gD, eps)
+    ref = O.render_fwd(pk, t0, t1, sig, rgb, neg_log_eps=L)
+    gs, grgb = O.render_bwd(pk, t0, t1, sig, rgb, gC, gO, gD, neg_log_eps=L)
+    ok_rays = np.ones(n, bool)
+    if eps is not None:  # rays with an early-stop decision in the tie band are compared leniently
+        _, margin = O.filter_counts(pk, t0, t1, sig, L)
+        ok_rays = margin >= 1e-9 * L
+    assert np.all(close_rel(got[0], ref["color"])[ok_rays])
+    assert np.all(close_rel(got[1], ref["opacity"])[ok_rays])
+    assert np.all(close_rel(got[2], ref["depth"])[ok_rays])
+    samp_ok = np.repeat(ok_rays, pk[:, 1])
+    assert np.all(grad_ok(got[3], gs, pk)[samp_ok])
+    assert np.all(grad_ok(got[4], grgb, pk)[samp_ok])
+
+
+@pytest.mark.parametrize("eps", [None, 1e-4])
+def test_render_ragged(N, eps):
+    pk, t0, t1, _, sig, rgb = W.ragged_samples(2000, seed=3, long_rays=(0, 9, 1500))
+    run_render_parity(N, pk, t0, t1, sig, rgb, seed=4, eps=eps)
+
+
+def test_render_degenerate(N):
+    # zero-sample rays, σ ≡ 0 rays, one opaque interval
+    pk = np.array([[0, 0], [0, 3], [3, 0], [3, 1]], np.int64)
+    t0 = np.array([0.0, 0.1, 0.2, 1.0], np.float32)
+    t1 = np.array([0.1, 0.2, 0.3, 1.5], np.float32)
+    sig = np.array([0.0, 0.0, 0.0, 1e4], np.float32)
+    rgb = np.full((4, 3), 0.5, np.float32)
+    run_render_parity(N, pk, t0, t1, sig, rgb, seed=5)
+    run_render_parity(N, pk, t0, t1, sig, rgb, seed=5, eps=1e-4)
+
+
+@pytest.fixture(scope="module")
+def cfg2_filtered(cfg2):
+    c, (pk, t0, t1, rid) = cfg2
+    sig, _ = W.field_at_intervals(c.scene.sigma_rgb, c.rays_o, c.rays_d, t0, t1, rid)
+    pk2, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, sig, L_EPS)
+    s2, rgb2 = W.field_at_intervals(c.scene.sigma_rgb, c.rays_o, c.rays_d, a0, a1, r2)
+    return pk2, a0, a1, r2, s2, rgb2
+
+
+def test_render_cfg2_full(N, cfg2_filtered):
+    """CFG2 full size, post-filter samples, every ray."""
+    pk2, a0, a1, r2, s2, rgb2 = cfg2_filtered
+    run_render_parity(N, pk2, a0, a1, s2, rgb2, seed=6, eps=1e-4)
+
+
+def test_render_cfg1(N):
+    c = W.cfg1()
+    pk, t0, t1, rid = O.march(c.occ, c.levels, c.res, c.roi, c.rays_o, c.rays_d, step=c.step)
+    sig, rgb = W.field_at_intervals(W.sphere_sigma_rgb, c.rays_o, c.rays_d, t0, t1, rid)
+    run_render_parity(N, pk, t0, t1, sig, rgb, seed=7)
+    run_render_parity(N, pk, t0, t1, sig, rgb, seed=7, eps=1e-4)
+
+
+def test_weights_and_accumulate(N):
+    import torch
+
+    pk, t0, t1, _, sig, rgb = W.ragged_samples(1500, seed=8, long_rays=(3,))
+    for eps in (None, 1e-4):
+        L = math.inf if eps is None else -math.log(float(np.float32(eps)))
+        s = N.PackedSamples(cuda(pk), cuda(t0), cuda(t1), cuda(np.zeros(len(t0), np.int32)))
+        sg = cuda(sig).requires_grad_()
+        w, T, a = N.render_weights(s, sg, eps=eps)
+        ref = O.render_fwd(pk, t0, t1, sig, None, neg_log_eps=L)
+        _, margin = O.filter_counts(pk, t0, t1, sig, L)
+        ok = np.repeat(margin >= 1e-9 * L, pk[:, 1])
+        assert np.all((np.abs(w.detach().cpu().numpy() - ref["weights"]) <= 1e-5)[ok])
+        assert np.all(np.abs(T.detach().cpu().numpy() - ref["trans"]) <= 1e-5)
+        assert np.all(np.abs(a.detach().cpu().numpy() - ref["alphas"]) <= 1e-5)
+        rng = np.random.default_rng(9)
+        gw, gT = rng.normal(size=len(t0)).astype(np.float32), rng.normal(size=len(t0)).astype(np.float32)
+        (w * cuda(gw)).sum().add_((T * cuda(gT)).sum()).backward()
+        gs = O.weights_bwd(pk, t0, t1, sig, gw, gT, neg_log_eps=L)
+        assert np.all(grad_ok(sg.grad.cpu().numpy(), gs, pk)[ok])
+    # accumulate fwd/bwd with C = 1 (opacity), 3 (rgb) and 5
+    w = torch.rand(len(t0), device="cuda", requires_grad=True)
+    for C_ in (None, 3, 5):
+        vals = None if C_ is None else torch.rand(len(t0), C_, device="cuda", requires_grad=True)
+        out = N.accumulate_along_rays(s, w, vals)
+        g = torch.randn_like(out)
+        out.backward(g)
+        wn = w.detach().cpu().numpy()
+        vn = None if vals is None else vals.detach().cpu().numpy()
+        ref = O.accumulate(pk, wn, vn, C_=1)
+        assert np.all(close_rel(out.detach().cpu().numpy(), ref, 1e-5, 1e-6))
+        gw_ref, gv_ref = O.accumulate_bwd(pk, wn, vn, g.cpu().numpy())
+        assert np.all(close_rel(w.grad.cpu().numpy(), gw_ref, 1e-5, 1e-6))
+        if vals is not None:
+            assert np.all(close_rel(vals.grad.cpu().numpy(), gv_ref, 1e-6, 1e-7))
+        w.grad = None
+
+
+# ============================================================================ resample
+def check_resample(s_gpu, s_ref, F_ref, e, n_out, stratified=False, seed=0):
+    n = len(s_gpu)
+    for r in range(n):
+        Fh = F_ref[r]
+        back = np.interp(s_gpu[r].astype(np.float64), e[r].astype(np.float64), Fh)
+        if not stratified:
+            u = np.arange(n_out + 1) / n_out
+            assert np.abs(back - u).max() <= 1e-6, r
+        assert np.all(np.diff(s_gpu[r]) >= 0)
+        slope = np.diff(Fh) / np.maximum(np.diff(e[r].astype(np.float64)), 1e-30)
+        j = np.clip(np.searchsorted(e[r], s_ref[r], side="right") - 1, 0, len(slope) - 1)
+        steep = slope[j] >= 1e-2
+        assert np.all(np.abs(s_gpu[r] - s_ref[r])[steep] <= 1e-5)
+
+
+def test_resample_cfg4_full(N):
+    """CFG4: 2^16 rays, 256 -> 96 -> 48 (lindisp, t_n = 0.2, t_f = 1000)."""
+    import torch
+
+    p = W.cfg4()
+    n = len(p.rays_o)
+    e0 = p.s_edges
+    tm = W.lindisp(0.5 * (e0[:, :-1].astype(np.float64) + e0[:, 1:]), p.t_near, p.t_far)
+    x = p.rays_o[:, None, :].astype(np.float64) + tm[..., None] * p.rays_d[:, None, :]
+    sig1, _ = p.scene.sigma_rgb(x)
+    sig1 = sig1.astype(np.float32)
+    s1_gpu, t1_gpu = N.importance_sample(cuda(e0), 96, sigma=cuda(sig1), map_kind=N.MAP_LINDISP, t_near=p.t_near,
+                                         t_far=p.t_far)
+    s1_ref, t1_ref = O.importance_sample(e0, 96, sigma=sig1, map_kind=1, t_near=p.t_near, t_far=p.t_far)
+    F1 = O.importance_cdf(e0, sigma=sig1, map_kind=1, t_near=p.t_near, t_far=p.t_far)
+    s1g = s1_gpu.cpu().numpy()
+    pick = np.random.default_rng(0).choice(n, 4096, replace=False)
+    check_resample(s1g[pick], s1_ref[pick], F1[pick], e0[pick], 96)
+    tg = t1_gpu.cpu().numpy().astype(np.float64)  # t_out = Φ(s_out): check it in s-space (Φ is steep near s = 1)
+    s_back = (1.0 / tg - 1.0 / p.t_near) / (1.0 / p.t_far - 1.0 / p.t_near)
+    assert np.abs(s_back - s1g).max() <= 1e-6
+    # round 2 from the oracle's round-1 edges (inputs never come from the CUDA path)
+    e1 = s1_ref.astype(np.float32)
+    tm2 = W.lindisp(0.5 * (e1[:, :-1].astype(np.float64) + e1[:, 1:]), p.t_near, p.t_far)
+    x2 = p.rays_o[:, None, :].astype(np.float64) + tm2[..., None] * p.rays_d[:, None, :]
+    sig2 = p.scene.sigma_rgb(x2)[0].astype(np.float32)
+    s2_gpu, _ = N.importance_sample(cuda(e1), 48, sigma=cuda(sig2), map_kind=N.MAP_LINDISP, t_near=p.t_near,
+                                    t_far=p.t_far)
+    s2_ref, _ = O.importance_sample(e1, 48, sigma=sig2, map_kind=1, t_near=p.t_near, t_far=p.t_far)
+    F2 = O.importance_cdf(e1, sigma=sig2, map_kind=1, t_near=p.t_near, t_far=p.t_far)
+    check_resample(s2_gpu.cpu().numpy()[pick], s2_ref[pick], F2[pick], e1[pick], 48)
+    torch.cuda.synchronize()
+
+
+def test_resample_cdf_input_stratified_and_degenerate(N):
+    rng = np.random.default_rng(11)
+    n, m = 700, 40
+    e = np.sort(rng.uniform(0, 1, (n, m + 1)), axis=1).astype(np.float32)
+    e[:, 0], e[:, -1] = 0, 1
+    w = np.where(rng.random((n, m)) < 0.4, 0, rng.uniform(0, 1, (n, m)))
+    w[:5] = 0.0  # zero-mass rays -> uniform edges
+    cdf = np.concatenate([np.zeros((n, 1)), np.cumsum(w, 1)], 1).astype(np.float32)
+    sg, _ = N.importance_sample(cuda(e), 33, cdf=cuda(cdf), map_kind=N.MAP_IDENTITY, t_near=1.0, t_far=5.0)
+    sr, _ = O.importance_sample(e, 33, cdf=cdf, map_kind=0, t_near=1.0, t_far=5.0)
+    F = O.importance_cdf(e, cdf=cdf, map_kind=0, t_near=1.0, t_far=5.0)
+    check_resample(sg.cpu().numpy(), sr, F, e, 33)
+    sig = rng.uniform(0, 20, (n, m)).astype(np.float32)
+    sg, _ = N.importance_sample(cuda(e), 17, sigma=cuda(sig), map_kind=N.MAP_LINDISP, stratified=True, seed=5)
+    sr, _ = O.importance_sample(e, 17, sigma=sig, map_kind=1, stratified=1, seed=5)
+    F = O.importance_cdf(e, sigma=sig, map_kind=1)
+    check_resample(sg.cpu().numpy(), sr, F, e, 17, stratified=True)
+
+
+# ============================================================================ grid update
+def test_occgrid_points_bit_exact(N):
+    import torch
+
+    for levels, res, roi in ((1, 128, (0, 0, 0, 1, 1, 1)), (4, 32, (-1, -1, -1, 1, 1, 1)), (2, 7, (-0.3, 0, 1, 0.9, 2, 1.5))):
+        g = N.OccupancyGrid(N.GridSpec(roi=roi, res=res, levels=levels), seed=77)
+        for jitter in (0, 1):
+            got = g.points(5, bool(jitter)).cpu().numpy()
+            ref = O.occgrid_points(levels, res, roi, seed=77, step=5, jitter=jitter)
+            assert np.array_equal(got, ref)
+        nc = levels * res**3
+        got = g.points(9, True, nc // 3, nc // 2).cpu().numpy()
+        ref = O.occgrid_points(levels, res, roi, seed=77, step=9, jitter=1, cell_begin=nc // 3, cell_count=nc // 2)
+        assert np.array_equal(got, ref)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("rule,thresh_rule", [(0, 0), (1, 0), (0, 1)])
+def test_occgrid_update_bit_exact(N, rule, thresh_rule):
+    import torch
+
+    levels, res = 2, 64
+    rng = np.random.default_rng(12 + rule + 2 * thresh_rule)
+    dens = rng.uniform(0, 0.05, levels * res**3).astype(np.float32)
+    g = N.OccupancyGrid(N.GridSpec(roi=(-1, -1, -1, 1, 1, 1), res=res, levels=levels), decay=0.95, threshold=0.01,
+                        rule=rule, thresh_rule=thresh_rule)
+    g.density.copy_(cuda(dens))
+    ref_d = dens.copy()
+    for it in range(4):
+        fresh = np.where(rng.random(dens.size) < 0.1, rng.uniform(0, 0.5, dens.size), 0).astype(np.float32)
+        g.update(cuda(fresh))
+        ref_d, ref_b, mean = O.occgrid_update(levels, res, (-1, -1, -1, 1, 1, 1), ref_d, fresh, rule=rule, decay=0.95,
+                                              threshold=0.01, thresh_rule=thresh_rule)
+        got_d = g.density.cpu().numpy()
+        assert np.array_equal(got_d, ref_d)
+        got_b = np.unpackbits(g.bits.cpu().numpy().view(np.uint8), bitorder="little")[: dens.size]
+        tau = min(0.01, mean) if thresh_rule else 0.01
+        tie = np.abs(ref_d.astype(np.float64) - tau) < 1e-12 * max(tau, 1e-30)
+        assert np.array_equal(got_b[~tie], ref_b[~tie])
+        assert abs(g.mean.item() - mean) <= 1e-12 * max(mean, 1e-30)
+    torch.cuda.synchronize()
+
+
+def test_update_every_n_steps_single_rank(N):
+    import torch
+
+    spec = N.GridSpec(roi=(0, 0, 0, 1, 1, 1), res=32)
+    g = N.OccupancyGrid(spec, seed=3)
+    box = lambda x: ((x < 0.5).all(dim=1).float() * 0.3)  # ConstantBox covering 1/8
+    for step in range(33):
+        g.update_every_n_steps(step, box, n=16, jitter=False)
+    torch.cuda.synchronize()
+    bits = np.unpackbits(g.bits.cpu().numpy().view(np.uint8), bitorder="little")[: spec.n_cells]
+    assert bits.mean() == 0.125  # 3 updates with γ = 0.95: 0.3·(1-0.95^3) > 0.01
