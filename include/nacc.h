@@ -179,18 +179,28 @@ nacc_status nacc_accumulate_along_rays_bwd(const int64_t *packed_info, int64_t n
                                            float *g_weights, float *g_values,
                                            cudaStream_t stream);
 
-/* Fused render (Alg. 1 nerfacc.rendering): per ray
+/* Fused render (Alg. 1 nerfacc.rendering(t0, t1, r_id, ...)).  On the
+ * flat path n_samples is the arrays' length (a capacity); the samples in use
+ * are [0, start + count of the last ray), read from packed_info on the device,
+ * so the call needs no host-side total (CUDA-graph capturable).  Per ray
  *   color = Σ w rgb, opacity = Σ w, depth = Σ w m / max(opacity, 1e-10),
  *   m = (t0+t1)/2 (reading #12).  ctx [n_rays][5] fp64 out (may be NULL) keeps
- *   (C_r, C_g, C_b, O, N) for the backward. */
-nacc_status nacc_render_fwd(const int64_t *packed_info, int64_t n_rays, const float *t0,
+ *   (C_r, C_g, C_b, O, N) for the backward.  ray_id [n_samples] (the packed
+ *   tensor's r) selects the flat ray-aligned-tile kernel, which needs
+ *   the contiguous packing the sampling calls produce (start_0 = 0, start_{r+1}
+ *   = start_r + count_r); NULL (or rgb == NULL) falls back to one warp per ray.
+ *   16-byte aligned arrays take vectorised loads. */
+nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
+                            const float *t0,
                             const float *t1, const float *sigma, const float *rgb,
                             int64_t n_samples, double neg_log_eps, float *color, float *opacity,
                             float *depth, double *ctx, cudaStream_t stream);
 /* Backward of nacc_render_fwd (t detached): given upstream
  * g_color [n][3], g_opacity [n], g_depth [n] (each may be NULL = 0), writes
- * g_sigma [N] and g_rgb [N][3].  ctx from the forward (NULL = recompute). */
-nacc_status nacc_render_bwd(const int64_t *packed_info, int64_t n_rays, const float *t0,
+ * g_sigma [N] and g_rgb [N][3].  ctx from the forward (NULL = recompute, one
+ * warp per ray); with ray_id and ctx the flat kernel runs. */
+nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
+                            const float *t0,
                             const float *t1, const float *sigma, const float *rgb,
                             int64_t n_samples, double neg_log_eps, const double *ctx,
                             const float *g_color, const float *g_opacity, const float *g_depth,

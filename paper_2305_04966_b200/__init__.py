@@ -17,6 +17,8 @@ from .api import (  # noqa: F401
     neg_log_eps,
     owner_slab,
     render_weights,
+    render_fwd,
+    render_bwd,
     rendering,
     sampling_occgrid,
     MAP_IDENTITY,

@@ -92,11 +92,17 @@ class MarchParams:
 @dataclasses.dataclass
 class PackedSamples:
     """Sample-as-interval packed tensor: t0, t1 fp32 [N], ray_id
-    int32 [N], packed_info int64 [n_rays, 2] = (start, count)."""
+    int32 [N], packed_info int64 [n_rays, 2] = (start, count).
+
+    In device-count mode (``sync=False``) the arrays have a fixed capacity,
+    ``total`` (device int64 [1]) holds N and nothing waits for the host, so a
+    whole step can be captured in a CUDA graph."""
     packed_info: torch.Tensor
     t0: torch.Tensor
     t1: torch.Tensor
     ray_id: torch.Tensor
+    total: Optional[torch.Tensor] = None
+    status: Optional[torch.Tensor] = None
 
     @property
     def n_rays(self) -> int:
@@ -104,16 +110,20 @@ class PackedSamples:
 
     @property
     def n_samples(self) -> int:
+        """N when synced; the capacity in device-count mode."""
         return self.t0.numel()
 
 
 # ----------------------------------------------------------------------------- sampling
 def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec, bits: torch.Tensor,
                      params: MarchParams, t_min: Optional[torch.Tensor] = None,
-                     t_max: Optional[torch.Tensor] = None, capacity: Optional[int] = None) -> PackedSamples:
+                     t_max: Optional[torch.Tensor] = None, capacity: Optional[int] = None,
+                     sync: bool = True) -> PackedSamples:
     """Alg. 1 ``nerfacc.sampling`` with the occupancy-grid estimator.
-    ``capacity`` (optional) enables the one-shot count+scan+fill; the exact
-    path (count+scan, read the total, fill) is used otherwise or on overflow."""
+    ``capacity`` enables the one-shot single-pass march; without it the exact
+    path runs (count + scan, read the total, fill).  ``sync=False`` (needs a
+    capacity) returns capacity-sized arrays with a device total and a device
+    status (NACC_ERR_INSUFFICIENT_CAPACITY if the capacity was too small)."""
     lib = L.lib()
     n = rays_o.shape[0]
     dev = rays_o.device
@@ -133,10 +143,16 @@ def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec,
     t1 = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
     rid = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
     with_out = cap > 0
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
     check(lib.nacc_sampling_occgrid(C.byref(g), _ptr(bits), C.byref(p), _ptr(rays_o), _ptr(rays_d), _ptr(t_min),
                                     _ptr(t_max), n, _ptr(packed), _ptr(t0) if with_out else None,
                                     _ptr(t1) if with_out else None, _ptr(rid) if with_out else None, cap,
-                                    _ptr(total), None, _ptr(ws), ws.numel(), _stream()), "nacc_sampling_occgrid")
+                                    _ptr(total), _ptr(status), _ptr(ws), ws.numel(), _stream()),
+          "nacc_sampling_occgrid")
+    if not sync:
+        if not with_out:
+            raise ValueError("sync=False needs a capacity")
+        return PackedSamples(packed, t0, t1, rid, total, status)
     N = int(total.item())
     if N > cap:
         t0 = torch.empty(max(N, 1), dtype=torch.float32, device=dev)
@@ -149,9 +165,11 @@ def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec,
     return PackedSamples(packed, t0[:N], t1[:N], rid[:N])
 
 
-def filter_early_stop(samples: PackedSamples, sigma: torch.Tensor, eps: Optional[float] = 1e-4) -> PackedSamples:
+def filter_early_stop(samples: PackedSamples, sigma: torch.Tensor, eps: Optional[float] = 1e-4,
+                      sync: bool = True) -> PackedSamples:
     """§4.2 no-gradient filtering: keep each ray's prefix with entering
-    transmittance >= ε.  ``sigma`` comes from the caller's no-grad density query."""
+    transmittance >= ε.  ``sigma`` comes from the caller's no-grad density query.
+    ``sync=False`` keeps the input capacity and returns a device total."""
     lib = L.lib()
     n, N = samples.n_rays, samples.n_samples
     dev = samples.packed_info.device
@@ -166,6 +184,8 @@ def filter_early_stop(samples: PackedSamples, sigma: torch.Tensor, eps: Optional
     check(lib.nacc_filter_early_stop(_ptr(samples.packed_info), n, _ptr(samples.t0), _ptr(samples.t1), _ptr(sigma),
                                      N, neg_log_eps(eps), _ptr(packed), _ptr(t0), _ptr(t1), _ptr(rid), cap,
                                      _ptr(total), _ptr(ws), ws.numel(), _stream()), "nacc_filter_early_stop")
+    if not sync:
+        return PackedSamples(packed, t0, t1, rid, total)
     M = int(total.item())
     return PackedSamples(packed, t0[:M], t1[:M], rid[:M])
 
@@ -173,33 +193,33 @@ def filter_early_stop(samples: PackedSamples, sigma: torch.Tensor, eps: Optional
 # ----------------------------------------------------------------------------- rendering
 class _RenderFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, packed_info, t0, t1, sigma, rgb, nle):
+    def forward(ctx, packed_info, ray_id, t0, t1, sigma, rgb, nle):
         n, N = packed_info.shape[0], t0.numel()
         dev = t0.device
         color = torch.empty((n, 3), dtype=torch.float32, device=dev)
         opacity = torch.empty(n, dtype=torch.float32, device=dev)
         depth = torch.empty(n, dtype=torch.float32, device=dev)
         cx = torch.empty((n, 5), dtype=torch.float64, device=dev)
-        check(L.lib().nacc_render_fwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), _ptr(rgb), N, nle,
-                                      _ptr(color), _ptr(opacity), _ptr(depth), _ptr(cx), _stream()),
+        check(L.lib().nacc_render_fwd(_ptr(packed_info), _ptr(ray_id), n, _ptr(t0), _ptr(t1), _ptr(sigma), _ptr(rgb),
+                                      N, nle, _ptr(color), _ptr(opacity), _ptr(depth), _ptr(cx), _stream()),
               "nacc_render_fwd")
-        ctx.save_for_backward(packed_info, t0, t1, sigma, rgb, cx)
+        ctx.save_for_backward(packed_info, ray_id, t0, t1, sigma, rgb, cx)
         ctx.nle = nle
         return color, opacity, depth
 
     @staticmethod
     def backward(ctx, g_color, g_opacity, g_depth):
-        packed_info, t0, t1, sigma, rgb, cx = ctx.saved_tensors
+        packed_info, ray_id, t0, t1, sigma, rgb, cx = ctx.saved_tensors
         n, N = packed_info.shape[0], t0.numel()
         g_sigma = torch.empty_like(sigma)
         g_rgb = torch.empty_like(rgb)
         gc = None if g_color is None else g_color.contiguous().float()
         go = None if g_opacity is None else g_opacity.contiguous().float()
         gd = None if g_depth is None else g_depth.contiguous().float()
-        check(L.lib().nacc_render_bwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), _ptr(rgb), N, ctx.nle,
-                                      _ptr(cx), _ptr(gc), _ptr(go), _ptr(gd), _ptr(g_sigma), _ptr(g_rgb),
-                                      _stream()), "nacc_render_bwd")
-        return None, None, None, g_sigma, g_rgb, None
+        check(L.lib().nacc_render_bwd(_ptr(packed_info), _ptr(ray_id), n, _ptr(t0), _ptr(t1), _ptr(sigma), _ptr(rgb),
+                                      N, ctx.nle, _ptr(cx), _ptr(gc), _ptr(go), _ptr(gd), _ptr(g_sigma),
+                                      _ptr(g_rgb), _stream()), "nacc_render_bwd")
+        return None, None, None, None, g_sigma, g_rgb, None
 
 
 def rendering(samples: PackedSamples, sigma: torch.Tensor, rgb: torch.Tensor, eps: Optional[float] = None):
@@ -208,7 +228,41 @@ def rendering(samples: PackedSamples, sigma: torch.Tensor, rgb: torch.Tensor, ep
     N = samples.n_samples
     sigma = _req(sigma, torch.float32, "sigma", N)
     rgb = _req(rgb, torch.float32, "rgb", 3 * N)
-    return _RenderFn.apply(samples.packed_info, samples.t0, samples.t1, sigma, rgb.view(N, 3), neg_log_eps(eps))
+    rid = samples.ray_id if samples.ray_id.numel() == N else None
+    return _RenderFn.apply(samples.packed_info, rid, samples.t0, samples.t1, sigma, rgb.view(N, 3), neg_log_eps(eps))
+
+
+def render_fwd(samples: PackedSamples, sigma: torch.Tensor, rgb: torch.Tensor, eps: Optional[float] = None):
+    """Functional (no autograd) ``nacc_render_fwd``: returns (color, opacity,
+    depth, ctx).  Works in device-count mode (no host sync; graph-capturable)."""
+    n, N = samples.n_rays, samples.n_samples
+    dev = samples.t0.device
+    sigma = _req(sigma.detach(), torch.float32, "sigma", N)
+    rgb = _req(rgb.detach(), torch.float32, "rgb", 3 * N)
+    color = torch.empty((n, 3), dtype=torch.float32, device=dev)
+    opacity = torch.empty(n, dtype=torch.float32, device=dev)
+    depth = torch.empty(n, dtype=torch.float32, device=dev)
+    cx = torch.empty((n, 5), dtype=torch.float64, device=dev)
+    check(L.lib().nacc_render_fwd(_ptr(samples.packed_info), _ptr(samples.ray_id), n, _ptr(samples.t0),
+                                  _ptr(samples.t1), _ptr(sigma), _ptr(rgb), N, neg_log_eps(eps), _ptr(color),
+                                  _ptr(opacity), _ptr(depth), _ptr(cx), _stream()), "nacc_render_fwd")
+    return color, opacity, depth, cx
+
+
+def render_bwd(samples: PackedSamples, sigma: torch.Tensor, rgb: torch.Tensor, ctx: torch.Tensor,
+               g_color: Optional[torch.Tensor] = None, g_opacity: Optional[torch.Tensor] = None,
+               g_depth: Optional[torch.Tensor] = None, eps: Optional[float] = None):
+    """Functional ``nacc_render_bwd``: returns (g_sigma, g_rgb)."""
+    n, N = samples.n_rays, samples.n_samples
+    sigma = _req(sigma.detach(), torch.float32, "sigma", N)
+    rgb = _req(rgb.detach(), torch.float32, "rgb", 3 * N)
+    g_sigma = torch.empty_like(sigma)
+    g_rgb = torch.empty_like(rgb)
+    check(L.lib().nacc_render_bwd(_ptr(samples.packed_info), _ptr(samples.ray_id), n, _ptr(samples.t0),
+                                  _ptr(samples.t1), _ptr(sigma), _ptr(rgb), N, neg_log_eps(eps), _ptr(ctx),
+                                  _ptr(g_color), _ptr(g_opacity), _ptr(g_depth), _ptr(g_sigma), _ptr(g_rgb),
+                                  _stream()), "nacc_render_bwd")
+    return g_sigma, g_rgb
 
 
 class _WeightsFn(torch.autograd.Function):
@@ -310,6 +364,20 @@ def owner_slab(n_cells: int, rank: int, world: int) -> tuple[int, int]:
     return n_cells * rank // world, n_cells * (rank + 1) // world
 
 
+def merge_fresh(slab_values: torch.Tensor, lo: int, hi: int, n_cells: int, group=None) -> torch.Tensor:
+    """Owner-computes merge of the fresh grid values (reading #15):
+    each rank fills its slab [lo, hi) of a zero buffer and a MAX all-reduce
+    over the process group (NCCL over NVLink on GPUs) assembles the full grid.
+    σ >= 0, so non-owners' zeros never win; the result is identical on every
+    rank and equal to a one-rank evaluation."""
+    fresh = torch.zeros(n_cells, dtype=torch.float32, device=slab_values.device)
+    fresh[lo:hi] = slab_values.reshape(-1).float()
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        if torch.distributed.get_world_size(group) > 1:
+            torch.distributed.all_reduce(fresh, op=torch.distributed.ReduceOp.MAX, group=group)
+    return fresh
+
+
 class OccupancyGrid:
     """The occupancy-grid transmittance estimator (P:240-241, P:26 ``nerfacc.
     TransmittanceEstimator``): fp32 cached density + public bitfield, updated
@@ -358,13 +426,9 @@ class OccupancyGrid:
             rank = torch.distributed.get_rank(process_group)
         C_ = self.spec.n_cells
         lo, hi = owner_slab(C_, rank, world)
-        fresh = torch.zeros(C_, dtype=torch.float32, device=self.device)
-        if hi > lo:
-            xyz = self.points(step, jitter, lo, hi - lo)
-            fresh[lo:hi] = occ_eval_fn(xyz).reshape(-1).float()
-        if world > 1:
-            torch.distributed.all_reduce(fresh, op=torch.distributed.ReduceOp.MAX, group=process_group)
-        self.update(fresh)
+        vals = occ_eval_fn(self.points(step, jitter, lo, hi - lo)) if hi > lo else \
+            torch.zeros(0, dtype=torch.float32, device=self.device)
+        self.update(merge_fresh(vals, lo, hi, C_, process_group))
         return True
 
     def state_dict(self):

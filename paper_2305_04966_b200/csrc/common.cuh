@@ -89,6 +89,11 @@ __device__ __forceinline__ float warp_sumf(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   return v;
 }
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
 __device__ __forceinline__ int64_t warp_incl_scan_i64(int64_t v) {
   const int lane = threadIdx.x & 31;
 #pragma unroll

@@ -1,61 +1,89 @@
 // filter.cu — §4.2 "No Gradient Filtering": samples whose entering
 // transmittance is below ε are dropped before the differentiable pass.
 // Per ray the kept set is a prefix (S_i never decreases; reading #9), so the
-// filter is a per-ray cut (fp64 segmented scan) + exclusive scan + prefix copy.
+// filter is a per-ray cut (sequential fp64 sum, early exit) + exclusive scan of
+// the cuts + a compacting copy of the prefixes.
 #include "common.cuh"
 
 namespace nacc {
 
-// one warp per ray: cut[r] = min{i : S_i > L}, S_i = Σ_{j<i} σ_j (t1_j - t0_j) in fp64
+// one thread per ray: walk the ray in order, accumulating S_i = Σ_{j<i} σ_j δ_j
+// in fp64 exactly as the definition (σ_j δ_j is exact in fp64, so the sum is
+// the sequential one), and stop at the first S_i > L.  Only the samples up to
+// the cut are read (the kept prefix plus one), four loads in flight.
 __global__ void __launch_bounds__(256) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
                                                          const float *__restrict__ t0, const float *__restrict__ t1,
                                                          const float *__restrict__ sigma, double L,
                                                          int32_t *__restrict__ cut_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n_rays) return;
-  const longlong2 pi = reinterpret_cast<const longlong2 *>(packed_info)[r];
+  const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
   const int64_t st = pi.x, cnt = pi.y;
-  double carry = 0.0;
+  double S = 0.0;
   int64_t cut = cnt;
-  for (int64_t base = 0; base < cnt; base += 32) {
-    const int64_t i = base + lane;
-    double s = 0.0;
-    if (i < cnt) {
-      const int64_t q = st + i;
-      s = (double)__ldg(sigma + q) * ((double)__ldg(t1 + q) - (double)__ldg(t0 + q));
+  for (int64_t i = 0; i < cnt; i += 4) {
+    float a[4], b[4], c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool in = i + j < cnt;
+      a[j] = in ? __ldg(t0 + st + i + j) : 0.f;
+      b[j] = in ? __ldg(t1 + st + i + j) : 0.f;
+      c[j] = in ? __ldg(sigma + st + i + j) : 0.f;
     }
-    const double incl = warp_incl_scan(s);
-    double excl = __shfl_up_sync(kFull, incl, 1);
-    if (lane == 0) excl = 0.0;
-    const double S = carry + excl;
-    const unsigned b = __ballot_sync(kFull, (i < cnt) && (S > L));
-    if (b) {
-      cut = base + __ffs(b) - 1;
-      break;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!done && i + j < cnt) {
+        if (S > L) {
+          cut = i + j;
+          done = true;
+        } else {
+          S = __dadd_rn(S, __dmul_rn((double)c[j], __dsub_rn((double)b[j], (double)a[j])));
+        }
+      }
     }
-    carry += __shfl_sync(kFull, incl, 31);
+    if (done) break;
   }
-  if (lane == 0) cut_out[r] = (int32_t)cut;
+  cut_out[r] = (int32_t)cut;
 }
 
-// one warp per ray: copy the kept prefix to its packed position
-__global__ void __launch_bounds__(256) filter_copy_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
-                                                          const float *__restrict__ t0, const float *__restrict__ t1,
-                                                          const int64_t *__restrict__ packed_out,
-                                                          const int64_t *__restrict__ total, int64_t capacity,
-                                                          float *__restrict__ t0_out, float *__restrict__ t1_out,
-                                                          int32_t *__restrict__ ray_id_out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= n_rays) return;
+// block of 256 consecutive rays: their kept prefixes are contiguous in the
+// output; each thread copies output positions, locating its ray by binary
+// search over the block's output starts (in shared memory)
+constexpr int kCopyRays = 256;
+
+__global__ void __launch_bounds__(kCopyRays) filter_copy_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
+                                                                const float *__restrict__ t0,
+                                                                const float *__restrict__ t1,
+                                                                const int64_t *__restrict__ packed_out,
+                                                                const int64_t *__restrict__ total, int64_t capacity,
+                                                                float *__restrict__ t0_out, float *__restrict__ t1_out,
+                                                                int32_t *__restrict__ ray_id_out) {
+  __shared__ int64_t s_out[kCopyRays + 1];
+  __shared__ int64_t s_in[kCopyRays];
   if (*total > capacity) return;
-  const int64_t src = packed_info[2 * r];
-  const longlong2 po = reinterpret_cast<const longlong2 *>(packed_out)[r];
-  for (int64_t i = lane; i < po.y; i += 32) {
-    t0_out[po.x + i] = __ldg(t0 + src + i);
-    t1_out[po.x + i] = __ldg(t1 + src + i);
-    ray_id_out[po.x + i] = (int32_t)r;
+  const int64_t r0 = (int64_t)blockIdx.x * kCopyRays;
+  const int nr = (int)min((int64_t)kCopyRays, n_rays - r0);
+  const int t = threadIdx.x;
+  if (t < nr) {
+    const longlong2 po = __ldg(reinterpret_cast<const longlong2 *>(packed_out) + r0 + t);
+    s_out[t] = po.x;
+    s_in[t] = __ldg(packed_info + 2 * (r0 + t));
+    if (t == nr - 1) s_out[nr] = po.x + po.y;
+  }
+  __syncthreads();
+  const int64_t p0 = s_out[0], p1 = s_out[nr];
+  for (int64_t p = p0 + t; p < p1; p += kCopyRays) {
+    int lo = 0, hi = nr - 1;  // largest k with s_out[k] <= p
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_out[mid] <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    const int64_t src = s_in[lo] + (p - s_out[lo]);
+    t0_out[p] = __ldg(t0 + src);
+    t1_out[p] = __ldg(t1 + src);
+    ray_id_out[p] = (int32_t)(r0 + lo);
   }
 }
 
@@ -101,14 +129,13 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   int32_t *cuts;
   void *scan_ws;
   filter_ws_layout(n_rays, &cuts, &scan_ws, ws);
-  const int blocks = grid_for(n_rays * 32, 256);
-  filter_cut_kernel<<<blocks, 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts);
+  filter_cut_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts);
   count_launch(1);
   NACC_CHECK_LAUNCH();
   NACC_CUDA(scan_counts_to_packed(cuts, n_rays, packed_info_out, total, scan_ws, stream));
   if (capacity > 0) {
-    filter_copy_kernel<<<blocks, 256, 0, stream>>>(packed_info, n_rays, t0, t1, packed_info_out, total, capacity,
-                                                   t0_out, t1_out, ray_id_out);
+    filter_copy_kernel<<<grid_for(n_rays, kCopyRays), kCopyRays, 0, stream>>>(
+        packed_info, n_rays, t0, t1, packed_info_out, total, capacity, t0_out, t1_out, ray_id_out);
     count_launch(1);
     NACC_CHECK_LAUNCH();
   }

@@ -49,10 +49,10 @@ __device__ __forceinline__ float4 lattice_at(const float4 *__restrict__ lat, int
 __global__ void field_samples_kernel(const float4 *__restrict__ lat, int R, float lo, float hi, int contracted,
                                      const float *__restrict__ o, const float *__restrict__ d,
                                      const float *__restrict__ t0, const float *__restrict__ t1,
-                                     const int32_t *__restrict__ rid, int64_t n, float *__restrict__ sigma,
-                                     float *__restrict__ rgb) {
+                                     const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
+                                     float *__restrict__ sigma, float *__restrict__ rgb) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= n || (n_dev && i >= *n_dev)) return;
   const int64_t r = __ldg(rid + i);
   const float m = 0.5f * (__ldg(t0 + i) + __ldg(t1 + i));
   const float x = __ldg(o + 3 * r) + m * __ldg(d + 3 * r);
@@ -88,12 +88,14 @@ extern "C" {
 
 nacc_status naccx_field_at_samples(const float *lattice, int32_t res, float lo, float hi, int32_t contracted,
                                    const float *rays_o, const float *rays_d, const float *t0, const float *t1,
-                                   const int32_t *ray_id, int64_t n, float *sigma, float *rgb, cudaStream_t stream) {
+                                   const int32_t *ray_id, int64_t n, const int64_t *n_dev, float *sigma, float *rgb,
+                                   cudaStream_t stream) {
   if (n < 0 || res < 2 || !(hi > lo)) return NACC_ERR_INVALID_ARGUMENT;
   if (n == 0) return NACC_OK;
   if (!lattice || !rays_o || !rays_d || !t0 || !t1 || !ray_id || !sigma) return NACC_ERR_INVALID_ARGUMENT;
   field_samples_kernel<<<blocks_for(n), 256, 0, stream>>>(reinterpret_cast<const float4 *>(lattice), res, lo, hi,
-                                                          contracted, rays_o, rays_d, t0, t1, ray_id, n, sigma, rgb);
+                                                          contracted, rays_o, rays_d, t0, t1, ray_id, n, n_dev, sigma,
+                                                          rgb);
   g_launches++;
   return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
 }

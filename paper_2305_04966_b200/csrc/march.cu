@@ -9,7 +9,7 @@
 //   l*   = first level l with lo_l <= x < hi_l on every axis
 //   u_a  = (x_a - lo_{l*,a}) * s_{l*,a},  i_a = clamp(floor(u_a), 0, R-1)
 //   P(k) = m_k < far_r  and  l* exists  and  bit[l*][i]
-// The k range each warp scans is a conservative fp64 slab bound (±2 steps
+// The k range each warp scans is a conservative fp32 slab bound (±2 steps
 // around the padded outermost box); membership alone decides emission.
 #include "common.cuh"
 
@@ -18,11 +18,11 @@ namespace nacc {
 struct GridConst {
   int levels, res;
   float lo[8][3], hi[8][3], s[8][3];
-  double olo[3], ohi[3];  // outermost box padded by 1e-4*width + 1e-6 (fp64)
+  float olo[3], ohi[3];  // outermost box padded by 1e-4*width + 1e-6
 };
 
 struct MarchConst {
-  float near_plane, far_plane, step, max_step, cone;
+  float near_plane, far_plane, step, max_step, cone, inv_step;
   int stratified;
   uint32_t key0, key1;
 };
@@ -43,24 +43,31 @@ static GridConst make_grid_const(const nacc_grid &g) {
     const int L = g.levels - 1;
     const double w = (double)c.hi[L][a] - (double)c.lo[L][a];
     const double pad = 1e-4 * w + 1e-6;
-    c.olo[a] = (double)c.lo[L][a] - pad;
-    c.ohi[a] = (double)c.hi[L][a] + pad;
+    c.olo[a] = (float)((double)c.lo[L][a] - pad);
+    c.ohi[a] = (float)((double)c.hi[L][a] + pad);
   }
   return c;
 }
 
 // -------------------------------------------------------------------------- device
-__device__ __forceinline__ bool occupied(const GridConst &g, const uint32_t *__restrict__ bits,
-                                         float m, float ox, float oy, float oz, float dx, float dy,
-                                         float dz) {
+// kL1: single-level grid (the level search reduces to the box-0 test)
+template <bool kL1>
+__device__ __forceinline__ int level_of(const GridConst &g, float x, float y, float z) {
+  const int L = kL1 ? 1 : g.levels;
+  for (int l = 0; l < L; ++l)
+    if (g.lo[l][0] <= x && x < g.hi[l][0] && g.lo[l][1] <= y && y < g.hi[l][1] && g.lo[l][2] <= z &&
+        z < g.hi[l][2])
+      return l;
+  return -1;
+}
+
+// P(k) for the fp32 midpoint m (readings #2, #3): the normative op sequence
+template <bool kL1>
+__device__ __forceinline__ bool occupied(const GridConst &g, const uint32_t *__restrict__ bits, float m, float ox,
+                                         float oy, float oz, float dx, float dy, float dz) {
   const float x = __fmaf_rn(m, dx, ox), y = __fmaf_rn(m, dy, oy), z = __fmaf_rn(m, dz, oz);
-  int l = 0;
-  for (; l < g.levels; ++l) {
-    if (g.lo[l][0] <= x && x < g.hi[l][0] && g.lo[l][1] <= y && y < g.hi[l][1] &&
-        g.lo[l][2] <= z && z < g.hi[l][2])
-      break;
-  }
-  if (l == g.levels) return false;
+  const int l = level_of<kL1>(g, x, y, z);
+  if (l < 0) return false;
   const int R = g.res;
   int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[l][0]), g.s[l][0]));
   int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[l][1]), g.s[l][1]));
@@ -68,21 +75,105 @@ __device__ __forceinline__ bool occupied(const GridConst &g, const uint32_t *__r
   ix = min(max(ix, 0), R - 1);
   iy = min(max(iy, 0), R - 1);
   iz = min(max(iz, 0), R - 1);
-  const uint32_t q = (uint32_t)l * (uint32_t)(R * R * R) + (uint32_t)ix + (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
+  const uint32_t q = (uint32_t)l * (uint32_t)(R * R * R) + (uint32_t)ix +
+                     (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
   return (__ldg(bits + (q >> 5)) >> (q & 31u)) & 1u;
 }
 
+// ---------------------------------------------------------------- empty-space skipping
+// A segment of kSeg consecutive lattice points whose first and last midpoints
+// are A and B is skipped only if no point of it can be emitted: both ends lie
+// in the same level l, the segment's box does not reach the finer box l-1, and
+// the 2x2x2-macro-cell neighbourhood (macro = 4^3 fine cells) containing the
+// segment's bounding box holds no occupied cell.  Points of the segment lie on
+// the segment AB (monotone lattice), so they share its bounding box; positions
+// use the same fp32 ops as P(k) and a 1e-3 macro-cell margin covers rounding.
+constexpr int kSeg = 8;    // lattice points per segment
+constexpr int kMacro = 4;  // fine cells per macro cell and axis
+constexpr float kSegEps = 1e-3f;
+
+template <bool kL1>
+__device__ __forceinline__ bool segment_maybe_occupied(const GridConst &g, const uint32_t *__restrict__ mask2, int M,
+                                                       const float A[3], const float B[3]) {
+  const int la = level_of<kL1>(g, A[0], A[1], A[2]);
+  if (la < 0 || la != level_of<kL1>(g, B[0], B[1], B[2])) return true;
+  if (!kL1 && la >= 1) {
+    bool meets = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float lo = fminf(A[a], B[a]), hi = fmaxf(A[a], B[a]);
+      const float pad = kSegEps * (g.hi[la - 1][a] - g.lo[la - 1][a]);
+      meets = meets && hi >= g.lo[la - 1][a] - pad && lo <= g.hi[la - 1][a] + pad;
+    }
+    if (meets) return true;
+  }
+  int i0[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float sm = g.s[la][a] * (1.0f / kMacro);
+    const float ua = (A[a] - g.lo[la][a]) * sm, ub = (B[a] - g.lo[la][a]) * sm;
+    const int lo = (int)floorf(fminf(ua, ub) - kSegEps), hi = (int)floorf(fmaxf(ua, ub) + kSegEps);
+    if (hi - lo > 1) return true;
+    i0[a] = min(max(lo, 0), M - 1);
+  }
+  const uint32_t q = (uint32_t)la * (uint32_t)(M * M * M) + (uint32_t)i0[0] +
+                     (uint32_t)M * ((uint32_t)i0[1] + (uint32_t)M * (uint32_t)i0[2]);
+  return (__ldg(mask2 + (q >> 5)) >> (q & 31u)) & 1u;
+}
+
+// macro[l][m] = OR of the 4^3 fine bits of macro cell m
+__global__ void macro_or_kernel(const uint32_t *__restrict__ bits, int levels, int R, uint8_t *__restrict__ macro) {
+  const int M = R / kMacro;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= (int64_t)levels * M * M * M) return;
+  const int64_t M3 = (int64_t)M * M * M;
+  const int l = (int)(q / M3);
+  const int64_t m = q - l * M3;
+  const int mx = (int)(m % M), my = (int)((m / M) % M), mz = (int)(m / ((int64_t)M * M));
+  uint32_t acc = 0;
+  for (int dz = 0; dz < kMacro; ++dz)
+    for (int dy = 0; dy < kMacro; ++dy) {
+      const int64_t base = (int64_t)l * R * R * R + (int64_t)(mx * kMacro) +
+                           (int64_t)R * ((my * kMacro + dy) + (int64_t)R * (mz * kMacro + dz));
+      const uint32_t w = __ldg(bits + (base >> 5));
+      acc |= (w >> (base & 31)) & 0xFu;  // 4 consecutive x bits (base is a multiple of 4)
+    }
+  macro[q] = acc ? 1 : 0;
+}
+
+// mask2[l][m] = OR over macro cells m + {0,1}^3 (inside the level)
+__global__ void macro_dilate_kernel(const uint8_t *__restrict__ macro, int levels, int M, uint32_t *__restrict__ mask2) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t M3 = (int64_t)M * M * M, n = (int64_t)levels * M3;
+  bool on = false;
+  if (q < n) {
+    const int l = (int)(q / M3);
+    const int64_t m = q - l * M3;
+    const int mx = (int)(m % M), my = (int)((m / M) % M), mz = (int)(m / ((int64_t)M * M));
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dy = 0; dy < 2; ++dy)
+        for (int dx = 0; dx < 2; ++dx) {
+          const int x = mx + dx, y = my + dy, z = mz + dz;
+          if (x < M && y < M && z < M) on = on || macro[l * M3 + x + (int64_t)M * (y + (int64_t)M * z)];
+        }
+  }
+  const unsigned b = __ballot_sync(kFull, on);
+  if ((threadIdx.x & 31) == 0 && q < n) mask2[q >> 5] = b;
+}
+
+// ---------------------------------------------------------------- per-ray setup
 struct RaySetup {
-  float ox, oy, oz, dx, dy, dz, near_r, far_r;
+  float ox, oy, oz, dx, dy, dz, near_r, far_r, t_lo, t_hi;
   bool hit;
-  double t_lo, t_hi;
 };
 
+// The slab only bounds the k range (±2 steps of slack around the outermost box
+// padded by 1e-4 of its width), so fp32 with reciprocals is conservative
+// enough: its error (~1e-6 of t) is far below the slack.  P(k) decides.
 __device__ __forceinline__ RaySetup ray_setup(const GridConst &g, const MarchConst &p,
-                                              const float *__restrict__ rays_o,
-                                              const float *__restrict__ rays_d,
-                                              const float *__restrict__ t_min,
-                                              const float *__restrict__ t_max, int64_t r) {
+                                              const float *__restrict__ rays_o, const float *__restrict__ rays_d,
+                                              const float *__restrict__ t_min, const float *__restrict__ t_max,
+                                              int64_t r) {
   RaySetup s;
   s.ox = __ldg(rays_o + 3 * r);
   s.oy = __ldg(rays_o + 3 * r + 1);
@@ -92,52 +183,47 @@ __device__ __forceinline__ RaySetup ray_setup(const GridConst &g, const MarchCon
   s.dz = __ldg(rays_d + 3 * r + 2);
   float nr = t_min ? __ldg(t_min + r) : p.near_plane;
   if (p.stratified) {
-    const u32x4 rnd = philox4x32_10(u32x4{(uint32_t)(uint64_t)r, (uint32_t)((uint64_t)r >> 32), 0u, 0u}, p.key0, p.key1);
+    const u32x4 rnd =
+        philox4x32_10(u32x4{(uint32_t)(uint64_t)r, (uint32_t)((uint64_t)r >> 32), 0u, 0u}, p.key0, p.key1);
     nr = __double2float_rn(__dadd_rn((double)nr, __dmul_rn(u24(rnd.x), (double)p.step)));
   }
   s.near_r = nr;
   s.far_r = t_max ? __ldg(t_max + r) : p.far_plane;
-  // fp64 slab against the padded outermost box (conservative k range only)
-  const double o[3] = {s.ox, s.oy, s.oz}, d[3] = {s.dx, s.dy, s.dz};
-  double tmin = -INFINITY, tmax = INFINITY;
+  const float o[3] = {s.ox, s.oy, s.oz}, d[3] = {s.dx, s.dy, s.dz};
+  float tmin = -INFINITY, tmax = INFINITY;
   bool hit = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (d[a] != 0.0) {
-      double ta = (g.olo[a] - o[a]) / d[a], tb = (g.ohi[a] - o[a]) / d[a];
-      if (ta > tb) {
-        const double tt = ta;
-        ta = tb;
-        tb = tt;
-      }
-      tmin = fmax(tmin, ta);
-      tmax = fmin(tmax, tb);
+    if (fabsf(d[a]) > 1e-30f) {
+      const float inv = __frcp_rn(d[a]);
+      float ta = (g.olo[a] - o[a]) * inv, tb = (g.ohi[a] - o[a]) * inv;
+      tmin = fmaxf(tmin, fminf(ta, tb));
+      tmax = fminf(tmax, fmaxf(ta, tb));
     } else if (!(g.olo[a] <= o[a] && o[a] < g.ohi[a])) {
       hit = false;
     }
   }
-  s.t_lo = fmax(tmin, (double)s.near_r);
-  s.t_hi = fmin(tmax, (double)s.far_r);
+  s.t_lo = fmaxf(tmin, s.near_r);
+  s.t_hi = fminf(tmax, s.far_r);
   s.hit = hit && (s.t_hi > s.t_lo);
   return s;
 }
 
-// k range of the uniform lattice that can hold emitted intervals
-__device__ __forceinline__ void uniform_k_range(const RaySetup &s, float step, int64_t &kb, int64_t &ke) {
-  const double dt = (double)step, nr = (double)s.near_r;
-  const double fb = floor((s.t_lo - nr) / dt - 0.5) - 2.0;
-  const double fe = ceil((s.t_hi - nr) / dt) + 3.0;
-  kb = fb > 0.0 ? (int64_t)fb : 0;
-  const double cap = (double)(1 << 24);
-  ke = fe < cap ? (fe > 0.0 ? (int64_t)fe : 0) : (int64_t)(1 << 24);
+// k range of the uniform lattice that can hold emitted intervals (±2 slack)
+__device__ __forceinline__ void uniform_k_range(const RaySetup &s, const MarchConst &p, int64_t &kb, int64_t &ke) {
+  const float fb = floorf((s.t_lo - s.near_r) * p.inv_step - 0.5f) - 2.0f;
+  const float fe = ceilf((s.t_hi - s.near_r) * p.inv_step) + 3.0f;
+  const float cap = (float)(1 << 24);
+  kb = fb > 0.0f ? (int64_t)fminf(fb, cap) : 0;
+  ke = fe > 0.0f ? (int64_t)fminf(fe, cap) : 0;
 }
 
 // first index k in [0, K) with tab[k] >= v (tab ascending)
-__device__ __forceinline__ int64_t lower_bound(const float *__restrict__ tab, int64_t K, double v) {
+__device__ __forceinline__ int64_t lower_bound(const float *__restrict__ tab, int64_t K, float v) {
   int64_t lo = 0, hi = K;
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    if ((double)__ldg(tab + mid) < v) lo = mid + 1;
+    if (__ldg(tab + mid) < v) lo = mid + 1;
     else hi = mid;
   }
   return lo;
@@ -160,7 +246,7 @@ __global__ void cone_tcap_kernel(GridConst g, MarchConst p, const float *__restr
   float v = 0.0f;
   if (r < n_rays) {
     RaySetup s = ray_setup(g, p, rays_o, rays_d, nullptr, t_max, r);
-    if (s.hit) v = (float)s.t_hi;
+    if (s.hit) v = s.t_hi;
   }
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
   if ((threadIdx.x & 31) == 0 && v > 0.0f) atomicMax(&hdr->t_cap_bits, __float_as_uint(v));
@@ -192,110 +278,341 @@ __global__ void cone_table_kernel(MarchConst p, ConeHeader *hdr, float *__restri
   hdr->overflow = overflow;
 }
 
-template <bool kCone, bool kFill>
-__global__ void __launch_bounds__(256) march_kernel(GridConst g, MarchConst p,
-                                                    const uint32_t *__restrict__ bits,
-                                                    const float *__restrict__ rays_o,
-                                                    const float *__restrict__ rays_d,
-                                                    const float *__restrict__ t_min,
-                                                    const float *__restrict__ t_max, int64_t n_rays,
-                                                    const ConeHeader *__restrict__ hdr,
-                                                    const float *__restrict__ tab,
-                                                    int32_t *__restrict__ counts,
-                                                    const int64_t *__restrict__ packed_info,
-                                                    const int64_t *__restrict__ total, int64_t capacity,
-                                                    float *__restrict__ t0, float *__restrict__ t1,
-                                                    int32_t *__restrict__ ray_id) {
+// midpoint of lattice interval k (uniform or cone table)
+template <bool kCone>
+__device__ __forceinline__ float lattice_mid(const MarchConst &p, const RaySetup &s, const float *__restrict__ tab,
+                                             int k) {
+  if (kCone) {
+    const float ta = __ldg(tab + k);
+    const float dt = fminf(fmaxf(__fmul_rn(ta, p.cone), p.step), p.max_step);
+    return __fadd_rn(ta, __fmul_rn(0.5f, dt));
+  }
+  return __fmaf_rn((float)k + 0.5f, p.step, s.near_r);
+}
+
+template <bool kCone>
+__device__ __forceinline__ void lattice_ends(const MarchConst &p, float near_r, const float *__restrict__ tab,
+                                             int k, float &ta, float &tb) {
+  if (kCone) {
+    ta = __ldg(tab + k);
+    tb = __ldg(tab + k + 1);
+  } else {
+    ta = __fmaf_rn((float)k, p.step, near_r);
+    tb = __fmaf_rn((float)(k + 1), p.step, near_r);
+  }
+}
+
+// Traverse one ray with one warp.  Each step the 32 lanes test 32 segments of
+// kSeg lattice points (kSkip), the flagged segments are compacted through the
+// warp's shared `seglist` and evaluated exactly, 4 segments = 32 points per
+// pass, in increasing k.  emit(ballot, pred, k) is called once per pass by all
+// lanes.  Returns the ray's count.
+template <bool kCone, bool kSkip, bool kL1, typename Emit>
+__device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchConst &p,
+                                                const uint32_t *__restrict__ bits,
+                                                const uint32_t *__restrict__ mask2, int M, const RaySetup &s,
+                                                const ConeHeader *__restrict__ hdr, const float *__restrict__ tab,
+                                                int *seglist, int &kb_out, int &ke_out, Emit emit) {
+  const int lane = threadIdx.x & 31;
+  int32_t cnt = 0;
+  kb_out = ke_out = 0;
+  if (!s.hit) return 0;
+  int kb, ke;  // lattice indices are < 2^24 (fp32-exact), so int32 throughout
+  if (kCone) {
+    const int K = (int)hdr->K;
+    kb = (int)lower_bound(tab + 1, K, s.t_lo) - 2;  // first k with t_{k+1} >= t_lo, minus slack
+    if (kb < 0) kb = 0;
+    ke = (int)lower_bound(tab, K + 1, s.t_hi) + 2;  // first k with t_k >= t_hi, plus slack
+    if (ke > K) ke = K;
+  } else {
+    int64_t b64, e64;
+    uniform_k_range(s, p, b64, e64);
+    kb = (int)b64;
+    ke = (int)e64;
+  }
+  kb_out = kb;
+  ke_out = ke;
+  constexpr int kSpan = kSkip ? 32 * kSeg : 32;
+  for (int k0 = kb; k0 < ke; k0 += kSpan) {
+    int nseg = 1;
+    if (kSkip) {
+      const int ks = k0 + lane * kSeg;
+      bool flag = false;
+      if (ks < ke) {
+        const int kl = min(ks + kSeg - 1, ke - 1);
+        const float ma = lattice_mid<kCone>(p, s, tab, ks), mb = lattice_mid<kCone>(p, s, tab, kl);
+        const float A[3] = {__fmaf_rn(ma, s.dx, s.ox), __fmaf_rn(ma, s.dy, s.oy), __fmaf_rn(ma, s.dz, s.oz)};
+        const float B[3] = {__fmaf_rn(mb, s.dx, s.ox), __fmaf_rn(mb, s.dy, s.oy), __fmaf_rn(mb, s.dz, s.oz)};
+        flag = segment_maybe_occupied<kL1>(g, mask2, M, A, B);
+      }
+      const unsigned F = __ballot_sync(kFull, flag);
+      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane;
+      __syncwarp();
+      nseg = __popc(F);
+    }
+    for (int first = 0; first < nseg; first += 4) {
+      int k;
+      if (kSkip) {
+        const int idx = first + (lane >> 3);
+        k = idx < nseg ? k0 + seglist[idx] * kSeg + (lane & 7) : ke;
+      } else {
+        k = k0 + lane;
+      }
+      bool pred = false;
+      if (k < ke) {
+        const float m = lattice_mid<kCone>(p, s, tab, k);
+        pred = (m < s.far_r) && occupied<kL1>(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz);
+      }
+      const unsigned b = __ballot_sync(kFull, pred);
+      emit(b, pred, k, cnt);
+      cnt += __popc(b);
+    }
+    if (kSkip) __syncwarp();
+  }
+  return cnt;
+}
+
+// ---------------------------------------------------------------- fused single-pass march
+// Tile = 4 warps x 4 rays.  Phase 1 traverses the tile's rays once, keeping
+// each ray's emitted lattice indices (as 16-bit offsets from the ray's first
+// candidate index) in the warp's shared k-list; the tile's count is published
+// and its output offset found by a warp-wide decoupled look-back over the
+// preceding tiles; phase 2 writes packed_info and, when the total fits the
+// capacity, the samples from the k-lists with coalesced stores.  A ray whose
+// k-list overflowed is traversed again in phase 2, writing directly.
+constexpr int kFWarps = 4, kFRaysPerWarp = 4, kFTileRays = kFWarps * kFRaysPerWarp, kFKCap = 2048;
+
+struct LookbackWs {
+  unsigned int tile_counter;
+  unsigned int pad;
+  unsigned long long status[1];  // [n_tiles]: (value << 2) | flag, flag 1 = aggregate, 2 = inclusive prefix
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// warp 0: publish this tile's aggregate and return its exclusive prefix
+__device__ __forceinline__ long long lookback(unsigned long long *st, int64_t tile, long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release(st, ((unsigned long long)agg << 2) | 2ull);
+    return 0;
+  }
+  if (lane == 0) st_release(st + tile, ((unsigned long long)agg << 2) | 1ull);
+  long long excl = 0;
+  int64_t j = tile - 1;  // lanes look at tiles j, j-1, ..., j-31
+  for (;;) {
+    const int64_t idx = j - lane;
+    unsigned long long w = idx >= 0 ? 0ull : 2ull;  // before tile 0: an inclusive prefix of 0
+    if (idx >= 0) {
+      do {
+        w = ld_acquire(st + idx);
+      } while ((w & 3ull) == 0ull);
+    }
+    const unsigned m2 = __ballot_sync(kFull, (w & 3ull) == 2ull);
+    const int last = m2 ? __ffs(m2) - 1 : 31;  // nearest predecessor with an inclusive prefix
+    long long v = lane <= last ? (long long)(w >> 2) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    excl += v;
+    if (m2) break;
+    j -= 32;
+  }
+  if (lane == 0) st_release(st + tile, ((unsigned long long)(excl + agg) << 2) | 2ull);
+  return excl;
+}
+
+template <bool kCone, bool kSkip, bool kL1>
+__global__ void __launch_bounds__(kFWarps * 32) march_fused_kernel(
+    GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
+    const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
+    const float *__restrict__ t_max, int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr,
+    const float *__restrict__ tab, LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info,
+    int64_t *__restrict__ total, int64_t capacity, int32_t *__restrict__ status_out, float *__restrict__ t0,
+    float *__restrict__ t1, int32_t *__restrict__ ray_id) {
+  __shared__ uint16_t kbuf[kFWarps][kFKCap];
+  __shared__ int seglist[kFWarps][32];
+  __shared__ int32_t s_cnt[kFTileRays];
+  __shared__ int32_t s_kb[kFTileRays];
+  __shared__ int32_t s_lpos[kFTileRays];  // start of the ray's k-list in kbuf[warp], -1 if unusable
+  __shared__ float s_near[kFTileRays];
+  __shared__ unsigned int s_tile;
+  __shared__ long long s_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&lb->tile_counter, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t r_base = tile * kFTileRays;
+  // ---- phase 1: traverse, keep k-lists
+  int pos = 0;  // warp-uniform fill level of kbuf[warp]; kFKCap + 1 once it overflowed
+#pragma unroll 1
+  for (int j = 0; j < kFRaysPerWarp; ++j) {
+    const int slot = warp * kFRaysPerWarp + j;
+    const int64_t r = r_base + slot;
+    int32_t c = 0;
+    int kb = 0, lpos = -1;
+    if (r < n_rays) {
+      const RaySetup s = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r);
+      const int start = pos;
+      int kb0 = 0, ke0 = 0;
+      c = traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+                                           [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                             const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
+                                             const int off = k - kb0;
+                                             if (pred && q < kFKCap && off < 65536) kbuf[warp][q] = (uint16_t)off;
+                                           });
+      kb = kb0;
+      if (lane == 0) s_near[slot] = s.near_r;
+      // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
+      const bool usable = start + c <= kFKCap && ke0 - kb0 <= 65536;
+      lpos = usable ? start : -1;
+      pos = usable ? start + c : kFKCap + 1;
+    }
+    if (lane == 0) {
+      s_cnt[slot] = c;
+      s_kb[slot] = kb;
+      s_lpos[slot] = lpos;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const long long agg = warp_sum_i64(lane < kFTileRays ? (int64_t)s_cnt[lane] : 0);
+    const long long excl = lookback(lb->status, tile, agg);
+    if (lane == 0) {
+      s_prefix = excl;
+      if (tile == n_tiles - 1) {
+        *total = excl + agg;
+        if (status_out) {
+          int32_t stt = (excl + agg > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
+          if (hdr && hdr->overflow) stt = NACC_ERR_UNSUPPORTED;
+          *status_out = stt;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- phase 2: packed_info and samples (each warp handles its own rays)
+  int64_t run = s_prefix;
+  for (int slot = 0; slot < warp * kFRaysPerWarp; ++slot) run += s_cnt[slot];
+#pragma unroll 1
+  for (int j = 0; j < kFRaysPerWarp; ++j) {
+    const int slot = warp * kFRaysPerWarp + j;
+    const int64_t r = r_base + slot;
+    if (r >= n_rays) break;
+    const int32_t c = s_cnt[slot];
+    if (lane == 0) reinterpret_cast<longlong2 *>(packed_info)[r] = make_longlong2(run, c);
+    if (t0 != nullptr && run + c <= capacity && c > 0) {
+      const int lpos = s_lpos[slot];
+      if (lpos >= 0) {
+        const int kb = s_kb[slot];
+        const float nr = s_near[slot];
+        for (int i = lane; i < c; i += 32) {
+          const int k = kb + (int)kbuf[warp][lpos + i];
+          float ta, tb;
+          lattice_ends<kCone>(p, nr, tab, k, ta, tb);
+          t0[run + i] = ta;
+          t1[run + i] = tb;
+          ray_id[run + i] = (int32_t)r;
+        }
+      } else {  // k-list overflowed: traverse again, writing directly
+        const RaySetup s = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r);
+        const int64_t base = run;
+        int kb0, ke0;
+        traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+                                        [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                          if (pred) {
+                                            const int64_t q = base + cnt + __popc(b & ((1u << lane) - 1u));
+                                            float ta, tb;
+                                            lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb);
+                                            t0[q] = ta;
+                                            t1[q] = tb;
+                                            ray_id[q] = (int32_t)r;
+                                          }
+                                        });
+      }
+    }
+    run += c;
+  }
+}
+
+// ---------------------------------------------------------------- fill from a given packed_info
+template <bool kCone, bool kSkip, bool kL1>
+__global__ void __launch_bounds__(256) march_fill_kernel(GridConst g, MarchConst p, const uint32_t *__restrict__ bits,
+                                                         const uint32_t *__restrict__ mask2, int M,
+                                                         const float *__restrict__ rays_o,
+                                                         const float *__restrict__ rays_d,
+                                                         const float *__restrict__ t_min,
+                                                         const float *__restrict__ t_max, int64_t n_rays,
+                                                         const ConeHeader *__restrict__ hdr,
+                                                         const float *__restrict__ tab,
+                                                         const int64_t *__restrict__ packed_info,
+                                                         float *__restrict__ t0, float *__restrict__ t1,
+                                                         int32_t *__restrict__ ray_id) {
+  __shared__ int seglist[8][32];
   const int lane = threadIdx.x & 31;
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= n_rays) return;
-  if (kFill && total && *total > capacity) return;
-  int64_t out = 0;
-  if (kFill) out = packed_info[2 * r];
-  int32_t cnt = 0;
+  const int64_t out = packed_info[2 * r];
   const RaySetup s = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r);
-  if (s.hit) {
-    int64_t kb, ke;
-    if (kCone) {
-      const int64_t K = hdr->K;
-      kb = lower_bound(tab + 1, K, s.t_lo) - 2;  // first k with t_{k+1} >= t_lo, minus slack
-      if (kb < 0) kb = 0;
-      ke = lower_bound(tab, K + 1, s.t_hi) + 2;  // first k with t_k >= t_hi, plus slack
-      if (ke > K) ke = K;
-    } else {
-      uniform_k_range(s, p.step, kb, ke);
-    }
-    for (int64_t k0 = kb; k0 < ke; k0 += 32) {
-      const int64_t k = k0 + lane;
-      bool pred = false, stop = false;
-      float ta = 0.f, tb = 0.f;
-      if (k < ke) {
-        float m;
-        if (kCone) {
-          ta = __ldg(tab + k);
-          tb = __ldg(tab + k + 1);
-          const float dt = fminf(fmaxf(__fmul_rn(ta, p.cone), p.step), p.max_step);
-          m = __fadd_rn(ta, __fmul_rn(0.5f, dt));
-        } else {
-          m = __fmaf_rn((float)k + 0.5f, p.step, s.near_r);
-        }
-        if (!(m < s.far_r)) stop = true;
-        else pred = occupied(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz);
-      }
-      const unsigned b = __ballot_sync(kFull, pred);
-      if (kFill && pred) {
-        if (!kCone) {
-          ta = __fmaf_rn((float)k, p.step, s.near_r);
-          tb = __fmaf_rn((float)(k + 1), p.step, s.near_r);
-        }
-        const int64_t q = out + cnt + __popc(b & ((1u << lane) - 1u));
-        t0[q] = ta;
-        t1[q] = tb;
-        ray_id[q] = (int32_t)r;
-      }
-      cnt += __popc(b);
-      if (__any_sync(kFull, stop)) break;
-    }
-  }
-  if (!kFill && lane == 0) counts[r] = cnt;
-}
-
-__global__ void capacity_status_kernel(const int64_t *total, int64_t capacity, const ConeHeader *hdr,
-                                       int32_t *status) {
-  int32_t st = (*total > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
-  if (hdr && hdr->overflow) st = NACC_ERR_UNSUPPORTED;
-  *status = st;
+  int kb0, ke0;
+  traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[threadIdx.x >> 5], kb0, ke0,
+                                  [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                    if (pred) {
+                                      const int64_t q = out + cnt + __popc(b & ((1u << lane) - 1u));
+                                      float ta, tb;
+                                      lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb);
+                                      t0[q] = ta;
+                                      t1[q] = tb;
+                                      ray_id[q] = (int32_t)r;
+                                    }
+                                  });
 }
 
 // -------------------------------------------------------------------------- host
 struct MarchWs {
-  int32_t *counts;
-  void *scan_ws;
+  LookbackWs *lb;
   ConeHeader *hdr;
   float *tab;
+  uint8_t *macro;
+  uint32_t *mask2;
 };
 
-static size_t march_ws_layout(const nacc_march &p, int64_t n, MarchWs *w, void *base) {
+static bool skip_enabled(const nacc_grid &g) { return g.res % kMacro == 0 && g.res >= 2 * kMacro; }
+static int64_t fused_tiles(int64_t n) { return ceil_div(n, kFTileRays); }
+
+static size_t march_ws_layout(const nacc_grid &g, const nacc_march &p, int64_t n, MarchWs *w, void *base) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off += align_up(bytes, 256);
     return o;
   };
-  const size_t o_counts = take((size_t)n * 4);
-  const size_t o_scan = take(scan_workspace_bytes(n));
-  size_t o_hdr = 0, o_tab = 0;
+  const size_t o_lb = take(8 + 8 * (size_t)fused_tiles(n));
+  size_t o_hdr = 0, o_tab = 0, o_macro = 0, o_mask = 0;
   const bool cone = p.cone_angle > 0.0f;
   if (cone) {
     o_hdr = take(sizeof(ConeHeader));
     o_tab = take((size_t)(kConeTableMax + 1) * 4);
   }
+  const bool skip = skip_enabled(g);
+  if (skip) {
+    const int64_t M = g.res / kMacro, n_m = (int64_t)g.levels * M * M * M;
+    o_macro = take((size_t)n_m);
+    o_mask = take((size_t)ceil_div(n_m, 32) * 4);
+  }
   if (w && base) {
     char *b = static_cast<char *>(base);
-    w->counts = reinterpret_cast<int32_t *>(b + o_counts);
-    w->scan_ws = b + o_scan;
+    w->lb = reinterpret_cast<LookbackWs *>(b + o_lb);
     w->hdr = cone ? reinterpret_cast<ConeHeader *>(b + o_hdr) : nullptr;
     w->tab = cone ? reinterpret_cast<float *>(b + o_tab) : nullptr;
+    w->macro = skip ? reinterpret_cast<uint8_t *>(b + o_macro) : nullptr;
+    w->mask2 = skip ? reinterpret_cast<uint32_t *>(b + o_mask) : nullptr;
   }
   return off;
 }
@@ -333,57 +650,65 @@ static MarchConst make_march_const(const nacc_march &p) {
   m.step = p.step;
   m.max_step = p.max_step;
   m.cone = p.cone_angle;
+  m.inv_step = 1.0f / p.step;
   m.stratified = p.stratified;
   m.key0 = (uint32_t)(p.seed & 0xffffffffu);
   m.key1 = (uint32_t)(p.seed >> 32);
   return m;
 }
 
+#define NACC_DISPATCH3(KERNEL, GRID, BLOCK, STREAM, ...)                                         \
+  do {                                                                                           \
+    if (cone && skip && l1) KERNEL<true, true, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);     \
+    else if (cone && skip) KERNEL<true, true, false><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);     \
+    else if (cone && l1) KERNEL<true, false, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);       \
+    else if (cone) KERNEL<true, false, false><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);            \
+    else if (skip && l1) KERNEL<false, true, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);       \
+    else if (skip) KERNEL<false, true, false><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);            \
+    else if (l1) KERNEL<false, false, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);              \
+    else KERNEL<false, false, false><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);                     \
+  } while (0)
+
 static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t *bits,
                                 const nacc_march *params, const float *rays_o, const float *rays_d,
                                 const float *t_min, const float *t_max, int64_t n_rays,
                                 int64_t *packed_info, float *t0, float *t1, int32_t *ray_id,
                                 int64_t capacity, int64_t *total, int32_t *status_out, void *ws,
-                                cudaStream_t stream, bool build_table) {
+                                cudaStream_t stream) {
   MarchWs w;
-  march_ws_layout(*params, n_rays, &w, ws);
+  march_ws_layout(*grid, *params, n_rays, &w, ws);
   const GridConst g = make_grid_const(*grid);
   const MarchConst p = make_march_const(*params);
   const bool cone = params->cone_angle > 0.0f;
-  if (cone && build_table) {
+  const bool skip = skip_enabled(*grid);
+  const bool l1 = grid->levels == 1;
+  const int M = grid->res / kMacro;
+  if (cone) {  // shared cone lattice table (reading #5)
     NACC_CUDA(cudaMemsetAsync(w.hdr, 0, sizeof(ConeHeader), stream));
     cone_tcap_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(g, p, rays_o, rays_d, t_max, n_rays, w.hdr);
     cone_table_kernel<<<1, 32, 0, stream>>>(p, w.hdr, w.tab);
     count_launch(2);
     NACC_CHECK_LAUNCH();
   }
-  const int blocks = grid_for(n_rays * 32, 256);
+  if (skip) {  // macro-cell occupancy for empty-space skipping (rebuilt from the bits every call)
+    const int64_t n_m = (int64_t)grid->levels * M * M * M;
+    macro_or_kernel<<<grid_for(n_m, 256), 256, 0, stream>>>(bits, grid->levels, grid->res, w.macro);
+    macro_dilate_kernel<<<grid_for(n_m, 256), 256, 0, stream>>>(w.macro, grid->levels, M, w.mask2);
+    count_launch(2);
+    NACC_CHECK_LAUNCH();
+  }
   if (!fill) {
-    if (cone)
-      march_kernel<true, false><<<blocks, 256, 0, stream>>>(g, p, bits, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab,
-                                                            w.counts, nullptr, nullptr, 0, nullptr, nullptr, nullptr);
-    else
-      march_kernel<false, false><<<blocks, 256, 0, stream>>>(g, p, bits, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab,
-                                                             w.counts, nullptr, nullptr, 0, nullptr, nullptr, nullptr);
-    count_launch(1);
-    NACC_CHECK_LAUNCH();
-    NACC_CUDA(scan_counts_to_packed(w.counts, n_rays, packed_info, total, w.scan_ws, stream));
-    if (status_out) {
-      capacity_status_kernel<<<1, 1, 0, stream>>>(total, capacity, w.hdr, status_out);
-      count_launch(1);
-    }
-    NACC_CHECK_LAUNCH();
+    const int64_t n_tiles = fused_tiles(n_rays);
+    NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
+    NACC_DISPATCH3(march_fused_kernel, (unsigned)n_tiles, kFWarps * 32, stream, g, p, bits, w.mask2, M, rays_o,
+                   rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,
+                   status_out, t0, t1, ray_id);
+  } else {
+    NACC_DISPATCH3(march_fill_kernel, (unsigned)grid_for(n_rays * 32, 256), 256, stream, g, p, bits, w.mask2, M,
+                   rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, packed_info, t0, t1, ray_id);
   }
-  if (t0 && t1 && ray_id) {
-    if (cone)
-      march_kernel<true, true><<<blocks, 256, 0, stream>>>(g, p, bits, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab,
-                                                           nullptr, packed_info, fill ? nullptr : total, capacity, t0, t1, ray_id);
-    else
-      march_kernel<false, true><<<blocks, 256, 0, stream>>>(g, p, bits, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab,
-                                                            nullptr, packed_info, fill ? nullptr : total, capacity, t0, t1, ray_id);
-    count_launch(1);
-    NACC_CHECK_LAUNCH();
-  }
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
   return NACC_OK;
 }
 
@@ -396,7 +721,7 @@ extern "C" {
 size_t nacc_sampling_occgrid_workspace_bytes(const nacc_grid *grid, const nacc_march *params,
                                              int64_t n_rays) {
   if (!grid || !params || n_rays < 0) return 0;
-  return march_ws_layout(*params, n_rays, nullptr, nullptr);
+  return march_ws_layout(*grid, *params, n_rays, nullptr, nullptr);
 }
 
 nacc_status nacc_sampling_occgrid(const nacc_grid *grid, const uint32_t *bits, const nacc_march *params,
@@ -416,7 +741,7 @@ nacc_status nacc_sampling_occgrid(const nacc_grid *grid, const uint32_t *bits, c
   NACC_REQUIRE(packed_info && aligned(packed_info, 16), "packed_info must be non-NULL and 16-byte aligned");
   NACC_REQUIRE((!t0 && !t1 && !ray_id) || (t0 && t1 && ray_id), "t0, t1, ray_id: all or none");
   return launch_march(false, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays, packed_info, t0, t1,
-                      ray_id, capacity, total, status_out, ws, stream, true);
+                      ray_id, capacity, total, status_out, ws, stream);
 }
 
 nacc_status nacc_sampling_occgrid_fill(const nacc_grid *grid, const uint32_t *bits, const nacc_march *params,
@@ -429,10 +754,9 @@ nacc_status nacc_sampling_occgrid_fill(const nacc_grid *grid, const uint32_t *bi
   if (st != NACC_OK) return st;
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(packed_info && t0 && t1 && ray_id, "packed_info, t0, t1, ray_id must be non-NULL");
-  // the cone table lives in the workspace of the preceding nacc_sampling_occgrid call; rebuild it
+  // the cone table and macro mask live in the workspace; they are rebuilt here
   return launch_march(true, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays,
-                      const_cast<int64_t *>(packed_info), t0, t1, ray_id, 0, nullptr, nullptr, ws, stream,
-                      true);
+                      const_cast<int64_t *>(packed_info), t0, t1, ray_id, 0, nullptr, nullptr, ws, stream);
 }
 
 }  // extern "C"

@@ -7,8 +7,10 @@
 //   g_σ_i = δ_i (g_w_i T_i (1-α_i) - Σ_{j>i} g_w_j w_j) for live samples,
 // with Σ_{j>i} g_w_j w_j = R - Σ_{j<=i} g_w_j w_j and R = <g_C,C> + g_O' O + g_N N
 // taken from the forward's fp64 per-ray sums (ctx), so one forward-order pass
-// suffices.  One warp per ray; 32 consecutive samples per step.
+// suffices.  Fused path: flat ray-aligned tiles (segscan.cuh); granular and
+// fallback paths: one warp per ray, 32 consecutive samples per step.
 #include "common.cuh"
+#include "segscan.cuh"
 
 namespace nacc {
 
@@ -46,8 +48,10 @@ __device__ __forceinline__ Chunk load_chunk(const float *__restrict__ t0, const 
   return c;
 }
 
-__device__ __forceinline__ float trans_of(double S) { return expf(-(float)S); }
-__device__ __forceinline__ float alpha_of(double s) { return -expm1f(-(float)s); }
+// fp64: the depth gradient divides by the opacity, so weights must carry
+// fp64 precision for the backward's R - P_i difference
+__device__ __forceinline__ double trans_of(double S) { return exp(-S); }
+__device__ __forceinline__ double alpha_of(double s) { return -expm1(-s); }
 
 // ------------------------------------------------------------------ fused forward
 __global__ void __launch_bounds__(256) render_fwd_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(256) render_fwd_kernel(const int64_t *__restri
   for (int64_t base = 0; base < cnt; base += 32) {
     const Chunk c = load_chunk(t0, t1, sigma, st, cnt, base, L, carry);
     if (c.live) {
-      const double w = (double)(trans_of(c.S) * alpha_of(c.s));
+      const double w = trans_of(c.S) * alpha_of(c.s);
       const int64_t q = st + base + lane;
       if (rgb) {
         C0 += w * (double)__ldg(rgb + 3 * q);
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(const int64_t *__restri
     for (int64_t base = 0; base < cnt; base += 32) {
       const Chunk c = load_chunk(t0, t1, sigma, st, cnt, base, L, carry);
       if (c.live) {
-        const double w = (double)(trans_of(c.S) * alpha_of(c.s));
+        const double w = trans_of(c.S) * alpha_of(c.s);
         const int64_t q = st + base + lane;
         if (rgb) {
           C0 += w * (double)__ldg(rgb + 3 * q);
@@ -177,12 +181,12 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(const int64_t *__restri
       continue;
     }
     const Chunk c = load_chunk(t0, t1, sigma, st, cnt, base, L, carry);
-    double gw = 0.0, w = 0.0;
-    float r0 = 0.f, r1 = 0.f, r2 = 0.f, T = 0.f, ea = 0.f;
+    double gw = 0.0, w = 0.0, T = 0.0, ea = 0.0;
+    float r0 = 0.f, r1 = 0.f, r2 = 0.f;
     if (c.live) {
       T = trans_of(c.S);
-      ea = expf(-(float)c.s);  // 1 - α
-      w = (double)(T * alpha_of(c.s));
+      ea = exp(-c.s);  // 1 - α
+      w = T * alpha_of(c.s);
       if (rgb) {
         r0 = __ldg(rgb + 3 * q);
         r1 = __ldg(rgb + 3 * q + 1);
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(const int64_t *__restri
     const double Q = R - (P + incl);  // Σ_{j>i} g_w_j w_j
     P += __shfl_sync(kFull, incl, 31);
     if (c.valid) {
-      const double gs = c.live ? gw * (double)T * (double)ea - Q : 0.0;
+      const double gs = c.live ? gw * T * ea - Q : 0.0;
       g_sigma[q] = (float)(c.delta * gs);
       if (g_rgb) {
         g_rgb[3 * q] = (float)(w * gc0);
@@ -204,6 +208,561 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(const int64_t *__restri
       }
     }
     dead = carry > L;
+  }
+}
+
+// ------------------------------------------------------------------ flat (ray-aligned tiles) fused render
+// Blocks own ray-aligned sample ranges [B, E) of ~kTile samples and walk them in
+// chunks of 256 threads x 4 consecutive samples; the open ray is carried across
+// chunks (segscan.cuh).  Per-ray outputs are written by the ray's last sample;
+// extra blocks past the tiles zero the outputs of rays without samples.
+constexpr int kFlatThreads = 256, kFlatItems = 4, kFlatWarps = kFlatThreads / 32;
+constexpr int kFlatChunk = kFlatThreads * kFlatItems;
+constexpr int64_t kFlatTile = 2048;
+
+struct Items {
+  int64_t q0;
+  bool valid[4], head[4], tail[4];
+  float t0[4], t1[4], sg[4];
+  int32_t rid[4];
+};
+
+template <bool kVec>
+__device__ __forceinline__ void load_items(Items &it, int64_t c0, int64_t B, int64_t E, const float *__restrict__ t0,
+                                           const float *__restrict__ t1, const float *__restrict__ sigma,
+                                           const int32_t *__restrict__ ray_id) {
+  const int64_t q0 = c0 + (int64_t)threadIdx.x * kFlatItems;
+  it.q0 = q0;
+  const bool full = kVec && q0 >= B && q0 + 3 < E;
+  if (full) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(t0 + q0));
+    const float4 b = __ldg(reinterpret_cast<const float4 *>(t1 + q0));
+    const float4 c = __ldg(reinterpret_cast<const float4 *>(sigma + q0));
+    const int4 d = __ldg(reinterpret_cast<const int4 *>(ray_id + q0));
+    it.t0[0] = a.x; it.t0[1] = a.y; it.t0[2] = a.z; it.t0[3] = a.w;
+    it.t1[0] = b.x; it.t1[1] = b.y; it.t1[2] = b.z; it.t1[3] = b.w;
+    it.sg[0] = c.x; it.sg[1] = c.y; it.sg[2] = c.z; it.sg[3] = c.w;
+    it.rid[0] = d.x; it.rid[1] = d.y; it.rid[2] = d.z; it.rid[3] = d.w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) it.valid[j] = true;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = q0 + j;
+      it.valid[j] = q >= B && q < E;
+      it.t0[j] = it.valid[j] ? __ldg(t0 + q) : 0.f;
+      it.t1[j] = it.valid[j] ? __ldg(t1 + q) : 0.f;
+      it.sg[j] = it.valid[j] ? __ldg(sigma + q) : 0.f;
+      it.rid[j] = it.valid[j] ? __ldg(ray_id + q) : -1;
+    }
+  }
+  const int32_t prev = (q0 - 1 >= B && q0 - 1 < E) ? __ldg(ray_id + q0 - 1) : -1;
+  const int32_t next = (q0 + 4 >= B && q0 + 4 < E) ? __ldg(ray_id + q0 + 4) : -2;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int32_t pr = j == 0 ? prev : it.rid[j - 1];
+    const int32_t nx = j == 3 ? next : (it.valid[j + 1] ? it.rid[j + 1] : -2);
+    it.head[j] = it.valid[j] && (q0 + j == B || it.rid[j] != pr);
+    it.tail[j] = it.valid[j] && (q0 + j + 1 == E || it.rid[j] != nx);
+  }
+}
+
+// entering optical depth S_j of the thread's items (fp64 segmented exclusive scan)
+__device__ __forceinline__ void items_optical_depth(const Items &it, double s[4], double S[4], Seg<1> &carry,
+                                                    Seg<1> *smem) {
+  Seg<1> agg = seg_identity<1>();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    s[j] = it.valid[j] ? (double)it.sg[j] * ((double)it.t1[j] - (double)it.t0[j]) : 0.0;
+    Seg<1> x;
+    x.f = it.head[j];
+    x.v[0] = s[j];
+    agg = seg_combine(agg, x);
+  }
+  Seg<1> run = block_seg_excl<1, kFlatWarps>(agg, carry, smem);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    S[j] = it.head[j] ? 0.0 : run.v[0];
+    Seg<1> x;
+    x.f = it.head[j];
+    x.v[0] = s[j];
+    run = seg_combine(run, x);
+  }
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(kFlatThreads) render_fwd_flat_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t N,
+    int64_t n_tiles, const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
+    const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
+    float *__restrict__ depth, double *__restrict__ ctx) {
+  __shared__ Seg<1> smS[kFlatWarps + 1];
+  __shared__ Seg<5> smC[kFlatWarps + 1];
+  if ((int64_t)blockIdx.x >= n_tiles) {  // rays without samples
+    const int64_t r = ((int64_t)blockIdx.x - n_tiles) * kFlatThreads + threadIdx.x;
+    if (r < n_rays && packed_info[2 * r + 1] == 0) {
+      if (color) { color[3 * r] = 0.f; color[3 * r + 1] = 0.f; color[3 * r + 2] = 0.f; }
+      if (opacity) opacity[r] = 0.f;
+      if (depth) depth[r] = 0.f;
+      if (ctx) for (int k = 0; k < 5; ++k) ctx[5 * r + k] = 0.0;
+    }
+    return;
+  }
+  N = packed_end(packed_info, n_rays);  // samples in use (the arrays may be a larger capacity)
+  const int64_t B = snap_to_ray(packed_info, ray_id, (int64_t)blockIdx.x * kFlatTile, N);
+  const int64_t E = snap_to_ray(packed_info, ray_id, ((int64_t)blockIdx.x + 1) * kFlatTile, N);
+  if (B >= E) return;
+  Seg<1> carryS = seg_identity<1>();
+  Seg<5> carryC = seg_identity<5>();
+  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kFlatChunk) {
+    Items it;
+    load_items<kVec>(it, c0, B, E, t0, t1, sigma, ray_id);
+    double s[4], S[4];
+    items_optical_depth(it, s, S, carryS, smS);
+    float col[12];
+    const bool full = kVec && it.valid[0] && it.valid[3];
+    if (full) {
+      const float4 *p = reinterpret_cast<const float4 *>(rgb + 3 * it.q0);
+      const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+      col[0] = a.x; col[1] = a.y; col[2] = a.z; col[3] = a.w; col[4] = b.x; col[5] = b.y;
+      col[6] = b.z; col[7] = b.w; col[8] = c.x; col[9] = c.y; col[10] = c.z; col[11] = c.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) col[3 * j + ch] = it.valid[j] ? __ldg(rgb + 3 * (it.q0 + j) + ch) : 0.f;
+    }
+    Seg<5> items[4];
+    Seg<5> agg = seg_identity<5>();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool live = it.valid[j] && !(S[j] > L);
+      const double w = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
+      items[j].f = it.head[j];
+      items[j].v[0] = w * (double)col[3 * j];
+      items[j].v[1] = w * (double)col[3 * j + 1];
+      items[j].v[2] = w * (double)col[3 * j + 2];
+      items[j].v[3] = w;
+      items[j].v[4] = w * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+      agg = seg_combine(agg, items[j]);
+    }
+    Seg<5> run = block_seg_excl<5, kFlatWarps>(agg, carryC, smC);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      run = seg_combine(run, items[j]);
+      if (it.tail[j]) {
+        const int64_t r = it.rid[j];
+        if (color) {
+          color[3 * r] = (float)run.v[0];
+          color[3 * r + 1] = (float)run.v[1];
+          color[3 * r + 2] = (float)run.v[2];
+        }
+        if (opacity) opacity[r] = (float)run.v[3];
+        if (depth) depth[r] = (float)(run.v[4] / fmax(run.v[3], 1e-10));
+        if (ctx)
+#pragma unroll
+          for (int k = 0; k < 5; ++k) ctx[5 * r + k] = run.v[k];
+      }
+    }
+  }
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(kFlatThreads) render_bwd_flat_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_tiles,
+    const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
+    const float *__restrict__ rgb, double L, const double *__restrict__ ctx, const float *__restrict__ g_color,
+    const float *__restrict__ g_opacity, const float *__restrict__ g_depth, float *__restrict__ g_sigma,
+    float *__restrict__ g_rgb) {
+  __shared__ Seg<1> smS[kFlatWarps + 1];
+  __shared__ Seg<1> smP[kFlatWarps + 1];
+  const int64_t N = packed_end(packed_info, n_rays);  // samples in use (arrays may be a larger capacity)
+  const int64_t B = snap_to_ray(packed_info, ray_id, (int64_t)blockIdx.x * kFlatTile, N);
+  const int64_t E = snap_to_ray(packed_info, ray_id, ((int64_t)blockIdx.x + 1) * kFlatTile, N);
+  if (B >= E) return;
+  Seg<1> carryS = seg_identity<1>(), carryP = seg_identity<1>();
+  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kFlatChunk) {
+    Items it;
+    load_items<kVec>(it, c0, B, E, t0, t1, sigma, ray_id);
+    double s[4], S[4];
+    items_optical_depth(it, s, S, carryS, smS);
+    float col[12];
+    const bool full = kVec && it.valid[0] && it.valid[3];
+    if (full) {
+      const float4 *p = reinterpret_cast<const float4 *>(rgb + 3 * it.q0);
+      const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+      col[0] = a.x; col[1] = a.y; col[2] = a.z; col[3] = a.w; col[4] = b.x; col[5] = b.y;
+      col[6] = b.z; col[7] = b.w; col[8] = c.x; col[9] = c.y; col[10] = c.z; col[11] = c.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) col[3 * j + ch] = it.valid[j] ? __ldg(rgb + 3 * (it.q0 + j) + ch) : 0.f;
+    }
+    // per-ray constants of the backward (gathered; consecutive items share a ray)
+    double gc[4][3], gOp[4], gN[4], Rr[4];
+    int32_t last = -1;
+    double lc0 = 0, lc1 = 0, lc2 = 0, lop = 0, lgn = 0, lR = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (it.valid[j] && it.rid[j] != last) {
+        const int64_t r = it.rid[j];
+        last = it.rid[j];
+        const double *cx = ctx + 5 * r;
+        const double C0 = cx[0], C1 = cx[1], C2 = cx[2], O = cx[3], Nn = cx[4];
+        lc0 = g_color ? (double)__ldg(g_color + 3 * r) : 0.0;
+        lc1 = g_color ? (double)__ldg(g_color + 3 * r + 1) : 0.0;
+        lc2 = g_color ? (double)__ldg(g_color + 3 * r + 2) : 0.0;
+        const double gO = g_opacity ? (double)__ldg(g_opacity + r) : 0.0;
+        const double gD = g_depth ? (double)__ldg(g_depth + r) : 0.0;
+        if (O > 1e-10) {
+          const double inv = 1.0 / O;
+          lgn = gD * inv;
+          lop = gO - gD * Nn * inv * inv;
+        } else {
+          lgn = gD * 1e10;
+          lop = gO;
+        }
+        lR = lc0 * C0 + lc1 * C1 + lc2 * C2 + lop * O + lgn * Nn;
+      }
+      gc[j][0] = lc0; gc[j][1] = lc1; gc[j][2] = lc2;
+      gOp[j] = lop; gN[j] = lgn; Rr[j] = lR;
+    }
+    double w[4], gwTea[4];
+    Seg<1> items[4];
+    Seg<1> agg = seg_identity<1>();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool live = it.valid[j] && !(S[j] > L);
+      double v = 0.0;
+      w[j] = 0.0;
+      gwTea[j] = 0.0;
+      if (live) {
+        const double T = exp(-S[j]), ea = exp(-s[j]);
+        w[j] = T * (1.0 - ea);  // α = 1 - e^{-s}: fp64 absolute error ~1e-16
+        const double gw = gc[j][0] * col[3 * j] + gc[j][1] * col[3 * j + 1] + gc[j][2] * col[3 * j + 2] + gOp[j] +
+                          gN[j] * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+        v = gw * w[j];
+        gwTea[j] = gw * T * ea;
+      }
+      items[j].f = it.head[j];
+      items[j].v[0] = v;
+      agg = seg_combine(agg, items[j]);
+    }
+    Seg<1> run = block_seg_excl<1, kFlatWarps>(agg, carryP, smP);
+    float gs[4], gr[12];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      run = seg_combine(run, items[j]);
+      const bool live = it.valid[j] && !(S[j] > L);
+      const double Q = Rr[j] - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
+      gs[j] = live ? (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q)) : 0.f;
+      gr[3 * j] = (float)(w[j] * gc[j][0]);
+      gr[3 * j + 1] = (float)(w[j] * gc[j][1]);
+      gr[3 * j + 2] = (float)(w[j] * gc[j][2]);
+    }
+    if (kVec && it.valid[0] && it.valid[3]) {
+      *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
+      if (g_rgb) {
+        float4 *p = reinterpret_cast<float4 *>(g_rgb + 3 * it.q0);
+        p[0] = make_float4(gr[0], gr[1], gr[2], gr[3]);
+        p[1] = make_float4(gr[4], gr[5], gr[6], gr[7]);
+        p[2] = make_float4(gr[8], gr[9], gr[10], gr[11]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!it.valid[j]) continue;
+        g_sigma[it.q0 + j] = gs[j];
+        if (g_rgb)
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) g_rgb[3 * (it.q0 + j) + ch] = gr[3 * j + ch];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ warp-tile fused render
+// Each warp owns the rays whose first sample lies in its 256-sample tile and
+// walks them in chunks of 32 lanes x 4 consecutive samples (float4 loads);
+// fp64 warp-level segmented scans (no shared memory, no block barriers) carry
+// the open ray across chunks.  Extra warps zero the outputs of empty rays.
+constexpr int64_t kWarpTile = 256;
+constexpr int kWarpChunk = 128;
+
+template <bool kVec>
+__device__ __forceinline__ void load_items_warp(Items &it, int64_t c0, int64_t B, int64_t E,
+                                                const float *__restrict__ t0, const float *__restrict__ t1,
+                                                const float *__restrict__ sigma, const int32_t *__restrict__ ray_id,
+                                                int32_t &carry_rid) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q0 = c0 + (int64_t)lane * 4;
+  it.q0 = q0;
+  const bool full = kVec && q0 >= B && q0 + 3 < E;
+  if (full) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(t0 + q0));
+    const float4 b = __ldg(reinterpret_cast<const float4 *>(t1 + q0));
+    const float4 c = __ldg(reinterpret_cast<const float4 *>(sigma + q0));
+    const int4 d = __ldg(reinterpret_cast<const int4 *>(ray_id + q0));
+    it.t0[0] = a.x; it.t0[1] = a.y; it.t0[2] = a.z; it.t0[3] = a.w;
+    it.t1[0] = b.x; it.t1[1] = b.y; it.t1[2] = b.z; it.t1[3] = b.w;
+    it.sg[0] = c.x; it.sg[1] = c.y; it.sg[2] = c.z; it.sg[3] = c.w;
+    it.rid[0] = d.x; it.rid[1] = d.y; it.rid[2] = d.z; it.rid[3] = d.w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) it.valid[j] = true;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t q = q0 + j;
+      it.valid[j] = q >= B && q < E;
+      it.t0[j] = it.valid[j] ? __ldg(t0 + q) : 0.f;
+      it.t1[j] = it.valid[j] ? __ldg(t1 + q) : 0.f;
+      it.sg[j] = it.valid[j] ? __ldg(sigma + q) : 0.f;
+      it.rid[j] = it.valid[j] ? __ldg(ray_id + q) : -1;
+    }
+  }
+  // neighbours through shuffles; the chunk's first lane uses the previous chunk's last ray,
+  // the last lane loads the next sample's ray
+  int32_t prev = __shfl_up_sync(kFull, it.rid[3], 1);
+  if (lane == 0) prev = carry_rid;
+  int32_t next = __shfl_down_sync(kFull, it.rid[0], 1);
+  if (lane == 31) next = (q0 + 4 < E) ? __ldg(ray_id + q0 + 4) : -2;
+  carry_rid = __shfl_sync(kFull, it.rid[3], 31);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int32_t pr = j == 0 ? prev : it.rid[j - 1];
+    const int32_t nx = j == 3 ? next : (it.valid[j + 1] ? it.rid[j + 1] : -2);
+    it.head[j] = it.valid[j] && (it.q0 + j == B || it.rid[j] != pr);
+    it.tail[j] = it.valid[j] && (it.q0 + j + 1 == E || it.rid[j] != nx);
+  }
+}
+
+__device__ __forceinline__ void load_rgb4(float col[12], const Items &it, const float *__restrict__ rgb, bool vec) {
+  if (vec && it.valid[0] && it.valid[3]) {
+    const float4 *p = reinterpret_cast<const float4 *>(rgb + 3 * it.q0);
+    const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+    col[0] = a.x; col[1] = a.y; col[2] = a.z; col[3] = a.w; col[4] = b.x; col[5] = b.y;
+    col[6] = b.z; col[7] = b.w; col[8] = c.x; col[9] = c.y; col[10] = c.z; col[11] = c.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) col[3 * j + ch] = it.valid[j] ? __ldg(rgb + 3 * (it.q0 + j) + ch) : 0.f;
+  }
+}
+
+// entering optical depth of the thread's items (fp64 warp segmented exclusive scan)
+__device__ __forceinline__ void warp_items_S(const Items &it, double s[4], double S[4], Seg<1> &carry) {
+  Seg<1> agg = seg_identity<1>();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    s[j] = it.valid[j] ? (double)it.sg[j] * ((double)it.t1[j] - (double)it.t0[j]) : 0.0;
+    Seg<1> x;
+    x.f = it.head[j];
+    x.v[0] = s[j];
+    agg = seg_combine(agg, x);
+  }
+  Seg<1> run = warp_seg_excl<1>(agg, carry);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    S[j] = it.head[j] ? 0.0 : run.v[0];
+    run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + s[j];
+  }
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(256) render_fwd_warp_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
+    const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
+    const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
+    float *__restrict__ depth, double *__restrict__ ctx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wt >= n_wtiles) {  // rays without samples
+    for (int64_t r = (wt - n_wtiles) * 32 + lane; r < n_rays; r += 1ll << 62) {
+      if (packed_info[2 * r + 1] == 0) {
+        if (color) { color[3 * r] = 0.f; color[3 * r + 1] = 0.f; color[3 * r + 2] = 0.f; }
+        if (opacity) opacity[r] = 0.f;
+        if (depth) depth[r] = 0.f;
+        if (ctx) for (int k = 0; k < 5; ++k) ctx[5 * r + k] = 0.0;
+      }
+      break;
+    }
+    return;
+  }
+  const int64_t N = packed_end(packed_info, n_rays);
+  const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+  const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+  if (B >= E) return;
+  Seg<1> carryS = seg_identity<1>();
+  Seg<5> carryC = seg_identity<5>();
+  int32_t carry_rid = -1;
+  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+    Items it;
+    load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
+    double s[4], S[4];
+    warp_items_S(it, s, S, carryS);
+    float col[12];
+    load_rgb4(col, it, rgb, kVec);
+    double w[4];
+    Seg<5> agg = seg_identity<5>();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool live = it.valid[j] && !(S[j] > L);
+      w[j] = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
+      Seg<5> x;
+      x.f = it.head[j];
+      x.v[0] = w[j] * (double)col[3 * j];
+      x.v[1] = w[j] * (double)col[3 * j + 1];
+      x.v[2] = w[j] * (double)col[3 * j + 2];
+      x.v[3] = w[j];
+      x.v[4] = w[j] * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+      agg = seg_combine(agg, x);
+    }
+    Seg<5> run = warp_seg_excl<5>(agg, carryC);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      Seg<5> x;
+      x.f = it.head[j];
+      x.v[0] = w[j] * (double)col[3 * j];
+      x.v[1] = w[j] * (double)col[3 * j + 1];
+      x.v[2] = w[j] * (double)col[3 * j + 2];
+      x.v[3] = w[j];
+      x.v[4] = w[j] * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+      run = seg_combine(run, x);
+      if (it.tail[j]) {
+        const int64_t r = it.rid[j];
+        if (color) {
+          color[3 * r] = (float)run.v[0];
+          color[3 * r + 1] = (float)run.v[1];
+          color[3 * r + 2] = (float)run.v[2];
+        }
+        if (opacity) opacity[r] = (float)run.v[3];
+        if (depth) depth[r] = (float)(run.v[4] / fmax(run.v[3], 1e-10));
+        if (ctx) {
+          double2 *cx = reinterpret_cast<double2 *>(ctx + 5 * r);
+          ctx[5 * r] = run.v[0];
+          ctx[5 * r + 1] = run.v[1];
+          ctx[5 * r + 2] = run.v[2];
+          ctx[5 * r + 3] = run.v[3];
+          ctx[5 * r + 4] = run.v[4];
+          (void)cx;
+        }
+      }
+    }
+  }
+}
+
+struct RayGrad {
+  double gc0, gc1, gc2, gOp, gN, R;
+};
+
+__device__ __forceinline__ RayGrad ray_grad(int64_t r, const double *__restrict__ ctx, const float *__restrict__ g_color,
+                                            const float *__restrict__ g_opacity, const float *__restrict__ g_depth) {
+  RayGrad q;
+  const double *cx = ctx + 5 * r;
+  const double C0 = __ldg(cx), C1 = __ldg(cx + 1), C2 = __ldg(cx + 2), O = __ldg(cx + 3), Nn = __ldg(cx + 4);
+  q.gc0 = g_color ? (double)__ldg(g_color + 3 * r) : 0.0;
+  q.gc1 = g_color ? (double)__ldg(g_color + 3 * r + 1) : 0.0;
+  q.gc2 = g_color ? (double)__ldg(g_color + 3 * r + 2) : 0.0;
+  const double gO = g_opacity ? (double)__ldg(g_opacity + r) : 0.0;
+  const double gD = g_depth ? (double)__ldg(g_depth + r) : 0.0;
+  if (O > 1e-10) {
+    const double inv = 1.0 / O;
+    q.gN = gD * inv;
+    q.gOp = gO - gD * Nn * inv * inv;
+  } else {
+    q.gN = gD * 1e10;
+    q.gOp = gO;
+  }
+  q.R = q.gc0 * C0 + q.gc1 * C1 + q.gc2 * C2 + q.gOp * O + q.gN * Nn;
+  return q;
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(256) render_bwd_warp_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
+    const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
+    const float *__restrict__ rgb, double L, const double *__restrict__ ctx, const float *__restrict__ g_color,
+    const float *__restrict__ g_opacity, const float *__restrict__ g_depth, float *__restrict__ g_sigma,
+    float *__restrict__ g_rgb) {
+  const int64_t wt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wt >= n_wtiles) return;
+  const int64_t N = packed_end(packed_info, n_rays);
+  const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+  const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+  if (B >= E) return;
+  Seg<1> carryS = seg_identity<1>(), carryP = seg_identity<1>();
+  int32_t carry_rid = -1;
+  int32_t cached = -1;
+  RayGrad rg{};
+  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+    Items it;
+    load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
+    double s[4], S[4];
+    warp_items_S(it, s, S, carryS);
+    float col[12];
+    load_rgb4(col, it, rgb, kVec);
+    double w[4], gwTea[4], Rr[4], gcs[4][3];
+    Seg<1> agg = seg_identity<1>();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (it.valid[j] && it.rid[j] != cached) {
+        cached = it.rid[j];
+        rg = ray_grad(cached, ctx, g_color, g_opacity, g_depth);
+      }
+      Rr[j] = rg.R;
+      gcs[j][0] = rg.gc0;
+      gcs[j][1] = rg.gc1;
+      gcs[j][2] = rg.gc2;
+      const bool live = it.valid[j] && !(S[j] > L);
+      double v = 0.0;
+      w[j] = 0.0;
+      gwTea[j] = 0.0;
+      if (live) {
+        const double T = exp(-S[j]), ea = exp(-s[j]);
+        w[j] = T * (1.0 - ea);
+        const double gw = rg.gc0 * col[3 * j] + rg.gc1 * col[3 * j + 1] + rg.gc2 * col[3 * j + 2] + rg.gOp +
+                          rg.gN * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+        v = gw * w[j];
+        gwTea[j] = gw * T * ea;
+      }
+      Seg<1> x;
+      x.f = it.head[j];
+      x.v[0] = v;
+      agg = seg_combine(agg, x);
+      s[j] = v;  // reuse: the item's g_w w term
+    }
+    Seg<1> run = warp_seg_excl<1>(agg, carryP);
+    float gs[4], gr[12];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + s[j];
+      const bool live = it.valid[j] && !(S[j] > L);
+      const double Q = Rr[j] - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
+      gs[j] = live ? (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q)) : 0.f;
+      gr[3 * j] = (float)(w[j] * gcs[j][0]);
+      gr[3 * j + 1] = (float)(w[j] * gcs[j][1]);
+      gr[3 * j + 2] = (float)(w[j] * gcs[j][2]);
+    }
+    if (kVec && it.valid[0] && it.valid[3]) {
+      *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
+      if (g_rgb) {
+        float4 *pp = reinterpret_cast<float4 *>(g_rgb + 3 * it.q0);
+        pp[0] = make_float4(gr[0], gr[1], gr[2], gr[3]);
+        pp[1] = make_float4(gr[4], gr[5], gr[6], gr[7]);
+        pp[2] = make_float4(gr[8], gr[9], gr[10], gr[11]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!it.valid[j]) continue;
+        g_sigma[it.q0 + j] = gs[j];
+        if (g_rgb)
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) g_rgb[3 * (it.q0 + j) + ch] = gr[3 * j + ch];
+      }
+    }
   }
 }
 
@@ -223,10 +782,10 @@ __global__ void __launch_bounds__(256) weights_fwd_kernel(const int64_t *__restr
     const Chunk c = load_chunk(t0, t1, sigma, st, cnt, base, L, carry);
     if (c.valid) {
       const int64_t q = st + base + lane;
-      const float T = trans_of(c.S), a = alpha_of(c.s);
-      weights[q] = c.live ? T * a : 0.f;
-      if (trans) trans[q] = T;
-      if (alphas) alphas[q] = a;
+      const double T = trans_of(c.S), a = alpha_of(c.s);
+      weights[q] = c.live ? (float)(T * a) : 0.f;
+      if (trans) trans[q] = (float)T;
+      if (alphas) alphas[q] = (float)a;
     }
   }
 }
@@ -248,9 +807,9 @@ __global__ void __launch_bounds__(256) weights_bwd_kernel(const int64_t *__restr
     const Chunk c = load_chunk(t0, t1, sigma, st, cnt, base, L, carry);
     if (c.valid) {
       const int64_t q = st + base + lane;
-      const float T = trans_of(c.S);
-      if (c.live) R += (double)__ldg(g_weights + q) * (double)(T * alpha_of(c.s));
-      if (g_trans) R += (double)__ldg(g_trans + q) * (double)T;
+      const double T = trans_of(c.S);
+      if (c.live) R += (double)__ldg(g_weights + q) * (T * alpha_of(c.s));
+      if (g_trans) R += (double)__ldg(g_trans + q) * T;
     }
   }
   R = warp_sum(R);
@@ -262,13 +821,13 @@ __global__ void __launch_bounds__(256) weights_bwd_kernel(const int64_t *__restr
     const int64_t q = st + base + lane;
     double v = 0.0, gwTa = 0.0;
     if (c.valid) {
-      const float T = trans_of(c.S);
+      const double T = trans_of(c.S);
       const double gw = (double)__ldg(g_weights + q);
       if (c.live) {
-        v += gw * (double)(T * alpha_of(c.s));
-        gwTa = gw * (double)T * (double)expf(-(float)c.s);
+        v += gw * (T * alpha_of(c.s));
+        gwTa = gw * T * exp(-c.s);
       }
-      if (g_trans) v += (double)__ldg(g_trans + q) * (double)T;
+      if (g_trans) v += (double)__ldg(g_trans + q) * T;
     }
     const double incl = warp_incl_scan(v);
     const double Q = R - (P + incl);
@@ -354,9 +913,10 @@ using namespace nacc;
 
 extern "C" {
 
-nacc_status nacc_render_fwd(const int64_t *packed_info, int64_t n_rays, const float *t0, const float *t1,
-                            const float *sigma, const float *rgb, int64_t n_samples, double neg_log_eps,
-                            float *color, float *opacity, float *depth, double *ctx, cudaStream_t stream) {
+nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays, const float *t0,
+                            const float *t1, const float *sigma, const float *rgb, int64_t n_samples,
+                            double neg_log_eps, float *color, float *opacity, float *depth, double *ctx,
+                            cudaStream_t stream) {
   clear_error();
   nacc_status s = check_packed(packed_info, n_rays, n_samples);
   if (s != NACC_OK) return s;
@@ -364,26 +924,55 @@ nacc_status nacc_render_fwd(const int64_t *packed_info, int64_t n_rays, const fl
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(n_samples == 0 || (t0 && t1 && sigma), "t0, t1, sigma must be non-NULL");
   NACC_REQUIRE(!ctx || aligned(ctx, 8), "ctx must be 8-byte aligned");
-  render_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, rgb,
-                                                                     neg_log_eps, color, opacity, depth, ctx);
+  if (ray_id && rgb) {
+    const int64_t n_wtiles = ceil_div(n_samples, kWarpTile);
+    const int64_t warps = n_wtiles + ceil_div(n_rays, 32);
+    const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(rgb, 16) &&
+                     aligned(ray_id, 16);
+    const unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
+    if (vec)
+      render_fwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+                                                               rgb, neg_log_eps, color, opacity, depth, ctx);
+    else
+      render_fwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+                                                                rgb, neg_log_eps, color, opacity, depth, ctx);
+  } else {
+    render_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, rgb,
+                                                                       neg_log_eps, color, opacity, depth, ctx);
+  }
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;
 }
 
-nacc_status nacc_render_bwd(const int64_t *packed_info, int64_t n_rays, const float *t0, const float *t1,
-                            const float *sigma, const float *rgb, int64_t n_samples, double neg_log_eps,
-                            const double *ctx, const float *g_color, const float *g_opacity,
+nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays, const float *t0,
+                            const float *t1, const float *sigma, const float *rgb, int64_t n_samples,
+                            double neg_log_eps, const double *ctx, const float *g_color, const float *g_opacity,
                             const float *g_depth, float *g_sigma, float *g_rgb, cudaStream_t stream) {
   clear_error();
   nacc_status s = check_packed(packed_info, n_rays, n_samples);
   if (s != NACC_OK) return s;
   NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
-  if (n_rays == 0) return NACC_OK;
-  NACC_REQUIRE(n_samples == 0 || (t0 && t1 && sigma && g_sigma), "t0, t1, sigma, g_sigma must be non-NULL");
-  render_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, rgb,
-                                                                     neg_log_eps, ctx, g_color, g_opacity, g_depth,
-                                                                     g_sigma, g_rgb);
+  if (n_rays == 0 || n_samples == 0) return NACC_OK;
+  NACC_REQUIRE(t0 && t1 && sigma && g_sigma, "t0, t1, sigma, g_sigma must be non-NULL");
+  if (ray_id && rgb && ctx) {
+    const int64_t n_wtiles = ceil_div(n_samples, kWarpTile);
+    const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(rgb, 16) &&
+                     aligned(ray_id, 16) && aligned(g_sigma, 16) && (!g_rgb || aligned(g_rgb, 16));
+    const unsigned blocks = (unsigned)ceil_div(n_wtiles * 32, 256);
+    if (vec)
+      render_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+                                                               rgb, neg_log_eps, ctx, g_color, g_opacity, g_depth,
+                                                               g_sigma, g_rgb);
+    else
+      render_bwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+                                                                rgb, neg_log_eps, ctx, g_color, g_opacity, g_depth,
+                                                                g_sigma, g_rgb);
+  } else {
+    render_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, rgb,
+                                                                       neg_log_eps, ctx, g_color, g_opacity, g_depth,
+                                                                       g_sigma, g_rgb);
+  }
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;

@@ -1,0 +1,117 @@
+// segscan.cuh — block-wide segmented scans over packed samples (flat tiles).
+//
+// A "segment" is one ray's run of consecutive samples in the packed tensor
+// (P:83).  Blocks own ray-aligned sample ranges, process them in chunks of
+// kThreads*kItems samples, and carry the open segment across chunks, so no
+// cross-block look-back is needed.  Values are fp64 (readings #9, #11).
+#pragma once
+#include "common.cuh"
+
+namespace nacc {
+
+template <int K>
+struct Seg {
+  int f;        // 1 if a segment head lies in the covered range
+  double v[K];  // sums since the last head (or since the start)
+};
+
+template <int K>
+__device__ __forceinline__ Seg<K> seg_identity() {
+  Seg<K> r;
+  r.f = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) r.v[k] = 0.0;
+  return r;
+}
+
+// associative segmented-sum operator: a then b
+template <int K>
+__device__ __forceinline__ Seg<K> seg_combine(const Seg<K> &a, const Seg<K> &b) {
+  Seg<K> r;
+  r.f = a.f | b.f;
+#pragma unroll
+  for (int k = 0; k < K; ++k) r.v[k] = b.f ? b.v[k] : a.v[k] + b.v[k];
+  return r;
+}
+
+template <int K>
+__device__ __forceinline__ Seg<K> seg_shfl_up(const Seg<K> &x, int o) {
+  Seg<K> y;
+  y.f = __shfl_up_sync(kFull, x.f, o);
+#pragma unroll
+  for (int k = 0; k < K; ++k) y.v[k] = __shfl_up_sync(kFull, x.v[k], o);
+  return y;
+}
+
+template <int K>
+__device__ __forceinline__ Seg<K> warp_seg_incl(Seg<K> x) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Seg<K> y = seg_shfl_up(x, o);
+    if (lane >= o) x = seg_combine(y, x);
+  }
+  return x;
+}
+
+// Exclusive block-wide segmented scan of one aggregate per thread, seeded with
+// `carry` (the open segment from the previous chunk).  Returns the thread's
+// exclusive prefix and advances `carry` to the chunk's inclusive total.
+// smem must hold kWarps + 1 elements.  Contains __syncthreads().
+template <int K, int kWarps>
+__device__ __forceinline__ Seg<K> block_seg_excl(const Seg<K> &x, Seg<K> &carry, Seg<K> *smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Seg<K> incl = warp_seg_incl(x);
+  Seg<K> ex = seg_shfl_up(incl, 1);
+  if (lane == 0) ex = seg_identity<K>();
+  if (lane == 31) smem[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    Seg<K> w = lane < kWarps ? smem[lane] : seg_identity<K>();
+    const Seg<K> wi = warp_seg_incl(w);
+    Seg<K> we = seg_shfl_up(wi, 1);
+    if (lane == 0) we = seg_identity<K>();
+    if (lane < kWarps) smem[lane] = seg_combine(carry, we);
+    if (lane == kWarps - 1) smem[kWarps] = seg_combine(carry, wi);
+  }
+  __syncthreads();
+  const Seg<K> res = seg_combine(smem[warp], ex);
+  carry = smem[kWarps];
+  __syncthreads();
+  return res;
+}
+
+// Exclusive warp-wide segmented scan seeded with `carry` (the open segment of
+// the previous chunk); advances `carry` to the chunk's inclusive total.
+template <int K>
+__device__ __forceinline__ Seg<K> warp_seg_excl(const Seg<K> &x, Seg<K> &carry) {
+  const int lane = threadIdx.x & 31;
+  const Seg<K> incl = warp_seg_incl(x);
+  Seg<K> ex = seg_shfl_up(incl, 1);
+  if (lane == 0) ex = seg_identity<K>();
+  const Seg<K> res = seg_combine(carry, ex);
+  Seg<K> last;
+  last.f = __shfl_sync(kFull, incl.f, 31);
+#pragma unroll
+  for (int k = 0; k < K; ++k) last.v[k] = __shfl_sync(kFull, incl.v[k], 31);
+  carry = seg_combine(carry, last);
+  return res;
+}
+
+// number of samples in use: end of the last ray's run
+__device__ __forceinline__ int64_t packed_end(const int64_t *__restrict__ packed_info, int64_t n_rays) {
+  const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + (n_rays - 1));
+  return pi.x + pi.y;
+}
+
+// Ray-aligned tile boundary: the first ray start at or after sample q.
+__device__ __forceinline__ int64_t snap_to_ray(const int64_t *__restrict__ packed_info,
+                                               const int32_t *__restrict__ ray_id, int64_t q, int64_t N) {
+  if (q >= N) return N;
+  if (q <= 0) return 0;
+  const int64_t r = __ldg(ray_id + q);
+  const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
+  return pi.x == q ? q : pi.x + pi.y;
+}
+
+}  // namespace nacc

@@ -60,7 +60,7 @@ def test_version_and_sizes(lib):
     assert lib.nacc_grid_bits_bytes(C.byref(g)) == 0
     g = GridSpec(res=128).c()
     p = MarchParams(step=0.01).c()
-    assert lib.nacc_sampling_occgrid_workspace_bytes(C.byref(g), C.byref(p), 1 << 18) >= 4 << 18
+    assert lib.nacc_sampling_occgrid_workspace_bytes(C.byref(g), C.byref(p), 1 << 18) >= 1 << 18
     assert lib.nacc_filter_workspace_bytes(1000) >= 4000
 
 
@@ -91,8 +91,8 @@ def test_host_validation_rejects_before_launch(lib):
     st = lib.nacc_sampling_occgrid(C.byref(g), fake, C.byref(pcone), fake, fake, fake, None, 10, fake, None, None,
                                    None, 0, fake, None, fake, 1 << 24, None)
     assert st == 4
-    assert lib.nacc_render_fwd(None, 5, None, None, None, None, 3, 1.0, None, None, None, None, None) == 1
-    assert lib.nacc_render_fwd(fake, -1, None, None, None, None, 3, 1.0, None, None, None, None, None) == 1
+    assert lib.nacc_render_fwd(None, None, 5, None, None, None, None, 3, 1.0, None, None, None, None, None) == 1
+    assert lib.nacc_render_fwd(fake, None, -1, None, None, None, None, 3, 1.0, None, None, None, None, None) == 1
     assert lib.nacc_accumulate_along_rays(fake, 3, fake, None, 3, 5, fake, None) == 1  # values NULL needs C == 1
     assert lib.nacc_importance_sample(4, 8, fake, fake, fake, 1, 0.2, 1000.0, 4, 0, 0, fake, None, None) == 1
     assert lib.nacc_importance_sample(4, 8, fake, fake, None, 0, 0.2, float("inf"), 4, 0, 0, fake, None, None) == 1

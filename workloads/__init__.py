@@ -240,6 +240,15 @@ def occupancy_from_lattice(lat, levels, res, roi, sigma_thresh=5.0):
     return np.concatenate(out)
 
 
+def pack_bits(occ):
+    """Public bitfield layout of include/nacc.h: bit q of the grid lives in
+    uint32 word q >> 5 at bit position q & 31 (LSB first)."""
+    occ = np.asarray(occ, np.uint8).ravel()
+    pad = (-occ.size) % 32
+    b = np.packbits(np.concatenate([occ, np.zeros(pad, np.uint8)]), bitorder="little")
+    return b.view(np.uint32)
+
+
 # --------------------------------------------------------------------------- configs
 @dataclasses.dataclass
 class MarchConfig:
