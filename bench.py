@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", default="nacc", choices=["nacc", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
+    ap.add_argument("--eager", action="store_true", help="time the eager (non-graph) step")
     return ap.parse_args()
 
 
@@ -210,9 +211,100 @@ class Pipeline:
         acc = {n: 0.0 for n in names}
         for ev in self.events:
             for i, n in enumerate(names):
-                acc[n] += ev[i].elapsed_time(ev[i + 1])
+                if i + 1 < len(ev):
+                    acc[n] += ev[i].elapsed_time(ev[i + 1])
         k = max(len(self.events), 1)
         return {n: v / k for n, v in acc.items()}
+
+    # ------------------------------------------------------------------ CUDA-graph step
+    def capture(self):
+        """Capture each stage of the step as a CUDA graph over static buffers,
+        using the device-count API (no host syncs): march -> field σ -> filter
+        -> field σ,rgb -> render fwd -> MSE grad -> render bwd (+ counters).
+        The capacity is the max total seen in warm-up x 1.25; an overflow is
+        recorded in a device status checked after the timed region."""
+        N, H, torch = self.N, self.H, self.torch
+        torch.cuda.synchronize()
+        caps = []
+        for o, d in self.rays:
+            s = N.sampling_occgrid(o, d, self.spec, self.grid.bits, self.params)
+            caps.append(s.n_samples)
+        cap1 = int(max(caps) * 1.25) + 4096
+        self.o_buf = self.rays[0][0].clone()
+        self.d_buf = self.rays[0][1].clone()
+        self.acc = torch.zeros(2, dtype=torch.int64, device=self.device)  # pre, post
+        self.acc_status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        pool = torch.cuda.graph_pool_handle()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        outs = {}
+        l0 = N.launch_count() + H.launch_count()
+
+        def st_march():
+            outs["s"] = N.sampling_occgrid(self.o_buf, self.d_buf, self.spec, self.grid.bits, self.params,
+                                           capacity=cap1, sync=False)
+
+        def st_f1():
+            s = outs["s"]
+            outs["sigma"], _ = self.field.at_samples(self.o_buf, self.d_buf, s.t0, s.t1, s.ray_id, want_rgb=False,
+                                                     n_dev=s.total)
+
+        def st_filter():
+            outs["f"] = N.filter_early_stop(outs["s"], outs["sigma"], EPS, sync=False)
+
+        def st_f2():
+            f = outs["f"]
+            outs["sig2"], outs["rgb"] = self.field.at_samples(self.o_buf, self.d_buf, f.t0, f.t1, f.ray_id,
+                                                              n_dev=f.total)
+
+        def st_rfwd():
+            outs["color"], outs["opacity"], outs["depth"], outs["ctx"] = N.render_fwd(outs["f"], outs["sig2"],
+                                                                                      outs["rgb"], EPS)
+
+        def st_mse():
+            outs["gcol"] = H.mse_grad(outs["color"], self.gt)
+
+        def st_rbwd():
+            outs["gs"], outs["grgb"] = N.render_bwd(outs["f"], outs["sig2"], outs["rgb"], outs["ctx"], outs["gcol"],
+                                                    None, None, EPS)
+            self.acc[0].add_(outs["s"].total[0])
+            self.acc[1].add_(outs["f"].total[0])
+            torch.maximum(self.acc_status, outs["s"].status, out=self.acc_status)
+
+        self.graphs = []
+        with torch.cuda.stream(side):
+            for fn in (st_march, st_f1, st_filter, st_f2, st_rfwd, st_mse, st_rbwd):
+                fn()  # eager warm-up of the stage on the side stream
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, pool=pool, stream=side):
+                    fn()
+                self.graphs.append(g)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.launches_per_graph_step = N.launch_count() + H.launch_count() - l0  # (eager + captured) / 2
+        self.launches_per_graph_step //= 2
+        self.outs = outs
+        self.capacity = cap1
+        self.acc.zero_()
+        self.acc_status.zero_()
+
+    def step_graph(self, timing=False, rays=None):
+        torch = self.torch
+        o, d = rays if rays is not None else self.rays[self.k % len(self.rays)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
+        self.o_buf.copy_(o, non_blocking=True)
+        self.d_buf.copy_(d, non_blocking=True)
+        for i, g in enumerate(self.graphs):
+            if timing:
+                ev[i].record()
+            g.replay()
+        if timing:
+            ev[7].record()
+        self.grid.update_every_n_steps(self.k, self.occ_fn, n=UPDATE_EVERY)
+        if timing:
+            ev[8].record()
+            self.events.append(ev)
+        self.k += 1
 
 
 def algorithmic_bytes(stage, pre, post, rays):
@@ -325,6 +417,15 @@ def run_nacc(args):
     for _ in range(max(args.warmup, 3)):
         pipe.step()
     torch.cuda.synchronize()
+    use_graph = not args.profile and not args.eager
+    if use_graph:
+        pipe.capture()
+        for _ in range(3):
+            pipe.step_graph()
+        torch.cuda.synchronize()
+        pipe.acc.zero_()
+        pipe.acc_status.zero_()
+    step = pipe.step_graph if use_graph else pipe.step
 
     def barrier():
         if world > 1:
@@ -332,6 +433,7 @@ def run_nacc(args):
 
     # ---- device-timed region: inputs resident in HBM
     pipe.stats = {"pre": 0, "post": 0, "rays": 0}
+    pipe.events = []
     l0 = N.launch_count() + H.launch_count()
     barrier()
     torch.cuda.synchronize()
@@ -340,13 +442,20 @@ def run_nacc(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            pipe.step(timing=not args.profile)
+            step(timing=not args.profile)
         e1.record()
         torch.cuda.synchronize()
     barrier()
     launches = N.launch_count() + H.launch_count() - l0
+    if use_graph:
+        launches += pipe.launches_per_graph_step * args.steps
+        pre_s, post_s = pipe.acc.tolist()
+        if int(pipe.acc_status.item()) != 0:
+            raise RuntimeError("march capacity overflow inside the captured step; increase the capacity margin")
+        stats = {"pre": pre_s, "post": post_s, "rays": RAYS_PER_GPU * args.steps}
+    else:
+        stats = dict(pipe.stats)
     ms = e0.elapsed_time(e1)
-    stats = dict(pipe.stats)
     stages = pipe.stage_ms() if not args.profile else {}
     t = torch.tensor([ms, stats["post"], stats["pre"], stats["rays"]], dtype=torch.float64, device=device)
     if world > 1:
@@ -363,6 +472,8 @@ def run_nacc(args):
         pinned = [(torch.from_numpy(o).pin_memory(), torch.from_numpy(d).pin_memory()) for o, d in pipe.rays_host]
         out_host = torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32).pin_memory()
         k2 = max(args.steps // 4, 20)
+        if use_graph:
+            pipe.acc.zero_()
         post_e2e = 0
         barrier()
         torch.cuda.synchronize()
@@ -371,15 +482,21 @@ def run_nacc(args):
         f0.record()
         for i in range(k2):
             ho, hd = pinned[i % len(pinned)]
-            o = ho.to(device, non_blocking=True)
-            d = hd.to(device, non_blocking=True)
-            color, opacity, depth, n_post = pipe.step(rays=(o, d))
-            res = torch.cat([color.detach(), opacity.detach()[:, None], depth.detach()[:, None]], 1)
+            if use_graph:
+                pipe.step_graph(rays=(ho, hd))  # H2D copy from pinned memory into the static inputs
+                res = torch.cat([pipe.outs["color"], pipe.outs["opacity"][:, None], pipe.outs["depth"][:, None]], 1)
+            else:
+                o = ho.to(device, non_blocking=True)
+                d = hd.to(device, non_blocking=True)
+                color, opacity, depth, n_post = pipe.step(rays=(o, d))
+                post_e2e += n_post
+                res = torch.cat([color.detach(), opacity.detach()[:, None], depth.detach()[:, None]], 1)
             out_host.copy_(res, non_blocking=True)
-            post_e2e += n_post
         f1.record()
         torch.cuda.synchronize()
         barrier()
+        if use_graph:
+            post_e2e = int(pipe.acc[1].item())
         ms2 = f0.elapsed_time(f1)
         t2 = torch.tensor([ms2, post_e2e], dtype=torch.float64, device=device)
         if world > 1:
@@ -415,6 +532,7 @@ def run_nacc(args):
                            "grid": "1x128^3", "parallelism": f"dp{world} (ray-sharded, replicated grid)",
                            "l2": "inputs larger than L2 (march output ~0.25 GB/step/GPU; 4 rotating ray batches)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+                "execution": "cuda-graph per stage, device-count API (no host syncs)" if use_graph else "eager",
                 "samples_pre_filter_per_step_per_gpu": pre_pg, "samples_post_filter_per_step_per_gpu": post_pg,
                 "pre_filter_samples_per_s": pre_all / (ms_max / 1e3), "rays_per_s": rays_all / (ms_max / 1e3),
                 "stage_ms": stages,

@@ -29,6 +29,13 @@ nacc_status naccx_field_at_samples(const float *lattice, int32_t res, float lo, 
                                    cudaStream_t stream);
 /* n is the arrays' capacity; n_dev (device int64, NULL = n) the count in use. */
 
+/* σ only, from a density-only lattice [res^3] fp32 (same interpolation). */
+nacc_status naccx_sigma_at_samples(const float *sigma_lattice, int32_t res, float lo, float hi,
+                                   int32_t contracted, const float *rays_o, const float *rays_d,
+                                   const float *t0, const float *t1, const int32_t *ray_id,
+                                   int64_t n, const int64_t *n_dev, float *sigma,
+                                   cudaStream_t stream);
+
 /* out[i] = scale * σ(xyz[i]) for the occupancy-grid update (v = σ·Δt). */
 nacc_status naccx_field_at_points(const float *lattice, int32_t res, float lo, float hi,
                                   int32_t contracted, const float *xyz, int64_t n, float scale,

@@ -72,6 +72,7 @@ SIGNATURES = {
 
 HARNESS_SIGNATURES = {
     "naccx_field_at_samples": (C.c_int, [P, I32, F, F, I32, P, P, P, P, P, I64, P, P, P, P]),
+    "naccx_sigma_at_samples": (C.c_int, [P, I32, F, F, I32, P, P, P, P, P, I64, P, P, P]),
     "naccx_field_at_points": (C.c_int, [P, I32, F, F, I32, P, I64, F, P, P]),
     "naccx_mse_grad": (C.c_int, [P, P, I64, P, P]),
     "naccx_launch_count": (C.c_uint64, []),

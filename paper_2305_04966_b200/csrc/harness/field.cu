@@ -46,6 +46,53 @@ __device__ __forceinline__ float4 lattice_at(const float4 *__restrict__ lat, int
   return acc;
 }
 
+// density-only lattice: one float per cell (the density query of Alg. 1 line 30
+// does not need colour); same interpolation as lattice_at
+__device__ __forceinline__ float lattice_sigma_at(const float *__restrict__ lat, int R, float lo, float hi,
+                                                  int contracted, float x, float y, float z) {
+  if (contracted) {
+    const float n = sqrtf(x * x + y * y + z * z);
+    if (n > 1.0f) {
+      const float s = (2.0f - 1.0f / n) / n;
+      x *= s;
+      y *= s;
+      z *= s;
+    }
+  }
+  if (!(x >= lo && x <= hi && y >= lo && y <= hi && z >= lo && z <= hi)) return 0.f;
+  const float sc = (float)R / (hi - lo);
+  float u[3] = {(x - lo) * sc - 0.5f, (y - lo) * sc - 0.5f, (z - lo) * sc - 0.5f};
+  int i0[3];
+  float f[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    u[a] = fminf(fmaxf(u[a], 0.0f), (float)(R - 1));
+    i0[a] = min((int)floorf(u[a]), R - 2);
+    f[a] = u[a] - (float)i0[a];
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int dx = c & 1, dy = (c >> 1) & 1, dz = c >> 2;
+    const float w = (dx ? f[0] : 1.f - f[0]) * (dy ? f[1] : 1.f - f[1]) * (dz ? f[2] : 1.f - f[2]);
+    acc += w * __ldg(lat + (i0[0] + dx) + R * ((i0[1] + dy) + R * (i0[2] + dz)));
+  }
+  return acc;
+}
+
+__global__ void field_sigma_kernel(const float *__restrict__ lat, int R, float lo, float hi, int contracted,
+                                   const float *__restrict__ o, const float *__restrict__ d,
+                                   const float *__restrict__ t0, const float *__restrict__ t1,
+                                   const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
+                                   float *__restrict__ sigma) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || (n_dev && i >= *n_dev)) return;
+  const int64_t r = __ldg(rid + i);
+  const float m = 0.5f * (__ldg(t0 + i) + __ldg(t1 + i));
+  sigma[i] = lattice_sigma_at(lat, R, lo, hi, contracted, __ldg(o + 3 * r) + m * __ldg(d + 3 * r),
+                              __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1), __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2));
+}
+
 __global__ void field_samples_kernel(const float4 *__restrict__ lat, int R, float lo, float hi, int contracted,
                                      const float *__restrict__ o, const float *__restrict__ d,
                                      const float *__restrict__ t0, const float *__restrict__ t1,
@@ -117,6 +164,19 @@ nacc_status naccx_mse_grad(const float *color, const float *gt, int64_t n_rays, 
   if (!color || !gt || !g_color) return NACC_ERR_INVALID_ARGUMENT;
   mse_grad_kernel<<<blocks_for(3 * n_rays), 256, 0, stream>>>(color, gt, 3 * n_rays, 2.0f / (3.0f * (float)n_rays),
                                                               g_color);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
+}
+
+nacc_status naccx_sigma_at_samples(const float *sigma_lattice, int32_t res, float lo, float hi, int32_t contracted,
+                                   const float *rays_o, const float *rays_d, const float *t0, const float *t1,
+                                   const int32_t *ray_id, int64_t n, const int64_t *n_dev, float *sigma,
+                                   cudaStream_t stream) {
+  if (n < 0 || res < 2 || !(hi > lo)) return NACC_ERR_INVALID_ARGUMENT;
+  if (n == 0) return NACC_OK;
+  if (!sigma_lattice || !rays_o || !rays_d || !t0 || !t1 || !ray_id || !sigma) return NACC_ERR_INVALID_ARGUMENT;
+  field_sigma_kernel<<<blocks_for(n), 256, 0, stream>>>(sigma_lattice, res, lo, hi, contracted, rays_o, rays_d, t0, t1,
+                                                        ray_id, n, n_dev, sigma);
   g_launches++;
   return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
 }

@@ -20,13 +20,21 @@ class LatticeField:
         self.res = int(round((self.data.numel() // 4) ** (1.0 / 3.0)))
         assert self.res ** 3 * 4 == self.data.numel()
         self.lo, self.hi, self.contracted = float(lo), float(hi), int(bool(contracted))
+        self.sigma_only = self.data.view(-1, 4)[:, 0].contiguous()  # density-only lattice (4 B per cell)
 
     def at_samples(self, rays_o, rays_d, t0, t1, ray_id, want_rgb=True, n_dev=None):
         """σ (and rgb) at the interval midpoints; with n_dev (device int64) only
         the first *n_dev of the capacity-sized arrays are evaluated."""
         n = t0.numel()
         sigma = torch.empty(n, dtype=torch.float32, device=t0.device)
-        rgb = torch.empty((n, 3), dtype=torch.float32, device=t0.device) if want_rgb else None
+        if not want_rgb:
+            st = L.harness().naccx_sigma_at_samples(_ptr(self.sigma_only), self.res, self.lo, self.hi,
+                                                    self.contracted, _ptr(rays_o), _ptr(rays_d), _ptr(t0), _ptr(t1),
+                                                    _ptr(ray_id), n, _ptr(n_dev), _ptr(sigma), _stream())
+            if st != 0:
+                raise L.NaccError(st, "naccx_sigma_at_samples")
+            return sigma, None
+        rgb = torch.empty((n, 3), dtype=torch.float32, device=t0.device)
         st = L.harness().naccx_field_at_samples(_ptr(self.data), self.res, self.lo, self.hi, self.contracted,
                                                 _ptr(rays_o), _ptr(rays_d), _ptr(t0), _ptr(t1), _ptr(ray_id), n,
                                                 _ptr(n_dev), _ptr(sigma), _ptr(rgb), _stream())
