@@ -198,13 +198,17 @@ nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, i
 /* Backward of nacc_render_fwd (t detached): given upstream
  * g_color [n][3], g_opacity [n], g_depth [n] (each may be NULL = 0), writes
  * g_sigma [N] and g_rgb [N][3].  ctx from the forward (NULL = recompute, one
- * warp per ray); with ray_id and ctx the flat kernel runs. */
+ * warp per ray); with ray_id and ctx the flat kernel runs and needs a
+ * workspace of nacc_render_bwd_workspace_bytes(n_rays) bytes (per-ray
+ * gradient constants). */
+size_t nacc_render_bwd_workspace_bytes(int64_t n_rays);
 nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
                             const float *t0,
                             const float *t1, const float *sigma, const float *rgb,
                             int64_t n_samples, double neg_log_eps, const double *ctx,
                             const float *g_color, const float *g_opacity, const float *g_depth,
-                            float *g_sigma, float *g_rgb, cudaStream_t stream);
+                            float *g_sigma, float *g_rgb, void *ws, size_t ws_bytes,
+                            cudaStream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Proposal estimator: inverse-transform resampling (Eq. 1) of the  */

@@ -216,9 +216,10 @@ class _RenderFn(torch.autograd.Function):
         gc = None if g_color is None else g_color.contiguous().float()
         go = None if g_opacity is None else g_opacity.contiguous().float()
         gd = None if g_depth is None else g_depth.contiguous().float()
+        ws = _ws(L.lib().nacc_render_bwd_workspace_bytes(n), t0.device)
         check(L.lib().nacc_render_bwd(_ptr(packed_info), _ptr(ray_id), n, _ptr(t0), _ptr(t1), _ptr(sigma), _ptr(rgb),
                                       N, ctx.nle, _ptr(cx), _ptr(gc), _ptr(go), _ptr(gd), _ptr(g_sigma),
-                                      _ptr(g_rgb), _stream()), "nacc_render_bwd")
+                                      _ptr(g_rgb), _ptr(ws), ws.numel(), _stream()), "nacc_render_bwd")
         return None, None, None, None, g_sigma, g_rgb, None
 
 
@@ -258,10 +259,11 @@ def render_bwd(samples: PackedSamples, sigma: torch.Tensor, rgb: torch.Tensor, c
     rgb = _req(rgb.detach(), torch.float32, "rgb", 3 * N)
     g_sigma = torch.empty_like(sigma)
     g_rgb = torch.empty_like(rgb)
+    ws = _ws(L.lib().nacc_render_bwd_workspace_bytes(n), samples.t0.device)
     check(L.lib().nacc_render_bwd(_ptr(samples.packed_info), _ptr(samples.ray_id), n, _ptr(samples.t0),
                                   _ptr(samples.t1), _ptr(sigma), _ptr(rgb), N, neg_log_eps(eps), _ptr(ctx),
                                   _ptr(g_color), _ptr(g_opacity), _ptr(g_depth), _ptr(g_sigma), _ptr(g_rgb),
-                                  _stream()), "nacc_render_bwd")
+                                  _ptr(ws), ws.numel(), _stream()), "nacc_render_bwd")
     return g_sigma, g_rgb
 
 

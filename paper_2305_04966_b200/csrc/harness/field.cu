@@ -80,17 +80,87 @@ __device__ __forceinline__ float lattice_sigma_at(const float *__restrict__ lat,
   return acc;
 }
 
+// 4 consecutive samples per thread (vector loads); consecutive samples of a ray
+// usually share the 2x2x2 corner block, whose values are reused
 __global__ void field_sigma_kernel(const float *__restrict__ lat, int R, float lo, float hi, int contracted,
                                    const float *__restrict__ o, const float *__restrict__ d,
                                    const float *__restrict__ t0, const float *__restrict__ t1,
                                    const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
                                    float *__restrict__ sigma) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || (n_dev && i >= *n_dev)) return;
-  const int64_t r = __ldg(rid + i);
-  const float m = 0.5f * (__ldg(t0 + i) + __ldg(t1 + i));
-  sigma[i] = lattice_sigma_at(lat, R, lo, hi, contracted, __ldg(o + 3 * r) + m * __ldg(d + 3 * r),
-                              __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1), __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2));
+  const int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int64_t nn = n_dev ? min(n, *n_dev) : n;
+  if (q0 >= nn) return;
+  const bool vec = q0 + 3 < nn && ((reinterpret_cast<uintptr_t>(t0) | reinterpret_cast<uintptr_t>(t1) |
+                                    reinterpret_cast<uintptr_t>(rid) | reinterpret_cast<uintptr_t>(sigma)) & 15) == 0;
+  float a[4], b[4], out[4];
+  int32_t ri[4];
+  if (vec) {
+    const float4 A = __ldg(reinterpret_cast<const float4 *>(t0 + q0)), Bv = __ldg(reinterpret_cast<const float4 *>(t1 + q0));
+    const int4 Ri = __ldg(reinterpret_cast<const int4 *>(rid + q0));
+    a[0] = A.x; a[1] = A.y; a[2] = A.z; a[3] = A.w;
+    b[0] = Bv.x; b[1] = Bv.y; b[2] = Bv.z; b[3] = Bv.w;
+    ri[0] = Ri.x; ri[1] = Ri.y; ri[2] = Ri.z; ri[3] = Ri.w;
+  } else {
+    for (int j = 0; j < 4; ++j) {
+      const bool in = q0 + j < nn;
+      a[j] = in ? __ldg(t0 + q0 + j) : 0.f;
+      b[j] = in ? __ldg(t1 + q0 + j) : 0.f;
+      ri[j] = in ? __ldg(rid + q0 + j) : -1;
+    }
+  }
+  int32_t cur = -1;
+  float ox = 0, oy = 0, oz = 0, dx = 0, dy = 0, dz = 0;
+  int cached = -1;
+  float cv[8];
+  const float sc = (float)R / (hi - lo);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    out[j] = 0.f;
+    if (ri[j] < 0) continue;
+    if (ri[j] != cur) {
+      cur = ri[j];
+      ox = __ldg(o + 3 * cur); oy = __ldg(o + 3 * cur + 1); oz = __ldg(o + 3 * cur + 2);
+      dx = __ldg(d + 3 * cur); dy = __ldg(d + 3 * cur + 1); dz = __ldg(d + 3 * cur + 2);
+    }
+    const float m = 0.5f * (a[j] + b[j]);
+    float x = ox + m * dx, y = oy + m * dy, z = oz + m * dz;
+    if (contracted) {
+      const float nr = sqrtf(x * x + y * y + z * z);
+      if (nr > 1.0f) {
+        const float s2 = (2.0f - 1.0f / nr) / nr;
+        x *= s2; y *= s2; z *= s2;
+      }
+    }
+    if (!(x >= lo && x <= hi && y >= lo && y <= hi && z >= lo && z <= hi)) continue;
+    float u[3] = {(x - lo) * sc - 0.5f, (y - lo) * sc - 0.5f, (z - lo) * sc - 0.5f};
+    int i0[3];
+    float f[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      u[k] = fminf(fmaxf(u[k], 0.0f), (float)(R - 1));
+      i0[k] = min((int)floorf(u[k]), R - 2);
+      f[k] = u[k] - (float)i0[k];
+    }
+    const int base = i0[0] + R * (i0[1] + R * i0[2]);
+    if (base != cached) {
+      cached = base;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) cv[c] = __ldg(lat + base + (c & 1) + R * (((c >> 1) & 1) + R * (c >> 2)));
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int ddx = c & 1, ddy = (c >> 1) & 1, ddz = c >> 2;
+      acc += (ddx ? f[0] : 1.f - f[0]) * (ddy ? f[1] : 1.f - f[1]) * (ddz ? f[2] : 1.f - f[2]) * cv[c];
+    }
+    out[j] = acc;
+  }
+  if (vec) {
+    *reinterpret_cast<float4 *>(sigma + q0) = make_float4(out[0], out[1], out[2], out[3]);
+  } else {
+    for (int j = 0; j < 4; ++j)
+      if (q0 + j < nn) sigma[q0 + j] = out[j];
+  }
 }
 
 __global__ void field_samples_kernel(const float4 *__restrict__ lat, int R, float lo, float hi, int contracted,
@@ -175,8 +245,8 @@ nacc_status naccx_sigma_at_samples(const float *sigma_lattice, int32_t res, floa
   if (n < 0 || res < 2 || !(hi > lo)) return NACC_ERR_INVALID_ARGUMENT;
   if (n == 0) return NACC_OK;
   if (!sigma_lattice || !rays_o || !rays_d || !t0 || !t1 || !ray_id || !sigma) return NACC_ERR_INVALID_ARGUMENT;
-  field_sigma_kernel<<<blocks_for(n), 256, 0, stream>>>(sigma_lattice, res, lo, hi, contracted, rays_o, rays_d, t0, t1,
-                                                        ray_id, n, n_dev, sigma);
+  field_sigma_kernel<<<blocks_for((n + 3) / 4), 256, 0, stream>>>(sigma_lattice, res, lo, hi, contracted, rays_o,
+                                                                  rays_d, t0, t1, ray_id, n, n_dev, sigma);
   g_launches++;
   return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
 }

@@ -571,7 +571,7 @@ __device__ __forceinline__ void warp_items_S(const Items &it, double s[4], doubl
 }
 
 template <bool kVec>
-__global__ void __launch_bounds__(256) render_fwd_warp_kernel(
+__global__ void __launch_bounds__(256, 2) render_fwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
@@ -679,13 +679,27 @@ __device__ __forceinline__ RayGrad ray_grad(int64_t r, const double *__restrict_
   return q;
 }
 
+// per-ray constants of the backward, once per ray: g_C (as floats), and
+// (g_O', g_N, R) in fp64, with R = <g_C, C> + g_O' O + g_N N (see header)
+__global__ void __launch_bounds__(256) ray_grad_kernel(int64_t n_rays, const double *__restrict__ ctx,
+                                                       const float *__restrict__ g_color,
+                                                       const float *__restrict__ g_opacity,
+                                                       const float *__restrict__ g_depth, float4 *__restrict__ gcv,
+                                                       double2 *__restrict__ gq) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_rays) return;
+  const RayGrad q = ray_grad(r, ctx, g_color, g_opacity, g_depth);
+  gcv[r] = make_float4((float)q.gc0, (float)q.gc1, (float)q.gc2, 0.f);
+  gq[2 * r] = make_double2(q.gOp, q.gN);
+  gq[2 * r + 1] = make_double2(q.R, 0.0);
+}
+
 template <bool kVec>
-__global__ void __launch_bounds__(256) render_bwd_warp_kernel(
+__global__ void __launch_bounds__(256, 2) render_bwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
-    const float *__restrict__ rgb, double L, const double *__restrict__ ctx, const float *__restrict__ g_color,
-    const float *__restrict__ g_opacity, const float *__restrict__ g_depth, float *__restrict__ g_sigma,
-    float *__restrict__ g_rgb) {
+    const float *__restrict__ rgb, double L, const float4 *__restrict__ gcv, const double2 *__restrict__ gq,
+    float *__restrict__ g_sigma, float *__restrict__ g_rgb) {
   const int64_t wt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (wt >= n_wtiles) return;
   const int64_t N = packed_end(packed_info, n_rays);
@@ -694,56 +708,57 @@ __global__ void __launch_bounds__(256) render_bwd_warp_kernel(
   if (B >= E) return;
   Seg<1> carryS = seg_identity<1>(), carryP = seg_identity<1>();
   int32_t carry_rid = -1;
-  int32_t cached = -1;
-  RayGrad rg{};
   for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
     Items it;
     load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
     double s[4], S[4];
     warp_items_S(it, s, S, carryS);
-    float col[12];
-    load_rgb4(col, it, rgb, kVec);
-    double w[4], gwTea[4], Rr[4], gcs[4][3];
+    // phase A: per item g_w w (scan input), w and g_w T (1-α); the only state kept
+    double w[4], gwTea[4];
+    unsigned live = 0;
     Seg<1> agg = seg_identity<1>();
+    {
+      float col[12];
+      load_rgb4(col, it, rgb, kVec);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (it.valid[j] && it.rid[j] != cached) {
-        cached = it.rid[j];
-        rg = ray_grad(cached, ctx, g_color, g_opacity, g_depth);
+      for (int j = 0; j < 4; ++j) {
+        w[j] = 0.0;
+        gwTea[j] = 0.0;
+        double v = 0.0;
+        if (it.valid[j] && !(S[j] > L)) {
+          live |= 1u << j;
+          const float4 gc = __ldg(gcv + it.rid[j]);
+          const double2 gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
+          const double T = exp(-S[j]), ea = exp(-s[j]);
+          w[j] = T * (1.0 - ea);
+          const double gw = (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2] +
+                            gon.x + gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+          v = gw * w[j];
+          gwTea[j] = gw * T * ea;
+        }
+        s[j] = v;
+        Seg<1> x;
+        x.f = it.head[j];
+        x.v[0] = v;
+        agg = seg_combine(agg, x);
       }
-      Rr[j] = rg.R;
-      gcs[j][0] = rg.gc0;
-      gcs[j][1] = rg.gc1;
-      gcs[j][2] = rg.gc2;
-      const bool live = it.valid[j] && !(S[j] > L);
-      double v = 0.0;
-      w[j] = 0.0;
-      gwTea[j] = 0.0;
-      if (live) {
-        const double T = exp(-S[j]), ea = exp(-s[j]);
-        w[j] = T * (1.0 - ea);
-        const double gw = rg.gc0 * col[3 * j] + rg.gc1 * col[3 * j + 1] + rg.gc2 * col[3 * j + 2] + rg.gOp +
-                          rg.gN * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-        v = gw * w[j];
-        gwTea[j] = gw * T * ea;
-      }
-      Seg<1> x;
-      x.f = it.head[j];
-      x.v[0] = v;
-      agg = seg_combine(agg, x);
-      s[j] = v;  // reuse: the item's g_w w term
     }
     Seg<1> run = warp_seg_excl<1>(agg, carryP);
     float gs[4], gr[12];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + s[j];
-      const bool live = it.valid[j] && !(S[j] > L);
-      const double Q = Rr[j] - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
-      gs[j] = live ? (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q)) : 0.f;
-      gr[3 * j] = (float)(w[j] * gcs[j][0]);
-      gr[3 * j + 1] = (float)(w[j] * gcs[j][1]);
-      gr[3 * j + 2] = (float)(w[j] * gcs[j][2]);
+      gs[j] = 0.f;
+      gr[3 * j] = gr[3 * j + 1] = gr[3 * j + 2] = 0.f;
+      if (live & (1u << j)) {
+        const float4 gc = __ldg(gcv + it.rid[j]);
+        const double R = __ldg(gq + 2 * (int64_t)it.rid[j] + 1).x;
+        const double Q = R - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
+        gs[j] = (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q));
+        gr[3 * j] = (float)(w[j] * gc.x);
+        gr[3 * j + 1] = (float)(w[j] * gc.y);
+        gr[3 * j + 2] = (float)(w[j] * gc.z);
+      }
     }
     if (kVec && it.valid[0] && it.valid[3]) {
       *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
@@ -948,7 +963,8 @@ nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, i
 nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays, const float *t0,
                             const float *t1, const float *sigma, const float *rgb, int64_t n_samples,
                             double neg_log_eps, const double *ctx, const float *g_color, const float *g_opacity,
-                            const float *g_depth, float *g_sigma, float *g_rgb, cudaStream_t stream) {
+                            const float *g_depth, float *g_sigma, float *g_rgb, void *ws, size_t ws_bytes,
+                            cudaStream_t stream) {
   clear_error();
   nacc_status s = check_packed(packed_info, n_rays, n_samples);
   if (s != NACC_OK) return s;
@@ -956,18 +972,21 @@ nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, i
   if (n_rays == 0 || n_samples == 0) return NACC_OK;
   NACC_REQUIRE(t0 && t1 && sigma && g_sigma, "t0, t1, sigma, g_sigma must be non-NULL");
   if (ray_id && rgb && ctx) {
+    NACC_REQUIRE(ws && ws_bytes >= nacc_render_bwd_workspace_bytes(n_rays), "workspace too small");
+    float4 *gcv = static_cast<float4 *>(ws);
+    double2 *gq = reinterpret_cast<double2 *>(static_cast<char *>(ws) + align_up((size_t)n_rays * 16, 256));
+    ray_grad_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(n_rays, ctx, g_color, g_opacity, g_depth, gcv, gq);
     const int64_t n_wtiles = ceil_div(n_samples, kWarpTile);
     const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(rgb, 16) &&
                      aligned(ray_id, 16) && aligned(g_sigma, 16) && (!g_rgb || aligned(g_rgb, 16));
     const unsigned blocks = (unsigned)ceil_div(n_wtiles * 32, 256);
     if (vec)
       render_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
-                                                               rgb, neg_log_eps, ctx, g_color, g_opacity, g_depth,
-                                                               g_sigma, g_rgb);
+                                                               rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb);
     else
       render_bwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
-                                                                rgb, neg_log_eps, ctx, g_color, g_opacity, g_depth,
-                                                                g_sigma, g_rgb);
+                                                                rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb);
+    count_launch(1);
   } else {
     render_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, rgb,
                                                                        neg_log_eps, ctx, g_color, g_opacity, g_depth,
@@ -976,6 +995,11 @@ nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, i
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;
+}
+
+size_t nacc_render_bwd_workspace_bytes(int64_t n_rays) {
+  if (n_rays < 0) return 0;
+  return align_up((size_t)n_rays * 16, 256) + (size_t)n_rays * 32 + 256;
 }
 
 nacc_status nacc_render_weights_fwd(const int64_t *packed_info, int64_t n_rays, const float *t0, const float *t1,
