@@ -159,7 +159,7 @@ class Pipeline:
         self.rays_host = rays
         self.rays = [(torch.from_numpy(o).to(device), torch.from_numpy(d).to(device)) for o, d in rays]
         self.gt = torch.from_numpy(gt).to(device)
-        self.field = H.LatticeField(torch.from_numpy(lat.data.reshape(-1, 4)).to(device), lat.lo, lat.hi)
+        self.field = H.TextureField(torch.from_numpy(lat.data.reshape(-1, 4)).to(device), lat.lo, lat.hi)
         self.spec = N.GridSpec(roi=(0, 0, 0, 1, 1, 1), res=128, levels=1)
         self.step_size = float(np.float32(W.SQRT3 / 1024.0))
         self.params = N.MarchParams(step=self.step_size)

@@ -87,8 +87,16 @@ typedef struct {
   uint64_t seed;
 } nacc_march;
 
-/* Bytes of the bitfield for `grid`: 4*ceil(levels*res^3/32). 0 if invalid. */
+/* Bytes of the bitfield buffer for `grid` (0 if invalid): the public fine bits
+ * (4*ceil(levels*res^3/32) bytes, rounded up to 256) followed by a
+ * library-private skip mask (1 bit per 4^3 macro cell, when res % 4 == 0). */
 size_t nacc_grid_bits_bytes(const nacc_grid *grid);
+
+/* Rebuild the private skip mask of `bits` from its fine bits.  Required after
+ * the caller writes fine bits directly; nacc_occgrid_update does it itself.
+ * nacc_sampling_occgrid reads the mask (its results do not depend on it, only
+ * its speed — but a stale mask would skip occupied cells). */
+nacc_status nacc_grid_prepare(const nacc_grid *grid, uint32_t *bits, cudaStream_t stream);
 
 /* Workspace for nacc_sampling_occgrid / _fill with n_rays rays. */
 size_t nacc_sampling_occgrid_workspace_bytes(const nacc_grid *grid, const nacc_march *params,
@@ -101,7 +109,8 @@ size_t nacc_sampling_occgrid_workspace_bytes(const nacc_grid *grid, const nacc_m
  * whose box holds it (readings #1-#3; the fp32 op sequence there is
  * normative).  Emitted intervals are packed: t0 = t_k, t1 = t_{k+1},
  * ray_id = r, in ray then k order.
- *   bits          occupancy bitfield (layout above), nacc_grid_bits_bytes()
+ *   bits          occupancy bitfield (layout above), nacc_grid_bits_bytes() bytes,
+ *                 prepared (nacc_grid_prepare / nacc_occgrid_update)
  *   rays_o/_d     [n_rays][3] fp32 origins / unit directions
  *   t_min, t_max  optional per-ray near/far [n_rays] (NULL = params' planes);
  *                 the cone lattice requires t_min == NULL and stratified == 0
@@ -250,6 +259,7 @@ nacc_status nacc_occgrid_update(const nacc_grid *grid, float *density, const flo
                                 nacc_update_rule rule, float decay, float threshold,
                                 nacc_thresh_rule thresh_rule, uint32_t *bits, double *mean,
                                 void *ws, size_t ws_bytes, cudaStream_t stream);
+/* (bits: the full nacc_grid_bits_bytes() buffer; its skip mask is rebuilt.) */
 
 #ifdef __cplusplus
 }

@@ -45,6 +45,17 @@ nacc_status naccx_field_at_points(const float *lattice, int32_t res, float lo, f
 nacc_status naccx_mse_grad(const float *color, const float *gt, int64_t n_rays, float *g_color,
                            cudaStream_t stream);
 
+/* The same lattice in texture memory, sampled with hardware trilinear
+ * filtering (8-bit fractional weights).  naccx_tex_create copies the lattice
+ * (synchronises `stream`) and returns an opaque handle. */
+nacc_status naccx_tex_create(const float *lattice, int32_t res, uint64_t *handle, cudaStream_t stream);
+void naccx_tex_destroy(uint64_t handle);
+nacc_status naccx_tex_at_samples(uint64_t handle, float lo, float hi, int32_t contracted,
+                                 const float *rays_o, const float *rays_d, const float *t0,
+                                 const float *t1, const int32_t *ray_id, int64_t n,
+                                 const int64_t *n_dev, float *sigma, float *rgb,
+                                 cudaStream_t stream);
+
 uint64_t naccx_launch_count(void);
 
 #ifdef __cplusplus

@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     launch_count,
     neg_log_eps,
     owner_slab,
+    prepare_bits,
     render_weights,
     render_fwd,
     render_bwd,

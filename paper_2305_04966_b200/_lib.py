@@ -53,6 +53,7 @@ SIGNATURES = {
     "nacc_abi_version": (C.c_int, []),
     "nacc_launch_count": (C.c_uint64, []),
     "nacc_grid_bits_bytes": (SZ, [GP]),
+    "nacc_grid_prepare": (C.c_int, [GP, P, P]),
     "nacc_sampling_occgrid_workspace_bytes": (SZ, [GP, MP, I64]),
     "nacc_sampling_occgrid": (C.c_int, [GP, P, MP, P, P, P, P, I64, P, P, P, P, I64, P, P, P, SZ, P]),
     "nacc_sampling_occgrid_fill": (C.c_int, [GP, P, MP, P, P, P, P, I64, P, P, P, P, P, SZ, P]),
@@ -76,6 +77,9 @@ HARNESS_SIGNATURES = {
     "naccx_sigma_at_samples": (C.c_int, [P, I32, F, F, I32, P, P, P, P, P, I64, P, P, P]),
     "naccx_field_at_points": (C.c_int, [P, I32, F, F, I32, P, I64, F, P, P]),
     "naccx_mse_grad": (C.c_int, [P, P, I64, P, P]),
+    "naccx_tex_create": (C.c_int, [P, I32, C.POINTER(C.c_uint64), P]),
+    "naccx_tex_destroy": (None, [C.c_uint64]),
+    "naccx_tex_at_samples": (C.c_int, [C.c_uint64, F, F, I32, P, P, P, P, P, I64, P, P, P, P]),
     "naccx_launch_count": (C.c_uint64, []),
 }
 

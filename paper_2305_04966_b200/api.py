@@ -115,6 +115,19 @@ class PackedSamples:
 
 
 # ----------------------------------------------------------------------------- sampling
+def prepare_bits(grid: GridSpec, fine_bits: torch.Tensor) -> torch.Tensor:
+    """A full bitfield buffer (public fine bits + the library's skip mask) from
+    fine bits packed as in nacc.h; ``OccupancyGrid.bits`` is already prepared."""
+    g = grid.c()
+    nb = L.lib().nacc_grid_bits_bytes(C.byref(g)) // 4
+    fine_bits = _req(fine_bits, torch.int32, "bits")
+    full = torch.zeros(nb, dtype=torch.int32, device=fine_bits.device)
+    n = min(fine_bits.numel(), nb)
+    full[:n] = fine_bits.reshape(-1)[:n]
+    check(L.lib().nacc_grid_prepare(C.byref(g), _ptr(full), _stream()), "nacc_grid_prepare")
+    return full
+
+
 def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec, bits: torch.Tensor,
                      params: MarchParams, t_min: Optional[torch.Tensor] = None,
                      t_max: Optional[torch.Tensor] = None, capacity: Optional[int] = None,
@@ -130,6 +143,8 @@ def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec,
     rays_o = _req(rays_o, torch.float32, "rays_o", 3 * n)
     rays_d = _req(rays_d, torch.float32, "rays_d", 3 * n)
     bits = _req(bits, torch.int32, "bits")
+    if bits.numel() * 4 < lib.nacc_grid_bits_bytes(C.byref(grid.c())):
+        raise ValueError("bits must be a full prepared bitfield (OccupancyGrid.bits or prepare_bits())")
     if t_min is not None:
         t_min = _req(t_min, torch.float32, "t_min", n)
     if t_max is not None:

@@ -112,10 +112,10 @@ inline int grid_for(int64_t work_items, int per_block, int64_t cap = (1ll << 31)
   return (int)g;
 }
 
-// exclusive scan of int32 counts -> packed_info (start, count) and *total.
-// Workspace: scan_workspace_bytes(n).  Launches 3 kernels (2 if n small).
-size_t scan_workspace_bytes(int64_t n);
-cudaError_t scan_counts_to_packed(const int32_t *counts, int64_t n, int64_t *packed_info,
-                                  int64_t *total, void *ws, cudaStream_t stream);
+// occupancy bitfield auxiliary skip mask (gridaux.cu)
+constexpr int kMacroCells = 4;  // fine cells per macro cell and axis
+bool grid_skip_enabled(const nacc_grid &g);
+int64_t grid_aux_offset_words(const nacc_grid &g);
+cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream);
 
 }  // namespace nacc

@@ -2,78 +2,128 @@
 // transmittance is below ε are dropped before the differentiable pass.
 // Per ray the kept set is a prefix (S_i never decreases; reading #9), so the
 // filter is a per-ray cut (sequential fp64 sum, early exit) + exclusive scan of
-// the cuts + a compacting copy of the prefixes.
+// the cuts + a compacting copy (three kernels, no host sync).
 #include "common.cuh"
 
 namespace nacc {
 
-// one thread per ray: walk the ray in order, accumulating S_i = Σ_{j<i} σ_j δ_j
-// in fp64 exactly as the definition (σ_j δ_j is exact in fp64, so the sum is
-// the sequential one), and stop at the first S_i > L.  Only the samples up to
-// the cut are read (the kept prefix plus one), four loads in flight.
-__global__ void __launch_bounds__(256) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
-                                                         const float *__restrict__ t0, const float *__restrict__ t1,
-                                                         const float *__restrict__ sigma, double L,
-                                                         int32_t *__restrict__ cut_out) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n_rays) return;
-  const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
-  const int64_t st = pi.x, cnt = pi.y;
-  double S = 0.0;
-  int64_t cut = cnt;
-  for (int64_t i = 0; i < cnt; i += 4) {
-    float a[4], b[4], c[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool in = i + j < cnt;
-      a[j] = in ? __ldg(t0 + st + i + j) : 0.f;
-      b[j] = in ? __ldg(t1 + st + i + j) : 0.f;
-      c[j] = in ? __ldg(sigma + st + i + j) : 0.f;
-    }
-    bool done = false;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (!done && i + j < cnt) {
-        if (S > L) {
-          cut = i + j;
-          done = true;
-        } else {
-          S = __dadd_rn(S, __dmul_rn((double)c[j], __dsub_rn((double)b[j], (double)a[j])));
-        }
-      }
-    }
-    if (done) break;
-  }
-  cut_out[r] = (int32_t)cut;
+// Pass 1: one thread per ray walks its samples in order, accumulating
+// S_i = Σ_{j<i} σ_j δ_j in fp64 exactly as the definition (σ_j δ_j is exact in
+// fp64, so this is the sequential sum), stopping at the first S_i > L; only the
+// kept prefix plus a few samples are read.  Each block also reduces its cuts.
+constexpr int kFiltRays = 256;
+
+__device__ __forceinline__ int64_t block_sum_i64(int64_t v, int64_t *sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum_i64(v);
+  if (lane == 0) sm[warp] = v;
+  __syncthreads();
+  int64_t tot = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sm[w];
+  return tot;
 }
 
-// block of 256 consecutive rays: their kept prefixes are contiguous in the
-// output; each thread copies output positions, locating its ray by binary
-// search over the block's output starts (in shared memory)
-constexpr int kCopyRays = 256;
+__global__ void __launch_bounds__(kFiltRays) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
+                                                               const float *__restrict__ t0,
+                                                               const float *__restrict__ t1,
+                                                               const float *__restrict__ sigma, double L,
+                                                               int32_t *__restrict__ cut_out,
+                                                               int64_t *__restrict__ block_sums) {
+  __shared__ int64_t sm[kFiltRays / 32];
+  const int64_t r = (int64_t)blockIdx.x * kFiltRays + threadIdx.x;
+  int64_t cut = 0;
+  if (r < n_rays) {
+    const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
+    const int64_t st = pi.x, cnt = pi.y;
+    double S = 0.0;
+    cut = cnt;
+    for (int64_t i = 0; i < cnt; i += 4) {
+      float a[4], b[4], c[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool in = i + j < cnt;
+        a[j] = in ? __ldg(t0 + st + i + j) : 0.f;
+        b[j] = in ? __ldg(t1 + st + i + j) : 0.f;
+        c[j] = in ? __ldg(sigma + st + i + j) : 0.f;
+      }
+      bool done = false;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!done && i + j < cnt) {
+          if (S > L) {
+            cut = i + j;
+            done = true;
+          } else {
+            S = __dadd_rn(S, __dmul_rn((double)c[j], __dsub_rn((double)b[j], (double)a[j])));
+          }
+        }
+      }
+      if (done) break;
+    }
+    cut_out[r] = (int32_t)cut;
+  }
+  const int64_t tot = block_sum_i64(cut, sm);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+}
 
-__global__ void __launch_bounds__(kCopyRays) filter_copy_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
-                                                                const float *__restrict__ t0,
-                                                                const float *__restrict__ t1,
-                                                                const int64_t *__restrict__ packed_out,
-                                                                const int64_t *__restrict__ total, int64_t capacity,
-                                                                float *__restrict__ t0_out, float *__restrict__ t1_out,
-                                                                int32_t *__restrict__ ray_id_out) {
-  __shared__ int64_t s_out[kCopyRays + 1];
-  __shared__ int64_t s_in[kCopyRays];
-  if (*total > capacity) return;
-  const int64_t r0 = (int64_t)blockIdx.x * kCopyRays;
-  const int nr = (int)min((int64_t)kCopyRays, n_rays - r0);
-  const int t = threadIdx.x;
+// Pass 2 (one block): exclusive scan of the block sums in place; *total.
+__global__ void __launch_bounds__(1024) block_sums_scan_kernel(int64_t *__restrict__ sums, int64_t nb,
+                                                               int64_t *__restrict__ total) {
+  __shared__ int64_t sm[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t carry = 0;
+  for (int64_t base = 0; base < nb; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = i < nb ? sums[i] : 0;
+    const int64_t incl = warp_incl_scan_i64(v);
+    if (lane == 31) sm[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int64_t w = sm[lane];
+      const int64_t wi = warp_incl_scan_i64(w);
+      sm[lane] = wi - w;
+      if (lane == 31) sm[32] = wi;
+    }
+    __syncthreads();
+    if (i < nb) sums[i] = carry + sm[warp] + incl - v;
+    carry += sm[32];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// Pass 3: blocks of 256 consecutive rays scan their cuts (+ the block offset)
+// into packed_info', then copy the kept prefixes, which are contiguous in the
+// output; each thread locates its ray by binary search over the block's output
+// starts in shared memory, so stores are coalesced.
+__global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
+    const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
+    const float *__restrict__ t1, const int32_t *__restrict__ cuts, const int64_t *__restrict__ block_off,
+    const int64_t *__restrict__ total, int64_t capacity, int64_t *__restrict__ packed_out,
+    float *__restrict__ t0_out, float *__restrict__ t1_out, int32_t *__restrict__ ray_id_out) {
+  __shared__ int64_t s_out[kFiltRays + 1];
+  __shared__ int64_t s_in[kFiltRays];
+  __shared__ int64_t s_w[kFiltRays / 32];
+  const int64_t r0 = (int64_t)blockIdx.x * kFiltRays;
+  const int nr = (int)min((int64_t)kFiltRays, n_rays - r0);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t c = t < nr ? (int64_t)cuts[r0 + t] : 0;
+  const int64_t incl = warp_incl_scan_i64(c);
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  int64_t wbase = block_off[blockIdx.x];
+  for (int w = 0; w < warp; ++w) wbase += s_w[w];
+  const int64_t out = wbase + incl - c;
   if (t < nr) {
-    const longlong2 po = __ldg(reinterpret_cast<const longlong2 *>(packed_out) + r0 + t);
-    s_out[t] = po.x;
+    reinterpret_cast<longlong2 *>(packed_out)[r0 + t] = make_longlong2(out, c);
+    s_out[t] = out;
     s_in[t] = __ldg(packed_info + 2 * (r0 + t));
-    if (t == nr - 1) s_out[nr] = po.x + po.y;
+    if (t == nr - 1) s_out[nr] = out + c;
   }
   __syncthreads();
+  if (t0_out == nullptr || *total > capacity) return;
   const int64_t p0 = s_out[0], p1 = s_out[nr];
-  for (int64_t p = p0 + t; p < p1; p += kCopyRays) {
+  for (int64_t p = p0 + t; p < p1; p += kFiltRays) {
     int lo = 0, hi = nr - 1;  // largest k with s_out[k] <= p
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -87,13 +137,13 @@ __global__ void __launch_bounds__(kCopyRays) filter_copy_kernel(const int64_t *_
   }
 }
 
-static size_t filter_ws_layout(int64_t n, int32_t **cuts, void **scan_ws, void *base) {
+static size_t filter_ws_layout(int64_t n, int32_t **cuts, int64_t **bsums, void *base) {
   const size_t a = align_up((size_t)n * 4, 256);
   if (base) {
     *cuts = static_cast<int32_t *>(base);
-    *scan_ws = static_cast<char *>(base) + a;
+    *bsums = reinterpret_cast<int64_t *>(static_cast<char *>(base) + a);
   }
-  return a + scan_workspace_bytes(n);
+  return a + align_up(8 * (size_t)ceil_div(n, kFiltRays), 256);
 }
 
 }  // namespace nacc
@@ -127,18 +177,18 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   NACC_REQUIRE(capacity == 0 || (t0_out && t1_out && ray_id_out), "outputs must be non-NULL when capacity > 0");
   NACC_REQUIRE(ws && ws_bytes >= nacc_filter_workspace_bytes(n_rays), "workspace too small");
   int32_t *cuts;
-  void *scan_ws;
-  filter_ws_layout(n_rays, &cuts, &scan_ws, ws);
-  filter_cut_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts);
+  int64_t *bsums;
+  filter_ws_layout(n_rays, &cuts, &bsums, ws);
+  const int64_t nb = ceil_div(n_rays, kFiltRays);
+  filter_cut_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts,
+                                                             bsums);
+  block_sums_scan_kernel<<<1, 1024, 0, stream>>>(bsums, nb, total);
+  filter_copy_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, cuts, bsums, total, capacity,
+                                                             packed_info_out, capacity > 0 ? t0_out : nullptr, t1_out,
+                                                             ray_id_out);
+  count_launch(2);
   count_launch(1);
   NACC_CHECK_LAUNCH();
-  NACC_CUDA(scan_counts_to_packed(cuts, n_rays, packed_info_out, total, scan_ws, stream));
-  if (capacity > 0) {
-    filter_copy_kernel<<<grid_for(n_rays, kCopyRays), kCopyRays, 0, stream>>>(
-        packed_info, n_rays, t0, t1, packed_info_out, total, capacity, t0_out, t1_out, ray_id_out);
-    count_launch(1);
-    NACC_CHECK_LAUNCH();
-  }
   return NACC_OK;
 }
 

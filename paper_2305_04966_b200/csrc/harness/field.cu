@@ -251,6 +251,132 @@ nacc_status naccx_sigma_at_samples(const float *sigma_lattice, int32_t res, floa
   return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
 }
 
-uint64_t naccx_launch_count(void) { return g_launches.load(); }
-
 }  // extern "C"
+
+// ---------------------------------------------------------------- texture-unit field
+// The same cell-centre lattice held in 3-D CUDA arrays and sampled by the
+// texture unit (hardware trilinear filtering, clamp-to-edge, unnormalised
+// coordinates: texel i is centred at i + 0.5, so u = (x - lo) R / (hi - lo) is
+// the cell-centre lattice coordinate of the numpy field).  Hardware filtering
+// uses 8-bit fractional weights, which is fine for a stand-in NeRF.
+struct TexField {
+  cudaArray_t a_sig = nullptr, a_rgba = nullptr;
+  cudaTextureObject_t t_sig = 0, t_rgba = 0;
+  int res = 0;
+};
+
+extern "C" nacc_status naccx_tex_create(const float *lattice, int32_t res, uint64_t *handle, cudaStream_t stream) {
+  if (!lattice || res < 2 || !handle) return NACC_ERR_INVALID_ARGUMENT;
+  TexField *f = new TexField();
+  f->res = res;
+  const cudaExtent ext = make_cudaExtent(res, res, res);
+  cudaChannelFormatDesc d1 = cudaCreateChannelDesc<float>(), d4 = cudaCreateChannelDesc<float4>();
+  if (cudaMalloc3DArray(&f->a_sig, &d1, ext) != cudaSuccess || cudaMalloc3DArray(&f->a_rgba, &d4, ext) != cudaSuccess) {
+    delete f;
+    return NACC_ERR_CUDA;
+  }
+  // rgba lattice: copy the (σ, r, g, b) float4 lattice as is; σ-only: strided copy of the first channel
+  cudaMemcpy3DParms c4 = {};
+  c4.srcPtr = make_cudaPitchedPtr(const_cast<float *>(lattice), (size_t)res * 16, res, res);
+  c4.dstArray = f->a_rgba;
+  c4.extent = ext;
+  c4.kind = cudaMemcpyDeviceToDevice;
+  float *sig = nullptr;
+  if (cudaMemcpy3DAsync(&c4, stream) != cudaSuccess || cudaMalloc(&sig, (size_t)res * res * res * 4) != cudaSuccess)
+    return NACC_ERR_CUDA;
+  if (cudaMemcpy2DAsync(sig, 4, lattice, 16, 4, (size_t)res * res * res, cudaMemcpyDeviceToDevice, stream) != cudaSuccess)
+    return NACC_ERR_CUDA;
+  cudaMemcpy3DParms c1 = {};
+  c1.srcPtr = make_cudaPitchedPtr(sig, (size_t)res * 4, res, res);
+  c1.dstArray = f->a_sig;
+  c1.extent = ext;
+  c1.kind = cudaMemcpyDeviceToDevice;
+  if (cudaMemcpy3DAsync(&c1, stream) != cudaSuccess) return NACC_ERR_CUDA;
+  cudaStreamSynchronize(stream);
+  cudaFree(sig);
+  for (int which = 0; which < 2; ++which) {
+    cudaResourceDesc rd = {};
+    rd.resType = cudaResourceTypeArray;
+    rd.res.array.array = which ? f->a_rgba : f->a_sig;
+    cudaTextureDesc td = {};
+    td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+    td.filterMode = cudaFilterModeLinear;
+    td.readMode = cudaReadModeElementType;
+    td.normalizedCoords = 0;
+    if (cudaCreateTextureObject(which ? &f->t_rgba : &f->t_sig, &rd, &td, nullptr) != cudaSuccess) return NACC_ERR_CUDA;
+  }
+  *handle = reinterpret_cast<uint64_t>(f);
+  return NACC_OK;
+}
+
+extern "C" void naccx_tex_destroy(uint64_t handle) {
+  TexField *f = reinterpret_cast<TexField *>(handle);
+  if (!f) return;
+  cudaDestroyTextureObject(f->t_sig);
+  cudaDestroyTextureObject(f->t_rgba);
+  cudaFreeArray(f->a_sig);
+  cudaFreeArray(f->a_rgba);
+  delete f;
+}
+
+__device__ __forceinline__ bool tex_coord(float lo, float hi, float sc, int contracted, float &x, float &y, float &z) {
+  if (contracted) {
+    const float n = sqrtf(x * x + y * y + z * z);
+    if (n > 1.0f) {
+      const float s = (2.0f - 1.0f / n) / n;
+      x *= s;
+      y *= s;
+      z *= s;
+    }
+  }
+  if (!(x >= lo && x <= hi && y >= lo && y <= hi && z >= lo && z <= hi)) return false;
+  x = (x - lo) * sc;
+  y = (y - lo) * sc;
+  z = (z - lo) * sc;
+  return true;
+}
+
+template <bool kRGB>
+__global__ void tex_samples_kernel(cudaTextureObject_t tex, int R, float lo, float hi, int contracted,
+                                   const float *__restrict__ o, const float *__restrict__ d,
+                                   const float *__restrict__ t0, const float *__restrict__ t1,
+                                   const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
+                                   float *__restrict__ sigma, float *__restrict__ rgb) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || (n_dev && i >= *n_dev)) return;
+  const int64_t r = __ldg(rid + i);
+  const float m = 0.5f * (__ldg(t0 + i) + __ldg(t1 + i));
+  float x = __ldg(o + 3 * r) + m * __ldg(d + 3 * r);
+  float y = __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1);
+  float z = __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2);
+  const bool in = tex_coord(lo, hi, (float)R / (hi - lo), contracted, x, y, z);
+  if (kRGB) {
+    const float4 v = in ? tex3D<float4>(tex, x, y, z) : make_float4(0.f, 0.f, 0.f, 0.f);
+    sigma[i] = v.x;
+    rgb[3 * i] = v.y;
+    rgb[3 * i + 1] = v.z;
+    rgb[3 * i + 2] = v.w;
+  } else {
+    sigma[i] = in ? tex3D<float>(tex, x, y, z) : 0.f;
+  }
+}
+
+extern "C" nacc_status naccx_tex_at_samples(uint64_t handle, float lo, float hi, int32_t contracted, const float *rays_o,
+                                 const float *rays_d, const float *t0, const float *t1, const int32_t *ray_id,
+                                 int64_t n, const int64_t *n_dev, float *sigma, float *rgb, cudaStream_t stream) {
+  TexField *f = reinterpret_cast<TexField *>(handle);
+  if (!f || n < 0 || !(hi > lo)) return NACC_ERR_INVALID_ARGUMENT;
+  if (n == 0) return NACC_OK;
+  if (rgb)
+    tex_samples_kernel<true><<<blocks_for(n), 256, 0, stream>>>(f->t_rgba, f->res, lo, hi, contracted, rays_o, rays_d,
+                                                                t0, t1, ray_id, n, n_dev, sigma, rgb);
+  else
+    tex_samples_kernel<false><<<blocks_for(n), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
+                                                                 t0, t1, ray_id, n, n_dev, sigma, nullptr);
+  g_launches++;
+  return cudaGetLastError() == cudaSuccess ? NACC_OK : NACC_ERR_CUDA;
+}
+
+extern "C" uint64_t naccx_launch_count(void) { return g_launches.load(); }
+
+

@@ -1,0 +1,57 @@
+// lookback.cuh — single-pass exclusive scan across thread blocks (decoupled
+// look-back): tiles take increasing ids from an atomic counter, publish their
+// aggregate, and warp 0 walks back over predecessors (32 at a time) until it
+// finds an inclusive prefix.  Used by the packing steps (start = exclusive
+// prefix sum of counts) so count, scan and write happen in one kernel.
+#pragma once
+#include "common.cuh"
+
+namespace nacc {
+
+struct LookbackWs {
+  unsigned int tile_counter;
+  unsigned int pad;
+  unsigned long long status[1];  // [n_tiles]: (value << 2) | flag, flag 1 = aggregate, 2 = inclusive prefix
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// warp 0: publish this tile's aggregate and return its exclusive prefix
+__device__ __forceinline__ long long lookback(unsigned long long *st, int64_t tile, long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release(st, ((unsigned long long)agg << 2) | 2ull);
+    return 0;
+  }
+  if (lane == 0) st_release(st + tile, ((unsigned long long)agg << 2) | 1ull);
+  long long excl = 0;
+  int64_t j = tile - 1;  // lanes look at tiles j, j-1, ..., j-31
+  for (;;) {
+    const int64_t idx = j - lane;
+    unsigned long long w = idx >= 0 ? 0ull : 2ull;  // before tile 0: an inclusive prefix of 0
+    if (idx >= 0) {
+      do {
+        w = ld_acquire(st + idx);
+      } while ((w & 3ull) == 0ull);
+    }
+    const unsigned m2 = __ballot_sync(kFull, (w & 3ull) == 2ull);
+    const int last = m2 ? __ffs(m2) - 1 : 31;  // nearest predecessor with an inclusive prefix
+    long long v = lane <= last ? (long long)(w >> 2) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    excl += v;
+    if (m2) break;
+    j -= 32;
+  }
+  if (lane == 0) st_release(st + tile, ((unsigned long long)(excl + agg) << 2) | 2ull);
+  return excl;
+}
+
+}  // namespace nacc

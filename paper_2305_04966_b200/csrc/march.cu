@@ -12,6 +12,7 @@
 // The k range each warp scans is a conservative fp32 slab bound (±2 steps
 // around the padded outermost box); membership alone decides emission.
 #include "common.cuh"
+#include "lookback.cuh"
 
 namespace nacc {
 
@@ -89,7 +90,7 @@ __device__ __forceinline__ bool occupied(const GridConst &g, const uint32_t *__r
 // the segment AB (monotone lattice), so they share its bounding box; positions
 // use the same fp32 ops as P(k) and a 1e-3 macro-cell margin covers rounding.
 constexpr int kSeg = 8;    // lattice points per segment
-constexpr int kMacro = 4;  // fine cells per macro cell and axis
+constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
 constexpr float kSegEps = 1e-3f;
 
 template <bool kL1>
@@ -119,46 +120,6 @@ __device__ __forceinline__ bool segment_maybe_occupied(const GridConst &g, const
   const uint32_t q = (uint32_t)la * (uint32_t)(M * M * M) + (uint32_t)i0[0] +
                      (uint32_t)M * ((uint32_t)i0[1] + (uint32_t)M * (uint32_t)i0[2]);
   return (__ldg(mask2 + (q >> 5)) >> (q & 31u)) & 1u;
-}
-
-// macro[l][m] = OR of the 4^3 fine bits of macro cell m
-__global__ void macro_or_kernel(const uint32_t *__restrict__ bits, int levels, int R, uint8_t *__restrict__ macro) {
-  const int M = R / kMacro;
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= (int64_t)levels * M * M * M) return;
-  const int64_t M3 = (int64_t)M * M * M;
-  const int l = (int)(q / M3);
-  const int64_t m = q - l * M3;
-  const int mx = (int)(m % M), my = (int)((m / M) % M), mz = (int)(m / ((int64_t)M * M));
-  uint32_t acc = 0;
-  for (int dz = 0; dz < kMacro; ++dz)
-    for (int dy = 0; dy < kMacro; ++dy) {
-      const int64_t base = (int64_t)l * R * R * R + (int64_t)(mx * kMacro) +
-                           (int64_t)R * ((my * kMacro + dy) + (int64_t)R * (mz * kMacro + dz));
-      const uint32_t w = __ldg(bits + (base >> 5));
-      acc |= (w >> (base & 31)) & 0xFu;  // 4 consecutive x bits (base is a multiple of 4)
-    }
-  macro[q] = acc ? 1 : 0;
-}
-
-// mask2[l][m] = OR over macro cells m + {0,1}^3 (inside the level)
-__global__ void macro_dilate_kernel(const uint8_t *__restrict__ macro, int levels, int M, uint32_t *__restrict__ mask2) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t M3 = (int64_t)M * M * M, n = (int64_t)levels * M3;
-  bool on = false;
-  if (q < n) {
-    const int l = (int)(q / M3);
-    const int64_t m = q - l * M3;
-    const int mx = (int)(m % M), my = (int)((m / M) % M), mz = (int)(m / ((int64_t)M * M));
-    for (int dz = 0; dz < 2; ++dz)
-      for (int dy = 0; dy < 2; ++dy)
-        for (int dx = 0; dx < 2; ++dx) {
-          const int x = mx + dx, y = my + dy, z = mz + dz;
-          if (x < M && y < M && z < M) on = on || macro[l * M3 + x + (int64_t)M * (y + (int64_t)M * z)];
-        }
-  }
-  const unsigned b = __ballot_sync(kFull, on);
-  if ((threadIdx.x & 31) == 0 && q < n) mask2[q >> 5] = b;
 }
 
 // ---------------------------------------------------------------- per-ray setup
@@ -382,52 +343,6 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 // k-list overflowed is traversed again in phase 2, writing directly.
 constexpr int kFWarps = 4, kFRaysPerWarp = 4, kFTileRays = kFWarps * kFRaysPerWarp, kFKCap = 2048;
 
-struct LookbackWs {
-  unsigned int tile_counter;
-  unsigned int pad;
-  unsigned long long status[1];  // [n_tiles]: (value << 2) | flag, flag 1 = aggregate, 2 = inclusive prefix
-};
-
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// warp 0: publish this tile's aggregate and return its exclusive prefix
-__device__ __forceinline__ long long lookback(unsigned long long *st, int64_t tile, long long agg) {
-  const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) st_release(st, ((unsigned long long)agg << 2) | 2ull);
-    return 0;
-  }
-  if (lane == 0) st_release(st + tile, ((unsigned long long)agg << 2) | 1ull);
-  long long excl = 0;
-  int64_t j = tile - 1;  // lanes look at tiles j, j-1, ..., j-31
-  for (;;) {
-    const int64_t idx = j - lane;
-    unsigned long long w = idx >= 0 ? 0ull : 2ull;  // before tile 0: an inclusive prefix of 0
-    if (idx >= 0) {
-      do {
-        w = ld_acquire(st + idx);
-      } while ((w & 3ull) == 0ull);
-    }
-    const unsigned m2 = __ballot_sync(kFull, (w & 3ull) == 2ull);
-    const int last = m2 ? __ffs(m2) - 1 : 31;  // nearest predecessor with an inclusive prefix
-    long long v = lane <= last ? (long long)(w >> 2) : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    excl += v;
-    if (m2) break;
-    j -= 32;
-  }
-  if (lane == 0) st_release(st + tile, ((unsigned long long)(excl + agg) << 2) | 2ull);
-  return excl;
-}
-
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(kFWarps * 32) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
@@ -579,11 +494,8 @@ struct MarchWs {
   LookbackWs *lb;
   ConeHeader *hdr;
   float *tab;
-  uint8_t *macro;
-  uint32_t *mask2;
 };
 
-static bool skip_enabled(const nacc_grid &g) { return g.res % kMacro == 0 && g.res >= 2 * kMacro; }
 static int64_t fused_tiles(int64_t n) { return ceil_div(n, kFTileRays); }
 
 static size_t march_ws_layout(const nacc_grid &g, const nacc_march &p, int64_t n, MarchWs *w, void *base) {
@@ -594,25 +506,17 @@ static size_t march_ws_layout(const nacc_grid &g, const nacc_march &p, int64_t n
     return o;
   };
   const size_t o_lb = take(8 + 8 * (size_t)fused_tiles(n));
-  size_t o_hdr = 0, o_tab = 0, o_macro = 0, o_mask = 0;
+  size_t o_hdr = 0, o_tab = 0;
   const bool cone = p.cone_angle > 0.0f;
   if (cone) {
     o_hdr = take(sizeof(ConeHeader));
     o_tab = take((size_t)(kConeTableMax + 1) * 4);
-  }
-  const bool skip = skip_enabled(g);
-  if (skip) {
-    const int64_t M = g.res / kMacro, n_m = (int64_t)g.levels * M * M * M;
-    o_macro = take((size_t)n_m);
-    o_mask = take((size_t)ceil_div(n_m, 32) * 4);
   }
   if (w && base) {
     char *b = static_cast<char *>(base);
     w->lb = reinterpret_cast<LookbackWs *>(b + o_lb);
     w->hdr = cone ? reinterpret_cast<ConeHeader *>(b + o_hdr) : nullptr;
     w->tab = cone ? reinterpret_cast<float *>(b + o_tab) : nullptr;
-    w->macro = skip ? reinterpret_cast<uint8_t *>(b + o_macro) : nullptr;
-    w->mask2 = skip ? reinterpret_cast<uint32_t *>(b + o_mask) : nullptr;
   }
   return off;
 }
@@ -680,9 +584,10 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
   const GridConst g = make_grid_const(*grid);
   const MarchConst p = make_march_const(*params);
   const bool cone = params->cone_angle > 0.0f;
-  const bool skip = skip_enabled(*grid);
+  const bool skip = grid_skip_enabled(*grid);
   const bool l1 = grid->levels == 1;
   const int M = grid->res / kMacro;
+  const uint32_t *mask2 = bits + grid_aux_offset_words(*grid);  // built by nacc_grid_prepare / nacc_occgrid_update
   if (cone) {  // shared cone lattice table (reading #5)
     NACC_CUDA(cudaMemsetAsync(w.hdr, 0, sizeof(ConeHeader), stream));
     cone_tcap_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(g, p, rays_o, rays_d, t_max, n_rays, w.hdr);
@@ -690,21 +595,14 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
     count_launch(2);
     NACC_CHECK_LAUNCH();
   }
-  if (skip) {  // macro-cell occupancy for empty-space skipping (rebuilt from the bits every call)
-    const int64_t n_m = (int64_t)grid->levels * M * M * M;
-    macro_or_kernel<<<grid_for(n_m, 256), 256, 0, stream>>>(bits, grid->levels, grid->res, w.macro);
-    macro_dilate_kernel<<<grid_for(n_m, 256), 256, 0, stream>>>(w.macro, grid->levels, M, w.mask2);
-    count_launch(2);
-    NACC_CHECK_LAUNCH();
-  }
   if (!fill) {
     const int64_t n_tiles = fused_tiles(n_rays);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
-    NACC_DISPATCH3(march_fused_kernel, (unsigned)n_tiles, kFWarps * 32, stream, g, p, bits, w.mask2, M, rays_o,
+    NACC_DISPATCH3(march_fused_kernel, (unsigned)n_tiles, kFWarps * 32, stream, g, p, bits, mask2, M, rays_o,
                    rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,
                    status_out, t0, t1, ray_id);
   } else {
-    NACC_DISPATCH3(march_fill_kernel, (unsigned)grid_for(n_rays * 32, 256), 256, stream, g, p, bits, w.mask2, M,
+    NACC_DISPATCH3(march_fill_kernel, (unsigned)grid_for(n_rays * 32, 256), 256, stream, g, p, bits, mask2, M,
                    rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, packed_info, t0, t1, ray_id);
   }
   count_launch(1);
@@ -754,7 +652,7 @@ nacc_status nacc_sampling_occgrid_fill(const nacc_grid *grid, const uint32_t *bi
   if (st != NACC_OK) return st;
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(packed_info && t0 && t1 && ray_id, "packed_info, t0, t1, ray_id must be non-NULL");
-  // the cone table and macro mask live in the workspace; they are rebuilt here
+  // the cone table lives in the workspace; it is rebuilt here
   return launch_march(true, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays,
                       const_cast<int64_t *>(packed_info), t0, t1, ray_id, 0, nullptr, nullptr, ws, stream);
 }

@@ -179,6 +179,7 @@ nacc_status nacc_occgrid_update(const nacc_grid *grid, float *density, const flo
     count_launch(1);
   }
   NACC_CHECK_LAUNCH();
+  NACC_CUDA(grid_prepare(*grid, bits, stream));  // refresh the march's skip mask
   return NACC_OK;
 }
 

@@ -52,6 +52,35 @@ class LatticeField:
         return out
 
 
+class TextureField(LatticeField):
+    """LatticeField sampled by the texture unit (hardware trilinear filtering)."""
+
+    def __init__(self, data: torch.Tensor, lo: float, hi: float, contracted: bool = False):
+        super().__init__(data, lo, hi, contracted)
+        h = C.c_uint64()
+        st = L.harness().naccx_tex_create(_ptr(self.data), self.res, C.byref(h), _stream())
+        if st != 0:
+            raise L.NaccError(st, "naccx_tex_create")
+        self.handle = h.value
+
+    def at_samples(self, rays_o, rays_d, t0, t1, ray_id, want_rgb=True, n_dev=None):
+        n = t0.numel()
+        sigma = torch.empty(n, dtype=torch.float32, device=t0.device)
+        rgb = torch.empty((n, 3), dtype=torch.float32, device=t0.device) if want_rgb else None
+        st = L.harness().naccx_tex_at_samples(self.handle, self.lo, self.hi, self.contracted, _ptr(rays_o),
+                                              _ptr(rays_d), _ptr(t0), _ptr(t1), _ptr(ray_id), n, _ptr(n_dev),
+                                              _ptr(sigma), _ptr(rgb), _stream())
+        if st != 0:
+            raise L.NaccError(st, "naccx_tex_at_samples")
+        return sigma, rgb
+
+    def __del__(self):
+        try:
+            L.harness().naccx_tex_destroy(self.handle)
+        except Exception:
+            pass
+
+
 def mse_grad(color: torch.Tensor, gt: torch.Tensor) -> torch.Tensor:
     n = color.shape[0]
     g = torch.empty_like(color)

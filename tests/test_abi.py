@@ -55,13 +55,13 @@ def test_version_and_sizes(lib):
 
     assert lib.nacc_abi_version() == 1
     g = GridSpec(res=128, levels=4).c()
-    assert lib.nacc_grid_bits_bytes(C.byref(g)) == 4 * 128**3 // 8
+    assert lib.nacc_grid_bits_bytes(C.byref(g)) == 4 * 128**3 // 8 + 4 * 32**3 // 8  # fine bits + skip mask
     g.levels = 0
     assert lib.nacc_grid_bits_bytes(C.byref(g)) == 0
     g = GridSpec(res=128).c()
     p = MarchParams(step=0.01).c()
     assert lib.nacc_sampling_occgrid_workspace_bytes(C.byref(g), C.byref(p), 1 << 18) >= (1 << 18) // 2
-    assert lib.nacc_filter_workspace_bytes(1000) >= 4000
+    assert lib.nacc_filter_workspace_bytes(1000) >= 8 + 8 * 4
 
 
 def test_host_validation_rejects_before_launch(lib):

@@ -45,11 +45,11 @@ def cuda(a, dtype=None):
 
 
 def gpu_march(N, occ, levels, res, roi, o, d, **kw):
-    bits = cuda(W.pack_bits(occ).view(np.int32))
     t_min = kw.pop("t_min", None)
     t_max = kw.pop("t_max", None)
     capacity = kw.pop("capacity", None)
     grid = N.GridSpec(roi=tuple(roi), res=res, levels=levels)
+    bits = N.prepare_bits(grid, cuda(W.pack_bits(occ).view(np.int32)))
     p = N.MarchParams(**kw)
     s = N.sampling_occgrid(cuda(o), cuda(d), grid, bits, p, None if t_min is None else cuda(t_min),
                            None if t_max is None else cuda(t_max), capacity=capacity)
