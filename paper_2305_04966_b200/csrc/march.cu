@@ -93,20 +93,26 @@ constexpr int kSeg = 8;    // lattice points per segment
 constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
 constexpr float kSegEps = 1e-3f;
 
+// Returns 0 (skip the segment), 1 (evaluate; the segment lies inside the
+// single level's box with margin, so P(k) can skip the box test) or 2
+// (evaluate with the full predicate).
 template <bool kL1>
-__device__ __forceinline__ bool segment_maybe_occupied(const GridConst &g, const uint32_t *__restrict__ mask2, int M,
-                                                       const float A[3], const float B[3]) {
-  const int la = level_of<kL1>(g, A[0], A[1], A[2]);
-  if (la < 0 || la != level_of<kL1>(g, B[0], B[1], B[2])) return true;
-  if (!kL1 && la >= 1) {
-    bool meets = true;
+__device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *__restrict__ mask2, int M,
+                                            const float A[3], const float B[3]) {
+  int la = 0;
+  if (!kL1) {
+    la = level_of<false>(g, A[0], A[1], A[2]);
+    if (la < 0 || la != level_of<false>(g, B[0], B[1], B[2])) return 2;
+    if (la >= 1) {
+      bool meets = true;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const float lo = fminf(A[a], B[a]), hi = fmaxf(A[a], B[a]);
-      const float pad = kSegEps * (g.hi[la - 1][a] - g.lo[la - 1][a]);
-      meets = meets && hi >= g.lo[la - 1][a] - pad && lo <= g.hi[la - 1][a] + pad;
+      for (int a = 0; a < 3; ++a) {
+        const float lo = fminf(A[a], B[a]), hi = fmaxf(A[a], B[a]);
+        const float pad = kSegEps * (g.hi[la - 1][a] - g.lo[la - 1][a]);
+        meets = meets && hi >= g.lo[la - 1][a] - pad && lo <= g.hi[la - 1][a] + pad;
+      }
+      if (meets) return 2;
     }
-    if (meets) return true;
   }
   int i0[3];
 #pragma unroll
@@ -114,12 +120,32 @@ __device__ __forceinline__ bool segment_maybe_occupied(const GridConst &g, const
     const float sm = g.s[la][a] * (1.0f / kMacro);
     const float ua = (A[a] - g.lo[la][a]) * sm, ub = (B[a] - g.lo[la][a]) * sm;
     const int lo = (int)floorf(fminf(ua, ub) - kSegEps), hi = (int)floorf(fmaxf(ua, ub) + kSegEps);
-    if (hi - lo > 1) return true;
+    // single level: a segment reaching outside [0, M) macro cells (with margin) touches the box faces
+    if (kL1 && (lo < 0 || hi >= M)) return 2;
+    if (hi - lo > 1) return 2;
     i0[a] = min(max(lo, 0), M - 1);
   }
   const uint32_t q = (uint32_t)la * (uint32_t)(M * M * M) + (uint32_t)i0[0] +
                      (uint32_t)M * ((uint32_t)i0[1] + (uint32_t)M * (uint32_t)i0[2]);
-  return (__ldg(mask2 + (q >> 5)) >> (q & 31u)) & 1u;
+  if (!((__ldg(mask2 + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
+  return kL1 ? 1 : 2;
+}
+
+// P(k) for a point known to lie inside the (single) level box by a margin far
+// above the fp32 error: the box test is skipped, the rest is the normative
+// sequence of occupied()
+__device__ __forceinline__ bool occupied_interior(const GridConst &g, const uint32_t *__restrict__ bits, float m,
+                                                  float ox, float oy, float oz, float dx, float dy, float dz) {
+  const float x = __fmaf_rn(m, dx, ox), y = __fmaf_rn(m, dy, oy), z = __fmaf_rn(m, dz, oz);
+  const int R = g.res;
+  int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[0][0]), g.s[0][0]));
+  int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[0][1]), g.s[0][1]));
+  int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[0][2]), g.s[0][2]));
+  ix = min(max(ix, 0), R - 1);
+  iy = min(max(iy, 0), R - 1);
+  iz = min(max(iz, 0), R - 1);
+  const uint32_t q = (uint32_t)ix + (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
+  return (__ldg(bits + (q >> 5)) >> (q & 31u)) & 1u;
 }
 
 // ---------------------------------------------------------------- per-ray setup
@@ -299,30 +325,37 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
     if (kSkip) {
       const int ks = k0 + lane * kSeg;
       bool flag = false;
+      int code = 0;
       if (ks < ke) {
         const int kl = min(ks + kSeg - 1, ke - 1);
         const float ma = lattice_mid<kCone>(p, s, tab, ks), mb = lattice_mid<kCone>(p, s, tab, kl);
         const float A[3] = {__fmaf_rn(ma, s.dx, s.ox), __fmaf_rn(ma, s.dy, s.oy), __fmaf_rn(ma, s.dz, s.oz)};
         const float B[3] = {__fmaf_rn(mb, s.dx, s.ox), __fmaf_rn(mb, s.dy, s.oy), __fmaf_rn(mb, s.dz, s.oz)};
-        flag = segment_maybe_occupied<kL1>(g, mask2, M, A, B);
+        code = segment_test<kL1>(g, mask2, M, A, B);
+        flag = code != 0;
       }
       const unsigned F = __ballot_sync(kFull, flag);
-      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane;
+      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : 0);
       __syncwarp();
       nseg = __popc(F);
     }
     for (int first = 0; first < nseg; first += 4) {
       int k;
+      bool interior = false;
       if (kSkip) {
         const int idx = first + (lane >> 3);
-        k = idx < nseg ? k0 + seglist[idx] * kSeg + (lane & 7) : ke;
+        const int e = idx < nseg ? seglist[idx] : 0;
+        k = idx < nseg ? k0 + (e & 0xff) * kSeg + (lane & 7) : ke;
+        interior = kL1 && (e & 0x100);
       } else {
         k = k0 + lane;
       }
       bool pred = false;
       if (k < ke) {
         const float m = lattice_mid<kCone>(p, s, tab, k);
-        pred = (m < s.far_r) && occupied<kL1>(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz);
+        if (m < s.far_r)
+          pred = interior ? occupied_interior(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz)
+                          : occupied<kL1>(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz);
       }
       const unsigned b = __ballot_sync(kFull, pred);
       emit(b, pred, k, cnt);

@@ -211,276 +211,13 @@ __global__ void __launch_bounds__(256) render_bwd_kernel(const int64_t *__restri
   }
 }
 
-// ------------------------------------------------------------------ flat (ray-aligned tiles) fused render
-// Blocks own ray-aligned sample ranges [B, E) of ~kTile samples and walk them in
-// chunks of 256 threads x 4 consecutive samples; the open ray is carried across
-// chunks (segscan.cuh).  Per-ray outputs are written by the ray's last sample;
-// extra blocks past the tiles zero the outputs of rays without samples.
-constexpr int kFlatThreads = 256, kFlatItems = 4, kFlatWarps = kFlatThreads / 32;
-constexpr int kFlatChunk = kFlatThreads * kFlatItems;
-constexpr int64_t kFlatTile = 2048;
-
+// Per-thread view of 4 consecutive packed samples.
 struct Items {
   int64_t q0;
   bool valid[4], head[4], tail[4];
   float t0[4], t1[4], sg[4];
   int32_t rid[4];
 };
-
-template <bool kVec>
-__device__ __forceinline__ void load_items(Items &it, int64_t c0, int64_t B, int64_t E, const float *__restrict__ t0,
-                                           const float *__restrict__ t1, const float *__restrict__ sigma,
-                                           const int32_t *__restrict__ ray_id) {
-  const int64_t q0 = c0 + (int64_t)threadIdx.x * kFlatItems;
-  it.q0 = q0;
-  const bool full = kVec && q0 >= B && q0 + 3 < E;
-  if (full) {
-    const float4 a = __ldg(reinterpret_cast<const float4 *>(t0 + q0));
-    const float4 b = __ldg(reinterpret_cast<const float4 *>(t1 + q0));
-    const float4 c = __ldg(reinterpret_cast<const float4 *>(sigma + q0));
-    const int4 d = __ldg(reinterpret_cast<const int4 *>(ray_id + q0));
-    it.t0[0] = a.x; it.t0[1] = a.y; it.t0[2] = a.z; it.t0[3] = a.w;
-    it.t1[0] = b.x; it.t1[1] = b.y; it.t1[2] = b.z; it.t1[3] = b.w;
-    it.sg[0] = c.x; it.sg[1] = c.y; it.sg[2] = c.z; it.sg[3] = c.w;
-    it.rid[0] = d.x; it.rid[1] = d.y; it.rid[2] = d.z; it.rid[3] = d.w;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) it.valid[j] = true;
-  } else {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t q = q0 + j;
-      it.valid[j] = q >= B && q < E;
-      it.t0[j] = it.valid[j] ? __ldg(t0 + q) : 0.f;
-      it.t1[j] = it.valid[j] ? __ldg(t1 + q) : 0.f;
-      it.sg[j] = it.valid[j] ? __ldg(sigma + q) : 0.f;
-      it.rid[j] = it.valid[j] ? __ldg(ray_id + q) : -1;
-    }
-  }
-  const int32_t prev = (q0 - 1 >= B && q0 - 1 < E) ? __ldg(ray_id + q0 - 1) : -1;
-  const int32_t next = (q0 + 4 >= B && q0 + 4 < E) ? __ldg(ray_id + q0 + 4) : -2;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int32_t pr = j == 0 ? prev : it.rid[j - 1];
-    const int32_t nx = j == 3 ? next : (it.valid[j + 1] ? it.rid[j + 1] : -2);
-    it.head[j] = it.valid[j] && (q0 + j == B || it.rid[j] != pr);
-    it.tail[j] = it.valid[j] && (q0 + j + 1 == E || it.rid[j] != nx);
-  }
-}
-
-// entering optical depth S_j of the thread's items (fp64 segmented exclusive scan)
-__device__ __forceinline__ void items_optical_depth(const Items &it, double s[4], double S[4], Seg<1> &carry,
-                                                    Seg<1> *smem) {
-  Seg<1> agg = seg_identity<1>();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    s[j] = it.valid[j] ? (double)it.sg[j] * ((double)it.t1[j] - (double)it.t0[j]) : 0.0;
-    Seg<1> x;
-    x.f = it.head[j];
-    x.v[0] = s[j];
-    agg = seg_combine(agg, x);
-  }
-  Seg<1> run = block_seg_excl<1, kFlatWarps>(agg, carry, smem);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    S[j] = it.head[j] ? 0.0 : run.v[0];
-    Seg<1> x;
-    x.f = it.head[j];
-    x.v[0] = s[j];
-    run = seg_combine(run, x);
-  }
-}
-
-template <bool kVec>
-__global__ void __launch_bounds__(kFlatThreads) render_fwd_flat_kernel(
-    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t N,
-    int64_t n_tiles, const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
-    const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
-    float *__restrict__ depth, double *__restrict__ ctx) {
-  __shared__ Seg<1> smS[kFlatWarps + 1];
-  __shared__ Seg<5> smC[kFlatWarps + 1];
-  if ((int64_t)blockIdx.x >= n_tiles) {  // rays without samples
-    const int64_t r = ((int64_t)blockIdx.x - n_tiles) * kFlatThreads + threadIdx.x;
-    if (r < n_rays && packed_info[2 * r + 1] == 0) {
-      if (color) { color[3 * r] = 0.f; color[3 * r + 1] = 0.f; color[3 * r + 2] = 0.f; }
-      if (opacity) opacity[r] = 0.f;
-      if (depth) depth[r] = 0.f;
-      if (ctx) for (int k = 0; k < 5; ++k) ctx[5 * r + k] = 0.0;
-    }
-    return;
-  }
-  N = packed_end(packed_info, n_rays);  // samples in use (the arrays may be a larger capacity)
-  const int64_t B = snap_to_ray(packed_info, ray_id, (int64_t)blockIdx.x * kFlatTile, N);
-  const int64_t E = snap_to_ray(packed_info, ray_id, ((int64_t)blockIdx.x + 1) * kFlatTile, N);
-  if (B >= E) return;
-  Seg<1> carryS = seg_identity<1>();
-  Seg<5> carryC = seg_identity<5>();
-  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kFlatChunk) {
-    Items it;
-    load_items<kVec>(it, c0, B, E, t0, t1, sigma, ray_id);
-    double s[4], S[4];
-    items_optical_depth(it, s, S, carryS, smS);
-    float col[12];
-    const bool full = kVec && it.valid[0] && it.valid[3];
-    if (full) {
-      const float4 *p = reinterpret_cast<const float4 *>(rgb + 3 * it.q0);
-      const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-      col[0] = a.x; col[1] = a.y; col[2] = a.z; col[3] = a.w; col[4] = b.x; col[5] = b.y;
-      col[6] = b.z; col[7] = b.w; col[8] = c.x; col[9] = c.y; col[10] = c.z; col[11] = c.w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) col[3 * j + ch] = it.valid[j] ? __ldg(rgb + 3 * (it.q0 + j) + ch) : 0.f;
-    }
-    Seg<5> items[4];
-    Seg<5> agg = seg_identity<5>();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool live = it.valid[j] && !(S[j] > L);
-      const double w = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
-      items[j].f = it.head[j];
-      items[j].v[0] = w * (double)col[3 * j];
-      items[j].v[1] = w * (double)col[3 * j + 1];
-      items[j].v[2] = w * (double)col[3 * j + 2];
-      items[j].v[3] = w;
-      items[j].v[4] = w * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-      agg = seg_combine(agg, items[j]);
-    }
-    Seg<5> run = block_seg_excl<5, kFlatWarps>(agg, carryC, smC);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      run = seg_combine(run, items[j]);
-      if (it.tail[j]) {
-        const int64_t r = it.rid[j];
-        if (color) {
-          color[3 * r] = (float)run.v[0];
-          color[3 * r + 1] = (float)run.v[1];
-          color[3 * r + 2] = (float)run.v[2];
-        }
-        if (opacity) opacity[r] = (float)run.v[3];
-        if (depth) depth[r] = (float)(run.v[4] / fmax(run.v[3], 1e-10));
-        if (ctx)
-#pragma unroll
-          for (int k = 0; k < 5; ++k) ctx[5 * r + k] = run.v[k];
-      }
-    }
-  }
-}
-
-template <bool kVec>
-__global__ void __launch_bounds__(kFlatThreads) render_bwd_flat_kernel(
-    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_tiles,
-    const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
-    const float *__restrict__ rgb, double L, const double *__restrict__ ctx, const float *__restrict__ g_color,
-    const float *__restrict__ g_opacity, const float *__restrict__ g_depth, float *__restrict__ g_sigma,
-    float *__restrict__ g_rgb) {
-  __shared__ Seg<1> smS[kFlatWarps + 1];
-  __shared__ Seg<1> smP[kFlatWarps + 1];
-  const int64_t N = packed_end(packed_info, n_rays);  // samples in use (arrays may be a larger capacity)
-  const int64_t B = snap_to_ray(packed_info, ray_id, (int64_t)blockIdx.x * kFlatTile, N);
-  const int64_t E = snap_to_ray(packed_info, ray_id, ((int64_t)blockIdx.x + 1) * kFlatTile, N);
-  if (B >= E) return;
-  Seg<1> carryS = seg_identity<1>(), carryP = seg_identity<1>();
-  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kFlatChunk) {
-    Items it;
-    load_items<kVec>(it, c0, B, E, t0, t1, sigma, ray_id);
-    double s[4], S[4];
-    items_optical_depth(it, s, S, carryS, smS);
-    float col[12];
-    const bool full = kVec && it.valid[0] && it.valid[3];
-    if (full) {
-      const float4 *p = reinterpret_cast<const float4 *>(rgb + 3 * it.q0);
-      const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-      col[0] = a.x; col[1] = a.y; col[2] = a.z; col[3] = a.w; col[4] = b.x; col[5] = b.y;
-      col[6] = b.z; col[7] = b.w; col[8] = c.x; col[9] = c.y; col[10] = c.z; col[11] = c.w;
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) col[3 * j + ch] = it.valid[j] ? __ldg(rgb + 3 * (it.q0 + j) + ch) : 0.f;
-    }
-    // per-ray constants of the backward (gathered; consecutive items share a ray)
-    double gc[4][3], gOp[4], gN[4], Rr[4];
-    int32_t last = -1;
-    double lc0 = 0, lc1 = 0, lc2 = 0, lop = 0, lgn = 0, lR = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (it.valid[j] && it.rid[j] != last) {
-        const int64_t r = it.rid[j];
-        last = it.rid[j];
-        const double *cx = ctx + 5 * r;
-        const double C0 = cx[0], C1 = cx[1], C2 = cx[2], O = cx[3], Nn = cx[4];
-        lc0 = g_color ? (double)__ldg(g_color + 3 * r) : 0.0;
-        lc1 = g_color ? (double)__ldg(g_color + 3 * r + 1) : 0.0;
-        lc2 = g_color ? (double)__ldg(g_color + 3 * r + 2) : 0.0;
-        const double gO = g_opacity ? (double)__ldg(g_opacity + r) : 0.0;
-        const double gD = g_depth ? (double)__ldg(g_depth + r) : 0.0;
-        if (O > 1e-10) {
-          const double inv = 1.0 / O;
-          lgn = gD * inv;
-          lop = gO - gD * Nn * inv * inv;
-        } else {
-          lgn = gD * 1e10;
-          lop = gO;
-        }
-        lR = lc0 * C0 + lc1 * C1 + lc2 * C2 + lop * O + lgn * Nn;
-      }
-      gc[j][0] = lc0; gc[j][1] = lc1; gc[j][2] = lc2;
-      gOp[j] = lop; gN[j] = lgn; Rr[j] = lR;
-    }
-    double w[4], gwTea[4];
-    Seg<1> items[4];
-    Seg<1> agg = seg_identity<1>();
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool live = it.valid[j] && !(S[j] > L);
-      double v = 0.0;
-      w[j] = 0.0;
-      gwTea[j] = 0.0;
-      if (live) {
-        const double T = exp(-S[j]), ea = exp(-s[j]);
-        w[j] = T * (1.0 - ea);  // α = 1 - e^{-s}: fp64 absolute error ~1e-16
-        const double gw = gc[j][0] * col[3 * j] + gc[j][1] * col[3 * j + 1] + gc[j][2] * col[3 * j + 2] + gOp[j] +
-                          gN[j] * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-        v = gw * w[j];
-        gwTea[j] = gw * T * ea;
-      }
-      items[j].f = it.head[j];
-      items[j].v[0] = v;
-      agg = seg_combine(agg, items[j]);
-    }
-    Seg<1> run = block_seg_excl<1, kFlatWarps>(agg, carryP, smP);
-    float gs[4], gr[12];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      run = seg_combine(run, items[j]);
-      const bool live = it.valid[j] && !(S[j] > L);
-      const double Q = Rr[j] - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
-      gs[j] = live ? (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q)) : 0.f;
-      gr[3 * j] = (float)(w[j] * gc[j][0]);
-      gr[3 * j + 1] = (float)(w[j] * gc[j][1]);
-      gr[3 * j + 2] = (float)(w[j] * gc[j][2]);
-    }
-    if (kVec && it.valid[0] && it.valid[3]) {
-      *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
-      if (g_rgb) {
-        float4 *p = reinterpret_cast<float4 *>(g_rgb + 3 * it.q0);
-        p[0] = make_float4(gr[0], gr[1], gr[2], gr[3]);
-        p[1] = make_float4(gr[4], gr[5], gr[6], gr[7]);
-        p[2] = make_float4(gr[8], gr[9], gr[10], gr[11]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (!it.valid[j]) continue;
-        g_sigma[it.q0 + j] = gs[j];
-        if (g_rgb)
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) g_rgb[3 * (it.q0 + j) + ch] = gr[3 * j + ch];
-      }
-    }
-  }
-}
 
 // ------------------------------------------------------------------ warp-tile fused render
 // Each warp owns the rays whose first sample lies in its 256-sample tile and
@@ -570,6 +307,70 @@ __device__ __forceinline__ void warp_items_S(const Items &it, double s[4], doubl
   }
 }
 
+// Per-ray sums of the forward, all fp64: O and N (the backward's depth term
+// divides by O, so R - P must keep fp64 precision) and colour (an fp32 sum
+// over a 5000-sample ray misses the 1e-4 bar).  Same operator as Seg<K>.
+struct SegM {
+  int f;
+  double o, n;
+  double c0, c1, c2;
+};
+__device__ __forceinline__ SegM segm_identity() { return SegM{0, 0.0, 0.0, 0.0, 0.0, 0.0}; }
+__device__ __forceinline__ SegM segm_combine(const SegM &a, const SegM &b) {
+  SegM r;
+  r.f = a.f | b.f;
+  r.o = b.f ? b.o : a.o + b.o;
+  r.n = b.f ? b.n : a.n + b.n;
+  r.c0 = b.f ? b.c0 : a.c0 + b.c0;
+  r.c1 = b.f ? b.c1 : a.c1 + b.c1;
+  r.c2 = b.f ? b.c2 : a.c2 + b.c2;
+  return r;
+}
+__device__ __forceinline__ SegM segm_shfl_up(const SegM &x, int o) {
+  SegM y;
+  y.f = __shfl_up_sync(kFull, x.f, o);
+  y.o = __shfl_up_sync(kFull, x.o, o);
+  y.n = __shfl_up_sync(kFull, x.n, o);
+  y.c0 = __shfl_up_sync(kFull, x.c0, o);
+  y.c1 = __shfl_up_sync(kFull, x.c1, o);
+  y.c2 = __shfl_up_sync(kFull, x.c2, o);
+  return y;
+}
+__device__ __forceinline__ SegM segm_shfl(const SegM &x, int src) {
+  SegM y;
+  y.f = __shfl_sync(kFull, x.f, src);
+  y.o = __shfl_sync(kFull, x.o, src);
+  y.n = __shfl_sync(kFull, x.n, src);
+  y.c0 = __shfl_sync(kFull, x.c0, src);
+  y.c1 = __shfl_sync(kFull, x.c1, src);
+  y.c2 = __shfl_sync(kFull, x.c2, src);
+  return y;
+}
+__device__ __forceinline__ SegM warp_segm_excl(const SegM &x, SegM &carry) {
+  const int lane = threadIdx.x & 31;
+  SegM incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const SegM y = segm_shfl_up(incl, o);
+    if (lane >= o) incl = segm_combine(y, incl);
+  }
+  SegM ex = segm_shfl_up(incl, 1);
+  if (lane == 0) ex = segm_identity();
+  const SegM res = segm_combine(carry, ex);
+  carry = segm_combine(carry, segm_shfl(incl, 31));
+  return res;
+}
+__device__ __forceinline__ SegM segm_item(const Items &it, int j, double w, const float *col) {
+  SegM x;
+  x.f = it.head[j];
+  x.o = w;
+  x.n = w * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+  x.c0 = w * (double)col[3 * j];
+  x.c1 = w * (double)col[3 * j + 1];
+  x.c2 = w * (double)col[3 * j + 2];
+  return x;
+}
+
 template <bool kVec>
 __global__ void __launch_bounds__(256, 2) render_fwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
@@ -595,7 +396,7 @@ __global__ void __launch_bounds__(256, 2) render_fwd_warp_kernel(
   const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
   if (B >= E) return;
   Seg<1> carryS = seg_identity<1>();
-  Seg<5> carryC = seg_identity<5>();
+  SegM carryC = segm_identity();
   int32_t carry_rid = -1;
   for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
     Items it;
@@ -605,48 +406,32 @@ __global__ void __launch_bounds__(256, 2) render_fwd_warp_kernel(
     float col[12];
     load_rgb4(col, it, rgb, kVec);
     double w[4];
-    Seg<5> agg = seg_identity<5>();
+    SegM agg = segm_identity();
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const bool live = it.valid[j] && !(S[j] > L);
       w[j] = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
-      Seg<5> x;
-      x.f = it.head[j];
-      x.v[0] = w[j] * (double)col[3 * j];
-      x.v[1] = w[j] * (double)col[3 * j + 1];
-      x.v[2] = w[j] * (double)col[3 * j + 2];
-      x.v[3] = w[j];
-      x.v[4] = w[j] * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-      agg = seg_combine(agg, x);
+      agg = segm_combine(agg, segm_item(it, j, w[j], col));
     }
-    Seg<5> run = warp_seg_excl<5>(agg, carryC);
+    SegM run = warp_segm_excl(agg, carryC);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      Seg<5> x;
-      x.f = it.head[j];
-      x.v[0] = w[j] * (double)col[3 * j];
-      x.v[1] = w[j] * (double)col[3 * j + 1];
-      x.v[2] = w[j] * (double)col[3 * j + 2];
-      x.v[3] = w[j];
-      x.v[4] = w[j] * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-      run = seg_combine(run, x);
+      run = segm_combine(run, segm_item(it, j, w[j], col));
       if (it.tail[j]) {
         const int64_t r = it.rid[j];
         if (color) {
-          color[3 * r] = (float)run.v[0];
-          color[3 * r + 1] = (float)run.v[1];
-          color[3 * r + 2] = (float)run.v[2];
+          color[3 * r] = (float)run.c0;
+          color[3 * r + 1] = (float)run.c1;
+          color[3 * r + 2] = (float)run.c2;
         }
-        if (opacity) opacity[r] = (float)run.v[3];
-        if (depth) depth[r] = (float)(run.v[4] / fmax(run.v[3], 1e-10));
+        if (opacity) opacity[r] = (float)run.o;
+        if (depth) depth[r] = (float)(run.n / fmax(run.o, 1e-10));
         if (ctx) {
-          double2 *cx = reinterpret_cast<double2 *>(ctx + 5 * r);
-          ctx[5 * r] = run.v[0];
-          ctx[5 * r + 1] = run.v[1];
-          ctx[5 * r + 2] = run.v[2];
-          ctx[5 * r + 3] = run.v[3];
-          ctx[5 * r + 4] = run.v[4];
-          (void)cx;
+          ctx[5 * r] = run.c0;
+          ctx[5 * r + 1] = run.c1;
+          ctx[5 * r + 2] = run.c2;
+          ctx[5 * r + 3] = run.o;
+          ctx[5 * r + 4] = run.n;
         }
       }
     }

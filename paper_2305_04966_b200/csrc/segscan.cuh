@@ -1,9 +1,9 @@
-// segscan.cuh — block-wide segmented scans over packed samples (flat tiles).
+// segscan.cuh — warp-wide segmented scans over packed samples (ray-aligned tiles).
 //
 // A "segment" is one ray's run of consecutive samples in the packed tensor
-// (P:83).  Blocks own ray-aligned sample ranges, process them in chunks of
-// kThreads*kItems samples, and carry the open segment across chunks, so no
-// cross-block look-back is needed.  Values are fp64 (readings #9, #11).
+// (P:83).  Warps own ray-aligned sample ranges, process them in chunks of
+// 32 lanes x 4 samples, and carry the open segment across chunks, so no
+// cross-warp look-back is needed.  Values are fp64 (readings #9, #11).
 #pragma once
 #include "common.cuh"
 
@@ -52,33 +52,6 @@ __device__ __forceinline__ Seg<K> warp_seg_incl(Seg<K> x) {
     if (lane >= o) x = seg_combine(y, x);
   }
   return x;
-}
-
-// Exclusive block-wide segmented scan of one aggregate per thread, seeded with
-// `carry` (the open segment from the previous chunk).  Returns the thread's
-// exclusive prefix and advances `carry` to the chunk's inclusive total.
-// smem must hold kWarps + 1 elements.  Contains __syncthreads().
-template <int K, int kWarps>
-__device__ __forceinline__ Seg<K> block_seg_excl(const Seg<K> &x, Seg<K> &carry, Seg<K> *smem) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const Seg<K> incl = warp_seg_incl(x);
-  Seg<K> ex = seg_shfl_up(incl, 1);
-  if (lane == 0) ex = seg_identity<K>();
-  if (lane == 31) smem[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    Seg<K> w = lane < kWarps ? smem[lane] : seg_identity<K>();
-    const Seg<K> wi = warp_seg_incl(w);
-    Seg<K> we = seg_shfl_up(wi, 1);
-    if (lane == 0) we = seg_identity<K>();
-    if (lane < kWarps) smem[lane] = seg_combine(carry, we);
-    if (lane == kWarps - 1) smem[kWarps] = seg_combine(carry, wi);
-  }
-  __syncthreads();
-  const Seg<K> res = seg_combine(smem[warp], ex);
-  carry = smem[kWarps];
-  __syncthreads();
-  return res;
 }
 
 // Exclusive warp-wide segmented scan seeded with `carry` (the open segment of

@@ -64,9 +64,11 @@ class TextureField(LatticeField):
         self.handle = h.value
 
     def at_samples(self, rays_o, rays_d, t0, t1, ray_id, want_rgb=True, n_dev=None):
+        if want_rgb:  # the float4 lattice gather measured faster than the float4 texture fetch
+            return super().at_samples(rays_o, rays_d, t0, t1, ray_id, want_rgb=True, n_dev=n_dev)
         n = t0.numel()
         sigma = torch.empty(n, dtype=torch.float32, device=t0.device)
-        rgb = torch.empty((n, 3), dtype=torch.float32, device=t0.device) if want_rgb else None
+        rgb = None
         st = L.harness().naccx_tex_at_samples(self.handle, self.lo, self.hi, self.contracted, _ptr(rays_o),
                                               _ptr(rays_d), _ptr(t0), _ptr(t1), _ptr(ray_id), n, _ptr(n_dev),
                                               _ptr(sigma), _ptr(rgb), _stream())
