@@ -16,6 +16,7 @@ Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import math
 import os
@@ -47,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
     ap.add_argument("--eager", action="store_true", help="time the eager (non-graph) step")
+    ap.add_argument("--no-extras", action="store_true", help="skip the CFG3/CFG4 secondary measurements")
     return ap.parse_args()
 
 
@@ -66,13 +68,20 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+NCU_KERNELS_OF_STAGE = {"march": ["march_fused"], "render_fwd": ["render_fwd_warp"], "render_bwd": ["render_bwd_warp"],
+                        "filter": ["filter_cut", "filter_copy"], "field_sigma": ["tex_samples"]}
+
+
 def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f)
-    return {}
+    """dram read+write bytes per launch per stage, from the newest committed `ncu --set full` capture
+    (profiles/<round>/ncu_traffic_bytes.json, written by tools/make_profiles.py)."""
+    rounds = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic_bytes.json")))
+    if not rounds:
+        return {}
+    with open(rounds[-1]) as f:
+        by_kernel = json.load(f)
+    return {st: sum(by_kernel[k] for k in ks) for st, ks in NCU_KERNELS_OF_STAGE.items()
+            if all(k in by_kernel for k in ks)}
 
 
 # ----------------------------------------------------------------------------- clocks (NVML)
@@ -307,6 +316,87 @@ class Pipeline:
         self.k += 1
 
 
+def run_extras(device, reps=20):
+    """Secondary measurements of the other §8 rows (not the headline): the
+    CFG3 cascaded cone march (640k rays, 4 levels) and the CFG4 proposal path
+    (2^16 rays, 256 -> 96 -> 48 inverse-CDF resampling, then a 48-sample render
+    fwd+bwd).  Device time per call with CUDA events, inputs resident."""
+    import torch
+
+    import workloads as W
+    import paper_2305_04966_b200 as N
+    from paper_2305_04966_b200 import harness as H
+
+    def timed(fn, n=reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / n, out
+
+    out = {}
+    peak, _ = measured_peaks()
+    # ---- CFG3: cascaded grid + cone steps
+    c = W.cfg3()
+    spec = N.GridSpec(roi=c.roi, res=c.res, levels=c.levels)
+    bits = N.prepare_bits(spec, torch.from_numpy(W.pack_bits(c.occ).view(np.int32)).to(device))
+    o, d = torch.from_numpy(c.rays_o).to(device), torch.from_numpy(c.rays_d).to(device)
+    prm = N.MarchParams(step=c.step, near_plane=c.near, cone_angle=c.cone_angle, max_step=c.max_step)
+    n3 = N.sampling_occgrid(o, d, spec, bits, prm).n_samples
+    cap = int(n3 * 1.1) + 1024
+    ms3, s3 = timed(lambda: N.sampling_occgrid(o, d, spec, bits, prm, capacity=cap, sync=False))
+    byts = len(c.rays_o) * 40 + n3 * 12
+    out["cfg3_march"] = {"rays": len(c.rays_o), "samples": n3, "ms": ms3, "samples_per_s": n3 / (ms3 / 1e3),
+                         "GBps": byts / (ms3 / 1e3) / 1e9, "frac_of_peak": byts / (ms3 / 1e3) / 1e9 / peak}
+    # ---- CFG4: proposal resampling 256 -> 96 -> 48 + 48-sample render fwd/bwd
+    pc = W.cfg4()
+    lat = H.LatticeField(torch.from_numpy(pc.scene.data.reshape(-1, 4)).to(device), pc.scene.lo, pc.scene.hi,
+                         contracted=True)
+    n4 = len(pc.rays_o)
+    o4, d4 = torch.from_numpy(pc.rays_o).to(device), torch.from_numpy(pc.rays_d).to(device)
+    e0 = torch.from_numpy(pc.s_edges).to(device)
+
+    def lindisp(sv):
+        return 1.0 / ((1.0 - sv) / pc.t_near + sv / pc.t_far)
+
+    def field_dense(s_edges):  # caller's proposal-field query at the interval midpoints (harness)
+        t = lindisp(s_edges)
+        m = s_edges.shape[1] - 1
+        rid = torch.arange(n4, device=device, dtype=torch.int32).repeat_interleave(m)
+        sig, _ = lat.at_samples(o4, d4, t[:, :-1].contiguous().view(-1), t[:, 1:].contiguous().view(-1), rid,
+                                want_rgb=False)
+        return sig.view(n4, m)
+
+    sig1 = field_dense(e0)
+    ms_a, (s1, _) = timed(lambda: N.importance_sample(e0, 96, sigma=sig1, map_kind=N.MAP_LINDISP, t_near=pc.t_near,
+                                                      t_far=pc.t_far))
+    sig2 = field_dense(s1)
+    ms_b, (s2, t2) = timed(lambda: N.importance_sample(s1, 48, sigma=sig2, map_kind=N.MAP_LINDISP, t_near=pc.t_near,
+                                                       t_far=pc.t_far))
+    t0 = t2[:, :-1].contiguous().view(-1)
+    t1 = t2[:, 1:].contiguous().view(-1)
+    rid = torch.arange(n4, device=device, dtype=torch.int32).repeat_interleave(48)
+    pk = torch.stack([torch.arange(n4, device=device, dtype=torch.int64) * 48,
+                      torch.full((n4,), 48, device=device, dtype=torch.int64)], 1).contiguous()
+    samples = N.PackedSamples(pk, t0, t1, rid)
+    sg, rgb = lat.at_samples(o4, d4, t0, t1, rid)
+    ms_f, (col, opa, dep, cx) = timed(lambda: N.render_fwd(samples, sg, rgb, EPS))
+    gcol = torch.randn_like(col)
+    ms_r, _ = timed(lambda: N.render_bwd(samples, sg, rgb, cx, gcol, None, None, EPS))
+    b_a = n4 * (4 * 257 + 4 * 256 + 8 * 97)
+    b_b = n4 * (4 * 97 + 4 * 96 + 8 * 49)
+    out["cfg4_proposal"] = {"rays": n4, "resample_256_96_ms": ms_a, "resample_96_48_ms": ms_b,
+                            "resample_GBps": (b_a + b_b) / ((ms_a + ms_b) / 1e3) / 1e9,
+                            "render_fwd_ms": ms_f, "render_bwd_ms": ms_r,
+                            "rendered_samples_per_s": n4 * 48 / ((ms_f + ms_r) / 1e3),
+                            "rays_per_s": n4 / ((ms_a + ms_b + ms_f + ms_r) / 1e3)}
+    return out
+
+
 def algorithmic_bytes(stage, pre, post, rays):
     """SURVEY §8(d).4 / DESIGN.md §6: bytes the method must move, per launch."""
     if stage == "march":
@@ -406,10 +496,10 @@ def run_nacc(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=device)
     import paper_2305_04966_b200 as N
     from paper_2305_04966_b200 import harness as H
 
@@ -524,6 +614,12 @@ def run_nacc(args):
         cpu = None
         if not args.no_cpu_baseline and not args.profile and world == 1:
             cpu = cpu_baseline()
+        extras = None
+        if not args.profile and not args.no_extras:
+            try:
+                extras = run_extras(device)
+            except Exception as exc:  # secondary lines never sink the headline
+                extras = {"error": repr(exc)}
         clocks = clk.summary()
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
                 "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -535,7 +631,7 @@ def run_nacc(args):
                 "execution": "cuda-graph per stage, device-count API (no host syncs)" if use_graph else "eager",
                 "samples_pre_filter_per_step_per_gpu": pre_pg, "samples_post_filter_per_step_per_gpu": post_pg,
                 "pre_filter_samples_per_s": pre_all / (ms_max / 1e3), "rays_per_s": rays_all / (ms_max / 1e3),
-                "stage_ms": stages,
+                "stage_ms": stages, "extras": extras,
                 "library_ms_per_step": sum(v for k, v in stages.items() if algorithmic_bytes(k, 1, 1, 1) is not None)
                 if stages else None}
         print(json.dumps(line), flush=True)

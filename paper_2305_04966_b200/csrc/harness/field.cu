@@ -361,6 +361,54 @@ __global__ void tex_samples_kernel(cudaTextureObject_t tex, int R, float lo, flo
   }
 }
 
+// density only, 4 consecutive samples per thread (vector loads/stores, four
+// independent texture fetches in flight)
+__global__ void tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, float hi, int contracted,
+                                  const float *__restrict__ o, const float *__restrict__ d,
+                                  const float *__restrict__ t0, const float *__restrict__ t1,
+                                  const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
+                                  float *__restrict__ sigma) {
+  const int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  const int64_t nn = n_dev ? min(n, *n_dev) : n;
+  if (q0 >= nn) return;
+  const float sc = (float)R / (hi - lo);
+  float a[4], b[4], out[4];
+  int32_t ri[4];
+  const bool full = q0 + 3 < nn;
+  if (full) {
+    const float4 A = __ldg(reinterpret_cast<const float4 *>(t0 + q0));
+    const float4 Bv = __ldg(reinterpret_cast<const float4 *>(t1 + q0));
+    const int4 Ri = __ldg(reinterpret_cast<const int4 *>(rid + q0));
+    a[0] = A.x; a[1] = A.y; a[2] = A.z; a[3] = A.w;
+    b[0] = Bv.x; b[1] = Bv.y; b[2] = Bv.z; b[3] = Bv.w;
+    ri[0] = Ri.x; ri[1] = Ri.y; ri[2] = Ri.z; ri[3] = Ri.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool in = q0 + j < nn;
+      a[j] = in ? __ldg(t0 + q0 + j) : 0.f;
+      b[j] = in ? __ldg(t1 + q0 + j) : 0.f;
+      ri[j] = in ? __ldg(rid + q0 + j) : 0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t r = ri[j];
+    const float m = 0.5f * (a[j] + b[j]);
+    float x = __ldg(o + 3 * r) + m * __ldg(d + 3 * r);
+    float y = __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1);
+    float z = __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2);
+    const bool in = tex_coord(lo, hi, sc, contracted, x, y, z);
+    out[j] = in ? tex3D<float>(tex, x, y, z) : 0.f;
+  }
+  if (full) {
+    *reinterpret_cast<float4 *>(sigma + q0) = make_float4(out[0], out[1], out[2], out[3]);
+  } else {
+    for (int j = 0; j < 4; ++j)
+      if (q0 + j < nn) sigma[q0 + j] = out[j];
+  }
+}
+
 extern "C" nacc_status naccx_tex_at_samples(uint64_t handle, float lo, float hi, int32_t contracted, const float *rays_o,
                                  const float *rays_d, const float *t0, const float *t1, const int32_t *ray_id,
                                  int64_t n, const int64_t *n_dev, float *sigma, float *rgb, cudaStream_t stream) {
@@ -370,6 +418,10 @@ extern "C" nacc_status naccx_tex_at_samples(uint64_t handle, float lo, float hi,
   if (rgb)
     tex_samples_kernel<true><<<blocks_for(n), 256, 0, stream>>>(f->t_rgba, f->res, lo, hi, contracted, rays_o, rays_d,
                                                                 t0, t1, ray_id, n, n_dev, sigma, rgb);
+  else if (((reinterpret_cast<uintptr_t>(t0) | reinterpret_cast<uintptr_t>(t1) | reinterpret_cast<uintptr_t>(ray_id) |
+              reinterpret_cast<uintptr_t>(sigma)) & 15) == 0)
+    tex_sigma4_kernel<<<blocks_for((n + 3) / 4), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
+                                                                    t0, t1, ray_id, n, n_dev, sigma);
   else
     tex_samples_kernel<false><<<blocks_for(n), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
                                                                  t0, t1, ray_id, n, n_dev, sigma, nullptr);
