@@ -117,7 +117,8 @@ size_t nacc_sampling_occgrid_workspace_bytes(const nacc_grid *grid, const nacc_m
  *                 (shared anchor), else NACC_ERR_UNSUPPORTED
  *   packed_info   [n_rays][2] int64 out, always written
  *   total         device int64 out: Σ counts, always written
- *   t0,t1,ray_id  [capacity] out; written only if total <= capacity, else the
+ *   t0,t1,ray_id  [capacity] out; complete iff total <= capacity (never written
+ *                 past capacity; unspecified otherwise), else the
  *                 device int32 *status_out (NULL allowed) is set to
  *                 NACC_ERR_INSUFFICIENT_CAPACITY (else NACC_OK) and the caller
  *                 re-allocates and calls nacc_sampling_occgrid_fill.

@@ -14,23 +14,27 @@ struct LookbackWs {
   unsigned long long status[1];  // [n_tiles]: (value << 2) | flag, flag 1 = aggregate, 2 = inclusive prefix
 };
 
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+// The flag and the value share one 64-bit word and nothing else is read on the
+// strength of the flag, so relaxed (strong, gpu-scope) accesses suffice; an
+// acquire load would add an L1 invalidation (CCTL.IVALL) per spin iteration,
+// evicting the occupancy bits the march keeps in L1.
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
   unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// warp 0: publish this tile's aggregate and return its exclusive prefix
+// one warp: publish this tile's aggregate and return its exclusive prefix
 __device__ __forceinline__ long long lookback(unsigned long long *st, int64_t tile, long long agg) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
-    if (lane == 0) st_release(st, ((unsigned long long)agg << 2) | 2ull);
+    if (lane == 0) st_relaxed(st, ((unsigned long long)agg << 2) | 2ull);
     return 0;
   }
-  if (lane == 0) st_release(st + tile, ((unsigned long long)agg << 2) | 1ull);
+  if (lane == 0) st_relaxed(st + tile, ((unsigned long long)agg << 2) | 1ull);
   long long excl = 0;
   int64_t j = tile - 1;  // lanes look at tiles j, j-1, ..., j-31
   for (;;) {
@@ -38,7 +42,7 @@ __device__ __forceinline__ long long lookback(unsigned long long *st, int64_t ti
     unsigned long long w = idx >= 0 ? 0ull : 2ull;  // before tile 0: an inclusive prefix of 0
     if (idx >= 0) {
       do {
-        w = ld_acquire(st + idx);
+        w = ld_relaxed(st + idx);
       } while ((w & 3ull) == 0ull);
     }
     const unsigned m2 = __ballot_sync(kFull, (w & 3ull) == 2ull);
@@ -50,7 +54,7 @@ __device__ __forceinline__ long long lookback(unsigned long long *st, int64_t ti
     if (m2) break;
     j -= 32;
   }
-  if (lane == 0) st_release(st + tile, ((unsigned long long)(excl + agg) << 2) | 2ull);
+  if (lane == 0) st_relaxed(st + tile, ((unsigned long long)(excl + agg) << 2) | 2ull);
   return excl;
 }
 

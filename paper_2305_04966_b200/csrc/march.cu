@@ -367,14 +367,16 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 }
 
 // ---------------------------------------------------------------- fused single-pass march
-// Tile = 4 warps x 4 rays.  Phase 1 traverses the tile's rays once, keeping
-// each ray's emitted lattice indices (as 16-bit offsets from the ray's first
-// candidate index) in the warp's shared k-list; the tile's count is published
-// and its output offset found by a warp-wide decoupled look-back over the
-// preceding tiles; phase 2 writes packed_info and, when the total fits the
-// capacity, the samples from the k-lists with coalesced stores.  A ray whose
-// k-list overflowed is traversed again in phase 2, writing directly.
-constexpr int kFWarps = 4, kFRaysPerWarp = 4, kFTileRays = kFWarps * kFRaysPerWarp, kFKCap = 2048;
+// Tile = one warp x kFRaysPerWarp rays (no block-level barrier, so a warp that
+// drew short rays never waits for a sibling).  Phase 1 traverses the tile's
+// rays once, keeping each ray's emitted lattice indices (16-bit offsets from
+// the ray's first candidate index) in the warp's shared k-list; the tile's
+// count is published and its output offset found by a warp-wide decoupled
+// look-back over the preceding tiles; phase 2 writes packed_info and, when the
+// total fits the capacity, the samples from the k-lists with coalesced stores.
+// A ray whose k-list overflowed is traversed again in phase 2, writing directly.
+constexpr int kFWarps = 4, kFRaysPerWarp = 8, kFKCap = 2048;
+static_assert(kFRaysPerWarp <= 32, "one lane holds one ray's metadata");
 
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(kFWarps * 32) march_fused_kernel(
@@ -386,106 +388,100 @@ __global__ void __launch_bounds__(kFWarps * 32) march_fused_kernel(
     float *__restrict__ t1, int32_t *__restrict__ ray_id) {
   __shared__ uint16_t kbuf[kFWarps][kFKCap];
   __shared__ int seglist[kFWarps][32];
-  __shared__ int32_t s_cnt[kFTileRays];
-  __shared__ int32_t s_kb[kFTileRays];
-  __shared__ int32_t s_lpos[kFTileRays];  // start of the ray's k-list in kbuf[warp], -1 if unusable
-  __shared__ float s_near[kFTileRays];
-  __shared__ unsigned int s_tile;
-  __shared__ long long s_prefix;
+  __shared__ RaySetup s_setup[kFWarps][kFRaysPerWarp];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(&lb->tile_counter, 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
-  const int64_t r_base = tile * kFTileRays;
-  // ---- phase 1: traverse, keep k-lists
+  unsigned int tile32 = 0;
+  if (lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
+  const int64_t tile = __shfl_sync(kFull, tile32, 0);
+  if (tile >= n_tiles) return;  // whole warp
+  const int64_t r_base = tile * kFRaysPerWarp;
+  // lane j < kFRaysPerWarp sets up ray r_base + j; the warp then walks the rays in order
+  const int64_t my_r = r_base + lane;
+  if (lane < kFRaysPerWarp && my_r < n_rays) s_setup[warp][lane] = ray_setup(g, p, rays_o, rays_d, t_min, t_max, my_r);
+  __syncwarp();
+  // ---- phase 1: traverse, keep k-lists; lane j keeps ray j's count, first index and list position
+  int32_t my_c = 0, my_kb = 0, my_lpos = -1;
   int pos = 0;  // warp-uniform fill level of kbuf[warp]; kFKCap + 1 once it overflowed
 #pragma unroll 1
   for (int j = 0; j < kFRaysPerWarp; ++j) {
-    const int slot = warp * kFRaysPerWarp + j;
-    const int64_t r = r_base + slot;
-    int32_t c = 0;
-    int kb = 0, lpos = -1;
-    if (r < n_rays) {
-      const RaySetup s = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r);
-      const int start = pos;
-      int kb0 = 0, ke0 = 0;
-      c = traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
-                                           [&](unsigned b, bool pred, int k, int32_t cnt) {
-                                             const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
-                                             const int off = k - kb0;
-                                             if (pred && q < kFKCap && off < 65536) kbuf[warp][q] = (uint16_t)off;
-                                           });
-      kb = kb0;
-      if (lane == 0) s_near[slot] = s.near_r;
-      // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
-      const bool usable = start + c <= kFKCap && ke0 - kb0 <= 65536;
-      lpos = usable ? start : -1;
-      pos = usable ? start + c : kFKCap + 1;
-    }
-    if (lane == 0) {
-      s_cnt[slot] = c;
-      s_kb[slot] = kb;
-      s_lpos[slot] = lpos;
+    const int64_t r = r_base + j;
+    if (r >= n_rays) break;
+    const RaySetup s = s_setup[warp][j];
+    const int start = pos;
+    int kb0 = 0, ke0 = 0;
+    const int32_t c = traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+                                                      [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                                        const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
+                                                        const int off = k - kb0;
+                                                        if (pred && q < kFKCap && off < 65536)
+                                                          kbuf[warp][q] = (uint16_t)off;
+                                                      });
+    // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
+    const bool usable = start + c <= kFKCap && ke0 - kb0 <= 65536;
+    pos = usable ? start + c : kFKCap + 1;
+    if (lane == j) {
+      my_c = c;
+      my_kb = kb0;
+      my_lpos = usable ? start : -1;
     }
   }
-  __syncthreads();
-  if (warp == 0) {
-    const long long agg = warp_sum_i64(lane < kFTileRays ? (int64_t)s_cnt[lane] : 0);
-    const long long excl = lookback(lb->status, tile, agg);
-    if (lane == 0) {
-      s_prefix = excl;
-      if (tile == n_tiles - 1) {
-        *total = excl + agg;
-        if (status_out) {
-          int32_t stt = (excl + agg > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
-          if (hdr && hdr->overflow) stt = NACC_ERR_UNSUPPORTED;
-          *status_out = stt;
-        }
-      }
+  // ---- tile prefix
+  int32_t incl = my_c;  // inclusive scan of the tile's ray counts over lanes
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const long long agg = __shfl_sync(kFull, incl, 31);
+  const long long excl = lookback(lb->status, tile, agg);
+  if (tile == n_tiles - 1 && lane == 0) {
+    *total = excl + agg;
+    if (status_out) {
+      int32_t stt = (excl + agg > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
+      if (hdr && hdr->overflow) stt = NACC_ERR_UNSUPPORTED;
+      *status_out = stt;
     }
   }
-  __syncthreads();
-  // ---- phase 2: packed_info and samples (each warp handles its own rays)
-  int64_t run = s_prefix;
-  for (int slot = 0; slot < warp * kFRaysPerWarp; ++slot) run += s_cnt[slot];
+  const int64_t my_run = excl + incl - my_c;
+  if (lane < kFRaysPerWarp && my_r < n_rays)
+    reinterpret_cast<longlong2 *>(packed_info)[my_r] = make_longlong2(my_run, my_c);
+  if (t0 == nullptr || excl + agg > capacity) return;
+  __syncwarp();
+  // ---- phase 2: samples (the warp writes its rays in order)
 #pragma unroll 1
   for (int j = 0; j < kFRaysPerWarp; ++j) {
-    const int slot = warp * kFRaysPerWarp + j;
-    const int64_t r = r_base + slot;
+    const int64_t r = r_base + j;
     if (r >= n_rays) break;
-    const int32_t c = s_cnt[slot];
-    if (lane == 0) reinterpret_cast<longlong2 *>(packed_info)[r] = make_longlong2(run, c);
-    if (t0 != nullptr && run + c <= capacity && c > 0) {
-      const int lpos = s_lpos[slot];
-      if (lpos >= 0) {
-        const int kb = s_kb[slot];
-        const float nr = s_near[slot];
-        for (int i = lane; i < c; i += 32) {
-          const int k = kb + (int)kbuf[warp][lpos + i];
-          float ta, tb;
-          lattice_ends<kCone>(p, nr, tab, k, ta, tb);
-          t0[run + i] = ta;
-          t1[run + i] = tb;
-          ray_id[run + i] = (int32_t)r;
-        }
-      } else {  // k-list overflowed: traverse again, writing directly
-        const RaySetup s = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r);
-        const int64_t base = run;
-        int kb0, ke0;
-        traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
-                                        [&](unsigned b, bool pred, int k, int32_t cnt) {
-                                          if (pred) {
-                                            const int64_t q = base + cnt + __popc(b & ((1u << lane) - 1u));
-                                            float ta, tb;
-                                            lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb);
-                                            t0[q] = ta;
-                                            t1[q] = tb;
-                                            ray_id[q] = (int32_t)r;
-                                          }
-                                        });
+    const int32_t c = __shfl_sync(kFull, my_c, j);
+    if (c == 0) continue;
+    const int64_t run = __shfl_sync(kFull, my_run, j);
+    const int lpos = __shfl_sync(kFull, my_lpos, j);
+    const float nr = s_setup[warp][j].near_r;
+    if (lpos >= 0) {
+      const int kb = __shfl_sync(kFull, my_kb, j);
+      for (int i = lane; i < c; i += 32) {
+        const int k = kb + (int)kbuf[warp][lpos + i];
+        float ta, tb;
+        lattice_ends<kCone>(p, nr, tab, k, ta, tb);
+        t0[run + i] = ta;
+        t1[run + i] = tb;
+        ray_id[run + i] = (int32_t)r;
       }
+    } else {  // k-list overflowed: traverse again, writing directly
+      const RaySetup s = s_setup[warp][j];
+      int kb0, ke0;
+      traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+                                      [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                        if (pred) {
+                                          const int64_t q = run + cnt + __popc(b & ((1u << lane) - 1u));
+                                          float ta, tb;
+                                          lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb);
+                                          t0[q] = ta;
+                                          t1[q] = tb;
+                                          ray_id[q] = (int32_t)r;
+                                        }
+                                      });
     }
-    run += c;
   }
 }
 
@@ -529,7 +525,7 @@ struct MarchWs {
   float *tab;
 };
 
-static int64_t fused_tiles(int64_t n) { return ceil_div(n, kFTileRays); }
+static int64_t fused_tiles(int64_t n) { return ceil_div(n, kFRaysPerWarp); }
 
 static size_t march_ws_layout(const nacc_grid &g, const nacc_march &p, int64_t n, MarchWs *w, void *base) {
   size_t off = 0;
@@ -631,7 +627,7 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
   if (!fill) {
     const int64_t n_tiles = fused_tiles(n_rays);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
-    NACC_DISPATCH3(march_fused_kernel, (unsigned)n_tiles, kFWarps * 32, stream, g, p, bits, mask2, M, rays_o,
+    NACC_DISPATCH3(march_fused_kernel, (unsigned)ceil_div(n_tiles, kFWarps), kFWarps * 32, stream, g, p, bits, mask2, M, rays_o,
                    rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,
                    status_out, t0, t1, ray_id);
   } else {
