@@ -27,23 +27,29 @@ __device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long 
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// one warp: publish this tile's aggregate and return its exclusive prefix
-__device__ __forceinline__ long long lookback(unsigned long long *st, int64_t tile, long long agg) {
+// one warp: publish this tile's aggregate (tile 0 publishes its inclusive prefix)
+__device__ __forceinline__ void lookback_publish(unsigned long long *st, int64_t tile, long long agg) {
+  if ((threadIdx.x & 31) == 0) st_relaxed(st + tile, ((unsigned long long)agg << 2) | (tile == 0 ? 2ull : 1ull));
+}
+
+// one warp: after lookback_publish(tile, agg), walk back over the predecessors
+// (32 at a time) to this tile's exclusive prefix, publish the inclusive one
+// and return the exclusive one.  Predecessors publish their aggregates without
+// waiting on anything, so the walk always terminates.
+__device__ __forceinline__ long long lookback_resolve(unsigned long long *st, int64_t tile, long long agg) {
   const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) st_relaxed(st, ((unsigned long long)agg << 2) | 2ull);
-    return 0;
-  }
-  if (lane == 0) st_relaxed(st + tile, ((unsigned long long)agg << 2) | 1ull);
+  if (tile == 0) return 0;
   long long excl = 0;
   int64_t j = tile - 1;  // lanes look at tiles j, j-1, ..., j-31
   for (;;) {
     const int64_t idx = j - lane;
     unsigned long long w = idx >= 0 ? 0ull : 2ull;  // before tile 0: an inclusive prefix of 0
     if (idx >= 0) {
-      do {
+      w = ld_relaxed(st + idx);
+      while ((w & 3ull) == 0ull) {
+        __nanosleep(100);
         w = ld_relaxed(st + idx);
-      } while ((w & 3ull) == 0ull);
+      }
     }
     const unsigned m2 = __ballot_sync(kFull, (w & 3ull) == 2ull);
     const int last = m2 ? __ffs(m2) - 1 : 31;  // nearest predecessor with an inclusive prefix

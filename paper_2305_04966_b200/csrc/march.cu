@@ -339,11 +339,10 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
       __syncwarp();
       nseg = __popc(F);
     }
-    for (int first = 0; first < nseg; first += 4) {
-      int k;
+    // lane (lane & 7) of segment list entry idx: its point k and P(k)
+    auto eval = [&](int idx, int &k) -> bool {
       bool interior = false;
       if (kSkip) {
-        const int idx = first + (lane >> 3);
         const int e = idx < nseg ? seglist[idx] : 0;
         k = idx < nseg ? k0 + (e & 0xff) * kSeg + (lane & 7) : ke;
         interior = kL1 && (e & 0x100);
@@ -357,9 +356,25 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
           pred = interior ? occupied_interior(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz)
                           : occupied<kL1>(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz);
       }
-      const unsigned b = __ballot_sync(kFull, pred);
-      emit(b, pred, k, cnt);
-      cnt += __popc(b);
+      return pred;
+    };
+    // two passes of 4 segments per iteration (independent chains for ILP), emitted in k order
+    for (int first = 0; first < nseg; first += (kSkip ? 8 : 32)) {
+      int ka, kb2;
+      const bool pa = eval(first + (lane >> 3), ka);
+      if (kSkip && first + 4 < nseg) {
+        const bool pb = eval(first + 4 + (lane >> 3), kb2);
+        const unsigned ba = __ballot_sync(kFull, pa);
+        emit(ba, pa, ka, cnt);
+        cnt += __popc(ba);
+        const unsigned bb = __ballot_sync(kFull, pb);
+        emit(bb, pb, kb2, cnt);
+        cnt += __popc(bb);
+      } else {
+        const unsigned ba = __ballot_sync(kFull, pa);
+        emit(ba, pa, ka, cnt);
+        cnt += __popc(ba);
+      }
     }
     if (kSkip) __syncwarp();
   }
@@ -367,121 +382,150 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 }
 
 // ---------------------------------------------------------------- fused single-pass march
-// Tile = one warp x kFRaysPerWarp rays (no block-level barrier, so a warp that
-// drew short rays never waits for a sibling).  Phase 1 traverses the tile's
-// rays once, keeping each ray's emitted lattice indices (16-bit offsets from
-// the ray's first candidate index) in the warp's shared k-list; the tile's
-// count is published and its output offset found by a warp-wide decoupled
-// look-back over the preceding tiles; phase 2 writes packed_info and, when the
-// total fits the capacity, the samples from the k-lists with coalesced stores.
-// A ray whose k-list overflowed is traversed again in phase 2, writing directly.
-constexpr int kFWarps = 4, kFRaysPerWarp = 8, kFKCap = 2048;
+// Persistent warps; tile = kFRaysPerWarp consecutive rays, handed out by an
+// atomic counter.  Each warp software-pipelines its tiles: phase 1 of tile t
+// traverses the rays once, keeping each ray's emitted lattice indices (16-bit
+// offsets from the ray's first candidate index) in one of the warp's two
+// shared k-list buffers, and publishes the tile's count; then the warp
+// resolves the output offset of its PREVIOUS tile by a warp-wide decoupled
+// look-back (its predecessors have had a whole tile's time to publish, so the
+// warp rarely waits) and writes that tile's packed_info and samples from the
+// other buffer with coalesced stores.  A ray whose k-list overflowed is
+// traversed again when its tile is written.
+constexpr int kFWarps = 4, kFRaysPerWarp = 8, kFKCap = 1024;
 static_assert(kFRaysPerWarp <= 32, "one lane holds one ray's metadata");
 
+struct FusedTile {  // per-lane metadata of a tile in flight (lane j: ray j)
+  int64_t tile;
+  int32_t c, kb, lpos;
+  long long incl, agg;
+};
+
 template <bool kCone, bool kSkip, bool kL1>
-__global__ void __launch_bounds__(kFWarps * 32) march_fused_kernel(
+__global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
     const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
     const float *__restrict__ t_max, int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr,
     const float *__restrict__ tab, LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info,
     int64_t *__restrict__ total, int64_t capacity, int32_t *__restrict__ status_out, float *__restrict__ t0,
     float *__restrict__ t1, int32_t *__restrict__ ray_id) {
-  __shared__ uint16_t kbuf[kFWarps][kFKCap];
+  __shared__ uint16_t kbuf[kFWarps][2][kFKCap];
   __shared__ int seglist[kFWarps][32];
-  __shared__ RaySetup s_setup[kFWarps][kFRaysPerWarp];
+  __shared__ RaySetup s_setup[kFWarps][2][kFRaysPerWarp];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned int tile32 = 0;
-  if (lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
-  const int64_t tile = __shfl_sync(kFull, tile32, 0);
-  if (tile >= n_tiles) return;  // whole warp
-  const int64_t r_base = tile * kFRaysPerWarp;
-  // lane j < kFRaysPerWarp sets up ray r_base + j; the warp then walks the rays in order
-  const int64_t my_r = r_base + lane;
-  if (lane < kFRaysPerWarp && my_r < n_rays) s_setup[warp][lane] = ray_setup(g, p, rays_o, rays_d, t_min, t_max, my_r);
-  __syncwarp();
-  // ---- phase 1: traverse, keep k-lists; lane j keeps ray j's count, first index and list position
-  int32_t my_c = 0, my_kb = 0, my_lpos = -1;
-  int pos = 0;  // warp-uniform fill level of kbuf[warp]; kFKCap + 1 once it overflowed
+  FusedTile prev;
+  prev.tile = -1;
+  int buf = 0;
 #pragma unroll 1
-  for (int j = 0; j < kFRaysPerWarp; ++j) {
-    const int64_t r = r_base + j;
-    if (r >= n_rays) break;
-    const RaySetup s = s_setup[warp][j];
-    const int start = pos;
-    int kb0 = 0, ke0 = 0;
-    const int32_t c = traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
-                                                      [&](unsigned b, bool pred, int k, int32_t cnt) {
-                                                        const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
-                                                        const int off = k - kb0;
-                                                        if (pred && q < kFKCap && off < 65536)
-                                                          kbuf[warp][q] = (uint16_t)off;
-                                                      });
-    // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
-    const bool usable = start + c <= kFKCap && ke0 - kb0 <= 65536;
-    pos = usable ? start + c : kFKCap + 1;
-    if (lane == j) {
-      my_c = c;
-      my_kb = kb0;
-      my_lpos = usable ? start : -1;
-    }
-  }
-  // ---- tile prefix
-  int32_t incl = my_c;  // inclusive scan of the tile's ray counts over lanes
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int32_t v = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const long long agg = __shfl_sync(kFull, incl, 31);
-  const long long excl = lookback(lb->status, tile, agg);
-  if (tile == n_tiles - 1 && lane == 0) {
-    *total = excl + agg;
-    if (status_out) {
-      int32_t stt = (excl + agg > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
-      if (hdr && hdr->overflow) stt = NACC_ERR_UNSUPPORTED;
-      *status_out = stt;
-    }
-  }
-  const int64_t my_run = excl + incl - my_c;
-  if (lane < kFRaysPerWarp && my_r < n_rays)
-    reinterpret_cast<longlong2 *>(packed_info)[my_r] = make_longlong2(my_run, my_c);
-  if (t0 == nullptr || excl + agg > capacity) return;
-  __syncwarp();
-  // ---- phase 2: samples (the warp writes its rays in order)
+  for (;;) {
+    unsigned int tile32 = 0;
+    if (lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
+    const int64_t tile = __shfl_sync(kFull, tile32, 0);
+    FusedTile cur;
+    cur.tile = tile < n_tiles ? tile : -1;
+    if (cur.tile >= 0) {
+      // ---- phase 1 of `tile`: lane j < kFRaysPerWarp sets up ray r_base + j, the warp walks the rays in order
+      const int64_t r_base = tile * kFRaysPerWarp;
+      if (lane < kFRaysPerWarp && r_base + lane < n_rays)
+        s_setup[warp][buf][lane] = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r_base + lane);
+      __syncwarp();
+      cur.c = 0;
+      cur.kb = 0;
+      cur.lpos = -1;
+      int pos = 0;  // warp-uniform fill level of the k-list; kFKCap + 1 once it overflowed
+      uint16_t *kl = kbuf[warp][buf];
 #pragma unroll 1
-  for (int j = 0; j < kFRaysPerWarp; ++j) {
-    const int64_t r = r_base + j;
-    if (r >= n_rays) break;
-    const int32_t c = __shfl_sync(kFull, my_c, j);
-    if (c == 0) continue;
-    const int64_t run = __shfl_sync(kFull, my_run, j);
-    const int lpos = __shfl_sync(kFull, my_lpos, j);
-    const float nr = s_setup[warp][j].near_r;
-    if (lpos >= 0) {
-      const int kb = __shfl_sync(kFull, my_kb, j);
-      for (int i = lane; i < c; i += 32) {
-        const int k = kb + (int)kbuf[warp][lpos + i];
-        float ta, tb;
-        lattice_ends<kCone>(p, nr, tab, k, ta, tb);
-        t0[run + i] = ta;
-        t1[run + i] = tb;
-        ray_id[run + i] = (int32_t)r;
+      for (int j = 0; j < kFRaysPerWarp; ++j) {
+        if (r_base + j >= n_rays) break;
+        const RaySetup s = s_setup[warp][buf][j];
+        const int start = pos;
+        int kb0 = 0, ke0 = 0;
+        const int32_t c =
+            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+                                             [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                               const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
+                                               const int off = k - kb0;
+                                               if (pred && q < kFKCap && off < 65536) kl[q] = (uint16_t)off;
+                                             });
+        // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
+        const bool usable = start + c <= kFKCap && ke0 - kb0 <= 65536;
+        pos = usable ? start + c : kFKCap + 1;
+        if (lane == j) {
+          cur.c = c;
+          cur.kb = kb0;
+          cur.lpos = usable ? start : -1;
+        }
       }
-    } else {  // k-list overflowed: traverse again, writing directly
-      const RaySetup s = s_setup[warp][j];
-      int kb0, ke0;
-      traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
-                                      [&](unsigned b, bool pred, int k, int32_t cnt) {
-                                        if (pred) {
-                                          const int64_t q = run + cnt + __popc(b & ((1u << lane) - 1u));
-                                          float ta, tb;
-                                          lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb);
-                                          t0[q] = ta;
-                                          t1[q] = tb;
-                                          ray_id[q] = (int32_t)r;
-                                        }
-                                      });
+      long long incl = cur.c;  // inclusive scan of the tile's ray counts over lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += v;
+      }
+      cur.incl = incl;
+      cur.agg = __shfl_sync(kFull, incl, 31);
+      lookback_publish(lb->status, tile, cur.agg);
     }
+    if (prev.tile >= 0) {
+      // ---- phase 2 of the previous tile (buffer buf ^ 1)
+      const int pb = buf ^ 1;
+      const int64_t ptile = prev.tile;
+      const long long excl = lookback_resolve(lb->status, ptile, prev.agg);
+      if (ptile == n_tiles - 1 && lane == 0) {
+        *total = excl + prev.agg;
+        if (status_out) {
+          int32_t stt = (excl + prev.agg > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
+          if (hdr && hdr->overflow) stt = NACC_ERR_UNSUPPORTED;
+          *status_out = stt;
+        }
+      }
+      const int64_t r_base = ptile * kFRaysPerWarp;
+      const int64_t my_run = excl + prev.incl - prev.c;
+      if (lane < kFRaysPerWarp && r_base + lane < n_rays)
+        reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(my_run, prev.c);
+      if (t0 != nullptr && excl + prev.agg <= capacity) {
+#pragma unroll 1
+        for (int j = 0; j < kFRaysPerWarp; ++j) {
+          const int64_t r = r_base + j;
+          if (r >= n_rays) break;
+          const int32_t c = __shfl_sync(kFull, prev.c, j);
+          if (c == 0) continue;
+          const int64_t run = __shfl_sync(kFull, my_run, j);
+          const int lpos = __shfl_sync(kFull, prev.lpos, j);
+          if (lpos >= 0) {
+            const int kb = __shfl_sync(kFull, prev.kb, j);
+            const float nr = s_setup[warp][pb][j].near_r;
+            const uint16_t *kl = kbuf[warp][pb] + lpos;
+            for (int i = lane; i < c; i += 32) {
+              const int k = kb + (int)kl[i];
+              float ta, tb;
+              lattice_ends<kCone>(p, nr, tab, k, ta, tb);
+              t0[run + i] = ta;
+              t1[run + i] = tb;
+              ray_id[run + i] = (int32_t)r;
+            }
+          } else {  // k-list overflowed: traverse again, writing directly
+            const RaySetup s = s_setup[warp][pb][j];
+            int kb0, ke0;
+            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+                                            [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                              if (pred) {
+                                                const int64_t q = run + cnt + __popc(b & ((1u << lane) - 1u));
+                                                float ta, tb;
+                                                lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb);
+                                                t0[q] = ta;
+                                                t1[q] = tb;
+                                                ray_id[q] = (int32_t)r;
+                                              }
+                                            });
+          }
+        }
+      }
+      __syncwarp();  // buffer pb is refilled next iteration
+    }
+    if (cur.tile < 0) break;
+    prev = cur;
+    buf ^= 1;
   }
 }
 
@@ -526,6 +570,37 @@ struct MarchWs {
 };
 
 static int64_t fused_tiles(int64_t n) { return ceil_div(n, kFRaysPerWarp); }
+
+// persistent grid: every warp resident at once (look-back needs no more; the
+// counter hands out tiles in order of arrival)
+static unsigned fused_blocks(int64_t n_tiles, bool cone, bool skip, bool l1) {
+  static int per_sm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, n_sm = 0;
+  const int v = (cone ? 4 : 0) | (skip ? 2 : 0) | (l1 ? 1 : 0);
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (per_sm[v] == 0) {
+    const void *fn = nullptr;
+    switch (v) {
+      case 0: fn = (const void *)march_fused_kernel<false, false, false>; break;
+      case 1: fn = (const void *)march_fused_kernel<false, false, true>; break;
+      case 2: fn = (const void *)march_fused_kernel<false, true, false>; break;
+      case 3: fn = (const void *)march_fused_kernel<false, true, true>; break;
+      case 4: fn = (const void *)march_fused_kernel<true, false, false>; break;
+      case 5: fn = (const void *)march_fused_kernel<true, false, true>; break;
+      case 6: fn = (const void *)march_fused_kernel<true, true, false>; break;
+      default: fn = (const void *)march_fused_kernel<true, true, true>; break;
+    }
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kFWarps * 32, 0);
+    per_sm[v] = b > 0 ? b : 1;
+  }
+  const int64_t want = ceil_div(n_tiles, (int64_t)kFWarps);
+  const int64_t cap = (int64_t)per_sm[v] * (n_sm > 0 ? n_sm : 1);
+  return (unsigned)(want < cap ? want : cap);
+}
 
 static size_t march_ws_layout(const nacc_grid &g, const nacc_march &p, int64_t n, MarchWs *w, void *base) {
   size_t off = 0;
@@ -627,7 +702,7 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
   if (!fill) {
     const int64_t n_tiles = fused_tiles(n_rays);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
-    NACC_DISPATCH3(march_fused_kernel, (unsigned)ceil_div(n_tiles, kFWarps), kFWarps * 32, stream, g, p, bits, mask2, M, rays_o,
+    NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, rays_o,
                    rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,
                    status_out, t0, t1, ray_id);
   } else {
