@@ -281,17 +281,23 @@ class Pipeline:
             torch.maximum(self.acc_status, outs["s"].status, out=self.acc_status)
 
         self.graphs = []
+        stages = (st_march, st_f1, st_filter, st_f2, st_rfwd, st_mse, st_rbwd)
         with torch.cuda.stream(side):
-            for fn in (st_march, st_f1, st_filter, st_f2, st_rfwd, st_mse, st_rbwd):
+            for fn in stages:
                 fn()  # eager warm-up of the stage on the side stream
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, pool=pool, stream=side):
                     fn()
                 self.graphs.append(g)
+            # the whole step as one graph (the timed path); per-stage graphs serve the stage breakdown
+            self.full_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.full_graph, pool=torch.cuda.graph_pool_handle(), stream=side):
+                for fn in stages:
+                    fn()
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
-        self.launches_per_graph_step = N.launch_count() + H.launch_count() - l0  # (eager + captured) / 2
-        self.launches_per_graph_step //= 2
+        self.launches_per_graph_step = N.launch_count() + H.launch_count() - l0  # (eager + 2 captures) / 3
+        self.launches_per_graph_step //= 3
         self.outs = outs
         self.capacity = cap1
         self.acc.zero_()
@@ -303,12 +309,13 @@ class Pipeline:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
         self.o_buf.copy_(o, non_blocking=True)
         self.d_buf.copy_(d, non_blocking=True)
-        for i, g in enumerate(self.graphs):
-            if timing:
+        if timing:  # stage breakdown: one graph per stage, events between
+            for i, g in enumerate(self.graphs):
                 ev[i].record()
-            g.replay()
-        if timing:
+                g.replay()
             ev[7].record()
+        else:
+            self.full_graph.replay()
         self.grid.update_every_n_steps(self.k, self.occ_fn, n=UPDATE_EVERY)
         if timing:
             ev[8].record()
@@ -532,7 +539,7 @@ def run_nacc(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            step(timing=not args.profile)
+            step(timing=args.eager and not args.profile)
         e1.record()
         torch.cuda.synchronize()
     barrier()
@@ -546,6 +553,10 @@ def run_nacc(args):
     else:
         stats = dict(pipe.stats)
     ms = e0.elapsed_time(e1)
+    if use_graph:  # stage breakdown (not the headline): per-stage graphs with events between them
+        for _ in range(min(args.steps, 50)):
+            pipe.step_graph(timing=True)
+        torch.cuda.synchronize()
     stages = pipe.stage_ms() if not args.profile else {}
     t = torch.tensor([ms, stats["post"], stats["pre"], stats["rays"]], dtype=torch.float64, device=device)
     if world > 1:

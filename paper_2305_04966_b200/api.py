@@ -152,13 +152,13 @@ def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec,
     g, p = grid.c(), params.c()
     ws = _ws(lib.nacc_sampling_occgrid_workspace_bytes(C.byref(g), C.byref(p), n), dev)
     packed = torch.empty((n, 2), dtype=torch.int64, device=dev)
-    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    total = torch.empty(1, dtype=torch.int64, device=dev)  # always written by the call
     cap = int(capacity) if capacity is not None else 0
     t0 = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
     t1 = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
     rid = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
     with_out = cap > 0
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    status = torch.empty(1, dtype=torch.int32, device=dev)
     check(lib.nacc_sampling_occgrid(C.byref(g), _ptr(bits), C.byref(p), _ptr(rays_o), _ptr(rays_d), _ptr(t_min),
                                     _ptr(t_max), n, _ptr(packed), _ptr(t0) if with_out else None,
                                     _ptr(t1) if with_out else None, _ptr(rid) if with_out else None, cap,
@@ -191,7 +191,7 @@ def filter_early_stop(samples: PackedSamples, sigma: torch.Tensor, eps: Optional
     sigma = _req(sigma.detach(), torch.float32, "sigma", N)
     ws = _ws(lib.nacc_filter_workspace_bytes(n), dev)
     packed = torch.empty((n, 2), dtype=torch.int64, device=dev)
-    total = torch.zeros(1, dtype=torch.int64, device=dev)
+    total = torch.empty(1, dtype=torch.int64, device=dev)  # always written by the call
     cap = max(N, 1)
     t0 = torch.empty(cap, dtype=torch.float32, device=dev)
     t1 = torch.empty(cap, dtype=torch.float32, device=dev)
@@ -220,6 +220,7 @@ class _RenderFn(torch.autograd.Function):
               "nacc_render_fwd")
         ctx.save_for_backward(packed_info, ray_id, t0, t1, sigma, rgb, cx)
         ctx.nle = nle
+        ctx.set_materialize_grads(False)  # unused outputs pass NULL gradients, not zero tensors
         return color, opacity, depth
 
     @staticmethod

@@ -371,8 +371,27 @@ __device__ __forceinline__ SegM segm_item(const Items &it, int j, double w, cons
   return x;
 }
 
+__device__ __forceinline__ void render_fwd_out(const SegM &v, int64_t r, float *__restrict__ color,
+                                               float *__restrict__ opacity, float *__restrict__ depth,
+                                               double *__restrict__ ctx) {
+  if (color) {
+    color[3 * r] = (float)v.c0;
+    color[3 * r + 1] = (float)v.c1;
+    color[3 * r + 2] = (float)v.c2;
+  }
+  if (opacity) opacity[r] = (float)v.o;
+  if (depth) depth[r] = (float)(v.n / fmax(v.o, 1e-10));
+  if (ctx) {
+    ctx[5 * r] = v.c0;
+    ctx[5 * r + 1] = v.c1;
+    ctx[5 * r + 2] = v.c2;
+    ctx[5 * r + 3] = v.o;
+    ctx[5 * r + 4] = v.n;
+  }
+}
+
 template <bool kVec>
-__global__ void __launch_bounds__(256, 2) render_fwd_warp_kernel(
+__global__ void __launch_bounds__(256, 3) render_fwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
@@ -405,36 +424,27 @@ __global__ void __launch_bounds__(256, 2) render_fwd_warp_kernel(
     warp_items_S(it, s, S, carryS);
     float col[12];
     load_rgb4(col, it, rgb, kVec);
-    double w[4];
-    SegM agg = segm_identity();
+    // One pass over the items: a ray whose head lies in this lane is summed
+    // here and written at its tail; only the lane's leading run (the ray
+    // entering from earlier lanes) waits for the warp scan.
+    SegM cur = segm_identity();  // sums since the lane start or its last head
+    SegM lead;                   // the leading run up to its tail, if that tail is in this lane
+    int64_t lead_r = -1;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const bool live = it.valid[j] && !(S[j] > L);
-      w[j] = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
-      agg = segm_combine(agg, segm_item(it, j, w[j], col));
-    }
-    SegM run = warp_segm_excl(agg, carryC);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      run = segm_combine(run, segm_item(it, j, w[j], col));
+      const double w = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
+      cur = segm_combine(cur, segm_item(it, j, w, col));
       if (it.tail[j]) {
-        const int64_t r = it.rid[j];
-        if (color) {
-          color[3 * r] = (float)run.c0;
-          color[3 * r + 1] = (float)run.c1;
-          color[3 * r + 2] = (float)run.c2;
-        }
-        if (opacity) opacity[r] = (float)run.o;
-        if (depth) depth[r] = (float)(run.n / fmax(run.o, 1e-10));
-        if (ctx) {
-          ctx[5 * r] = run.c0;
-          ctx[5 * r + 1] = run.c1;
-          ctx[5 * r + 2] = run.c2;
-          ctx[5 * r + 3] = run.o;
-          ctx[5 * r + 4] = run.n;
+        if (cur.f) render_fwd_out(cur, it.rid[j], color, opacity, depth, ctx);
+        else {
+          lead = cur;
+          lead_r = it.rid[j];
         }
       }
     }
+    const SegM enter = warp_segm_excl(cur, carryC);
+    if (lead_r >= 0) render_fwd_out(segm_combine(enter, lead), lead_r, color, opacity, depth, ctx);
   }
 }
 
@@ -480,7 +490,7 @@ __global__ void __launch_bounds__(256) ray_grad_kernel(int64_t n_rays, const dou
 }
 
 template <bool kVec>
-__global__ void __launch_bounds__(256, 2) render_bwd_warp_kernel(
+__global__ void __launch_bounds__(256, 3) render_bwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, const float4 *__restrict__ gcv, const double2 *__restrict__ gq,
