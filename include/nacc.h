@@ -89,13 +89,15 @@ typedef struct {
 
 /* Bytes of the bitfield buffer for `grid` (0 if invalid): the public fine bits
  * (4*ceil(levels*res^3/32) bytes, rounded up to 256) followed by a
- * library-private skip mask (1 bit per 4^3 macro cell, when res % 4 == 0). */
+ * library-private region: a 256-byte header (the boxes enclosing the occupied
+ * cells) and a skip mask (1 bit per 4^3 macro cell, when res % 4 == 0). */
 size_t nacc_grid_bits_bytes(const nacc_grid *grid);
 
-/* Rebuild the private skip mask of `bits` from its fine bits.  Required after
- * the caller writes fine bits directly; nacc_occgrid_update does it itself.
- * nacc_sampling_occgrid reads the mask (its results do not depend on it, only
- * its speed — but a stale mask would skip occupied cells). */
+/* Rebuild the private region of `bits` (occupied-cell boxes, skip mask) from
+ * its fine bits.  Required after the caller writes fine bits directly;
+ * nacc_occgrid_update does it itself.  nacc_sampling_occgrid reads the region
+ * (its results do not depend on it, only its speed — but a stale region would
+ * skip occupied cells). */
 nacc_status nacc_grid_prepare(const nacc_grid *grid, uint32_t *bits, cudaStream_t stream);
 
 /* Workspace for nacc_sampling_occgrid / _fill with n_rays rays. */
@@ -260,7 +262,7 @@ nacc_status nacc_occgrid_update(const nacc_grid *grid, float *density, const flo
                                 nacc_update_rule rule, float decay, float threshold,
                                 nacc_thresh_rule thresh_rule, uint32_t *bits, double *mean,
                                 void *ws, size_t ws_bytes, cudaStream_t stream);
-/* (bits: the full nacc_grid_bits_bytes() buffer; its skip mask is rebuilt.) */
+/* (bits: the full nacc_grid_bits_bytes() buffer; its private region is rebuilt.) */
 
 #ifdef __cplusplus
 }

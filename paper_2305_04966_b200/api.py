@@ -408,6 +408,7 @@ class OccupancyGrid:
         self.density = torch.zeros(spec.n_cells, dtype=torch.float32, device=self.device)
         nb = L.lib().nacc_grid_bits_bytes(C.byref(spec.c()))
         self.bits = torch.zeros(nb // 4, dtype=torch.int32, device=self.device)
+        check(L.lib().nacc_grid_prepare(C.byref(spec.c()), _ptr(self.bits), _stream()), "nacc_grid_prepare")
         self.decay, self.threshold, self.rule, self.thresh_rule, self.seed = decay, threshold, rule, thresh_rule, seed
         self.mean = torch.zeros(1, dtype=torch.float64, device=self.device)
         self._ws = _ws(L.lib().nacc_occgrid_workspace_bytes(C.byref(spec.c())), self.device)

@@ -1,12 +1,15 @@
-// gridaux.cu — the occupancy bitfield's auxiliary skip mask.
+// gridaux.cu — the occupancy bitfield's auxiliary region.
 //
 // After the public fine bits (cell q -> bit q & 31 of word q >> 5, nacc.h) the
-// bitfield buffer holds a library-private mask used by the march to skip empty
-// space: for every macro cell m (4^3 fine cells) of every level,
-// mask2[m] = OR of the fine bits of macro cells m + {0,1}^3, i.e. of the fine
-// cells [4m, 4m + 8)^3 clipped to the level.  It depends only on the fine bits,
-// so it is rebuilt when they change (nacc_occgrid_update, nacc_grid_prepare),
-// not on every march.
+// bitfield buffer holds library-private data used by the march to skip empty
+// space, rebuilt when the bits change (nacc_occgrid_update,
+// nacc_grid_prepare), not on every march:
+//   header (64 words): per level the index box of its occupied cells (int32
+//     x0,y0,z0,x1,y1,z1 at 6l) and the world box enclosing every occupied cell
+//     of every level, padded (6 floats at word 48; lo > hi when none is);
+//   mask2 (when skipping is enabled): for every macro cell m (4^3 fine cells)
+//     of every level, the OR of the fine bits of macro cells m + {0,1}^3,
+//     i.e. of the fine cells [4m, 4m + 8)^3 clipped to the level.
 #include "common.cuh"
 
 namespace nacc {
@@ -18,10 +21,100 @@ int64_t grid_aux_offset_words(const nacc_grid &g) {
   return ceil_div(ceil_div(cells, 32), 64) * 64;  // 256-byte aligned
 }
 
+int64_t grid_mask2_offset_words(const nacc_grid &g) { return grid_aux_offset_words(g) + kAuxHeaderWords; }
+
 static int64_t grid_aux_words(const nacc_grid &g) {
-  if (!grid_skip_enabled(g)) return 0;
+  if (!grid_skip_enabled(g)) return kAuxHeaderWords;
   const int64_t M = g.res / kMacroCells;
-  return ceil_div((int64_t)g.levels * M * M * M, 32);
+  return kAuxHeaderWords + ceil_div((int64_t)g.levels * M * M * M, 32);
+}
+
+__global__ void bbox_init_kernel(int32_t *__restrict__ hdr, int levels, int R) {
+  const int i = threadIdx.x;
+  if (i < 6 * levels) hdr[i] = (i % 6) < 3 ? R : -1;
+}
+
+// thread per fine word: index box of its set bits, reduced per level
+__global__ void __launch_bounds__(256) bbox_kernel(const uint32_t *__restrict__ bits, int levels, int R,
+                                                   int32_t *__restrict__ hdr) {
+  const int64_t R3 = (int64_t)R * R * R, cells = (int64_t)levels * R3;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t w = q < (cells + 31) / 32 ? bits[q] : 0u;
+  int lo[3] = {R, R, R}, hi[3] = {-1, -1, -1}, lv = -1;
+  while (w) {
+    const int b = __ffs(w) - 1;
+    w &= w - 1u;
+    const int64_t cell = q * 32 + b;
+    if (cell >= cells) break;
+    const int l = (int)(cell / R3);
+    const int64_t idx = cell - (int64_t)l * R3;
+    const int c[3] = {(int)(idx % R), (int)((idx / R) % R), (int)(idx / ((int64_t)R * R))};
+    if (l != lv && lv >= 0) {  // the word straddles levels: flush the previous level
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        atomicMin(hdr + 6 * lv + a, lo[a]);
+        atomicMax(hdr + 6 * lv + 3 + a, hi[a]);
+        lo[a] = R;
+        hi[a] = -1;
+      }
+    }
+    lv = l;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = min(lo[a], c[a]);
+      hi[a] = max(hi[a], c[a]);
+    }
+  }
+  // warp pre-reduction when every lane holding bits is on one level
+  const unsigned has = __ballot_sync(kFull, lv >= 0);
+  if (!has) return;
+  const int l0 = __shfl_sync(kFull, lv, __ffs(has) - 1);
+  if (__all_sync(kFull, lv < 0 || lv == l0)) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo[a] = min(lo[a], __shfl_xor_sync(kFull, lo[a], o));
+        hi[a] = max(hi[a], __shfl_xor_sync(kFull, hi[a], o));
+      }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        atomicMin(hdr + 6 * l0 + a, lo[a]);
+        atomicMax(hdr + 6 * l0 + 3 + a, hi[a]);
+      }
+  } else if (lv >= 0) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(hdr + 6 * lv + a, lo[a]);
+      atomicMax(hdr + 6 * lv + 3 + a, hi[a]);
+    }
+  }
+}
+
+// world box of all occupied cells: level l's box is lo_l + [i0, i1 + 1] * (hi_l - lo_l) / R,
+// widened by 1e-4 of the outermost width + 1e-6 (far above the fp32 error of P(k)'s positions)
+struct LevelBox {
+  double lo[8][3], hi[8][3];
+};
+__global__ void bbox_world_kernel(int32_t *__restrict__ hdr, LevelBox b, int levels, int R) {
+  if (threadIdx.x != 0) return;
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int l = 0; l < levels; ++l) {
+    const int32_t *h = hdr + 6 * l;
+    if (h[3] < 0) continue;  // level without occupied cells
+    for (int a = 0; a < 3; ++a) {
+      const double cw = (b.hi[l][a] - b.lo[l][a]) / R;
+      lo[a] = fmin(lo[a], b.lo[l][a] + h[a] * cw);
+      hi[a] = fmax(hi[a], b.lo[l][a] + (h[3 + a] + 1) * cw);
+    }
+  }
+  float *wb = reinterpret_cast<float *>(hdr + kAuxBoxWord);
+  for (int a = 0; a < 3; ++a) {
+    const double pad = 1e-4 * (b.hi[levels - 1][a] - b.lo[levels - 1][a]) + 1e-6;
+    wb[a] = lo[a] <= hi[a] ? (float)(lo[a] - pad) : INFINITY;
+    wb[3 + a] = lo[a] <= hi[a] ? (float)(hi[a] + pad) : -INFINITY;
+  }
 }
 
 __global__ void mask2_kernel(uint32_t *__restrict__ bits, int levels, int R, int64_t aux_off) {
@@ -49,11 +142,27 @@ __global__ void mask2_kernel(uint32_t *__restrict__ bits, int levels, int R, int
 }
 
 cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream) {
-  if (!grid_skip_enabled(g)) return cudaSuccess;
-  const int M = g.res / kMacroCells;
-  const int64_t n = (int64_t)g.levels * M * M * M;
-  mask2_kernel<<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, grid_aux_offset_words(g));
-  count_launch(1);
+  int32_t *hdr = reinterpret_cast<int32_t *>(bits + grid_aux_offset_words(g));
+  const int64_t cells = (int64_t)g.levels * g.res * g.res * g.res;
+  LevelBox lb;
+  for (int a = 0; a < 3; ++a) {
+    const double lo0 = (double)g.roi[a], hi0 = (double)g.roi[3 + a];
+    const double ctr = (lo0 + hi0) / 2.0, half = (hi0 - lo0) / 2.0;
+    for (int l = 0; l < g.levels; ++l) {  // the march's fp32 level boxes
+      lb.lo[l][a] = (double)(float)(ctr - half * std::ldexp(1.0, l));
+      lb.hi[l][a] = (double)(float)(ctr + half * std::ldexp(1.0, l));
+    }
+  }
+  bbox_init_kernel<<<1, 64, 0, stream>>>(hdr, g.levels, g.res);
+  bbox_kernel<<<grid_for(ceil_div(cells, 32), 256), 256, 0, stream>>>(bits, g.levels, g.res, hdr);
+  bbox_world_kernel<<<1, 32, 0, stream>>>(hdr, lb, g.levels, g.res);
+  count_launch(3);
+  if (grid_skip_enabled(g)) {
+    const int M = g.res / kMacroCells;
+    const int64_t n = (int64_t)g.levels * M * M * M;
+    mask2_kernel<<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, grid_mask2_offset_words(g));
+    count_launch(1);
+  }
   return cudaGetLastError();
 }
 

@@ -157,7 +157,10 @@ struct RaySetup {
 // The slab only bounds the k range (±2 steps of slack around the outermost box
 // padded by 1e-4 of its width), so fp32 with reciprocals is conservative
 // enough: its error (~1e-6 of t) is far below the slack.  P(k) decides.
-__device__ __forceinline__ RaySetup ray_setup(const GridConst &g, const MarchConst &p,
+// The slab box is the outermost level box intersected with the padded world
+// box of all occupied cells (gridaux.cu), so rays stop scanning where no cell
+// of any level can be occupied.
+__device__ __forceinline__ RaySetup ray_setup(const GridConst &g, const MarchConst &p, const float *__restrict__ obox,
                                               const float *__restrict__ rays_o, const float *__restrict__ rays_d,
                                               const float *__restrict__ t_min, const float *__restrict__ t_max,
                                               int64_t r) {
@@ -178,15 +181,16 @@ __device__ __forceinline__ RaySetup ray_setup(const GridConst &g, const MarchCon
   s.far_r = t_max ? __ldg(t_max + r) : p.far_plane;
   const float o[3] = {s.ox, s.oy, s.oz}, d[3] = {s.dx, s.dy, s.dz};
   float tmin = -INFINITY, tmax = INFINITY;
-  bool hit = true;
+  bool hit = __ldg(obox) <= __ldg(obox + 3);  // false when no cell is occupied
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
+    const float blo = fmaxf(g.olo[a], __ldg(obox + a)), bhi = fminf(g.ohi[a], __ldg(obox + 3 + a));
     if (fabsf(d[a]) > 1e-30f) {
       const float inv = __frcp_rn(d[a]);
-      float ta = (g.olo[a] - o[a]) * inv, tb = (g.ohi[a] - o[a]) * inv;
+      float ta = (blo - o[a]) * inv, tb = (bhi - o[a]) * inv;
       tmin = fmaxf(tmin, fminf(ta, tb));
       tmax = fminf(tmax, fmaxf(ta, tb));
-    } else if (!(g.olo[a] <= o[a] && o[a] < g.ohi[a])) {
+    } else if (!(blo <= o[a] && o[a] < bhi)) {
       hit = false;
     }
   }
@@ -226,13 +230,13 @@ struct ConeHeader {
   uint32_t t_cap_bits;
 };
 
-__global__ void cone_tcap_kernel(GridConst g, MarchConst p, const float *__restrict__ rays_o,
+__global__ void cone_tcap_kernel(GridConst g, MarchConst p, const float *__restrict__ obox, const float *__restrict__ rays_o,
                                  const float *__restrict__ rays_d, const float *__restrict__ t_max,
                                  int64_t n_rays, ConeHeader *hdr) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   float v = 0.0f;
   if (r < n_rays) {
-    RaySetup s = ray_setup(g, p, rays_o, rays_d, nullptr, t_max, r);
+    RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, nullptr, t_max, r);
     if (s.hit) v = s.t_hi;
   }
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, o));
@@ -404,7 +408,7 @@ struct FusedTile {  // per-lane metadata of a tile in flight (lane j: ray j)
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
-    const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
+    const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
     const float *__restrict__ t_max, int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr,
     const float *__restrict__ tab, LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info,
     int64_t *__restrict__ total, int64_t capacity, int32_t *__restrict__ status_out, float *__restrict__ t0,
@@ -427,7 +431,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
       // ---- phase 1 of `tile`: lane j < kFRaysPerWarp sets up ray r_base + j, the warp walks the rays in order
       const int64_t r_base = tile * kFRaysPerWarp;
       if (lane < kFRaysPerWarp && r_base + lane < n_rays)
-        s_setup[warp][buf][lane] = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r_base + lane);
+        s_setup[warp][buf][lane] = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r_base + lane);
       __syncwarp();
       cur.c = 0;
       cur.kb = 0;
@@ -533,6 +537,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(256) march_fill_kernel(GridConst g, MarchConst p, const uint32_t *__restrict__ bits,
                                                          const uint32_t *__restrict__ mask2, int M,
+                                                         const float *__restrict__ obox,
                                                          const float *__restrict__ rays_o,
                                                          const float *__restrict__ rays_d,
                                                          const float *__restrict__ t_min,
@@ -547,7 +552,7 @@ __global__ void __launch_bounds__(256) march_fill_kernel(GridConst g, MarchConst
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= n_rays) return;
   const int64_t out = packed_info[2 * r];
-  const RaySetup s = ray_setup(g, p, rays_o, rays_d, t_min, t_max, r);
+  const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r);
   int kb0, ke0;
   traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[threadIdx.x >> 5], kb0, ke0,
                                   [&](unsigned b, bool pred, int k, int32_t cnt) {
@@ -691,10 +696,12 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
   const bool skip = grid_skip_enabled(*grid);
   const bool l1 = grid->levels == 1;
   const int M = grid->res / kMacro;
-  const uint32_t *mask2 = bits + grid_aux_offset_words(*grid);  // built by nacc_grid_prepare / nacc_occgrid_update
+  // built by nacc_grid_prepare / nacc_occgrid_update (gridaux.cu)
+  const uint32_t *mask2 = bits + grid_mask2_offset_words(*grid);
+  const float *obox = reinterpret_cast<const float *>(bits + grid_aux_offset_words(*grid) + kAuxBoxWord);
   if (cone) {  // shared cone lattice table (reading #5)
     NACC_CUDA(cudaMemsetAsync(w.hdr, 0, sizeof(ConeHeader), stream));
-    cone_tcap_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(g, p, rays_o, rays_d, t_max, n_rays, w.hdr);
+    cone_tcap_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(g, p, obox, rays_o, rays_d, t_max, n_rays, w.hdr);
     cone_table_kernel<<<1, 32, 0, stream>>>(p, w.hdr, w.tab);
     count_launch(2);
     NACC_CHECK_LAUNCH();
@@ -702,12 +709,12 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
   if (!fill) {
     const int64_t n_tiles = fused_tiles(n_rays);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
-    NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, rays_o,
+    NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, obox, rays_o,
                    rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,
                    status_out, t0, t1, ray_id);
   } else {
     NACC_DISPATCH3(march_fill_kernel, (unsigned)grid_for(n_rays * 32, 256), 256, stream, g, p, bits, mask2, M,
-                   rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, packed_info, t0, t1, ray_id);
+                   obox, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, packed_info, t0, t1, ray_id);
   }
   count_launch(1);
   NACC_CHECK_LAUNCH();

@@ -138,6 +138,29 @@ def test_march_edge_cases(N):
     assert_march_equal(gpu_march(N, full, 1, 8, roi, o[:50], d[:50], step=1e-4), ref)
 
 
+@pytest.mark.parametrize("levels,res", [(1, 16), (3, 12), (2, 13)])
+def test_march_sparse_grid_bounds(N, levels, res):
+    """A handful of occupied cells (box corners, level boundaries): the march
+    narrows each ray's scan to the box enclosing the occupied cells, which must
+    never drop an emitted interval."""
+    rng = np.random.default_rng(50 + levels + res)
+    o, d = random_rays(4000, rng)
+    occ = np.zeros(levels * res**3, np.uint8)
+    picks = [0, res - 1, res * res - 1, res**3 - 1, (res // 2) * (1 + res + res * res)]
+    for l in range(levels):
+        for c in picks:
+            occ[l * res**3 + c] = 1
+    roi = (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5)
+    step = float(np.float32(0.003))
+    ref = O.march(occ, levels, res, roi, o, d, step=step)
+    assert ref[0][:, 1].sum() > 100
+    assert_march_equal(gpu_march(N, occ, levels, res, roi, o, d, step=step), ref)
+    one = np.zeros_like(occ)
+    one[(levels - 1) * res**3 + res**3 - 1] = 1  # only the outermost level's last corner cell
+    ref = O.march(one, levels, res, roi, o * 3, d, step=step)
+    assert_march_equal(gpu_march(N, one, levels, res, roi, o * 3, d, step=step), ref)
+
+
 def test_march_deterministic(N):
     rng = np.random.default_rng(2)
     o, d = random_rays(4000, rng)
