@@ -34,25 +34,28 @@ __device__ __forceinline__ void lookback_publish(unsigned long long *st, int64_t
 
 // one warp: after lookback_publish(tile, agg), walk back over the predecessors
 // (32 at a time) to this tile's exclusive prefix, publish the inclusive one
-// and return the exclusive one.  Predecessors publish their aggregates without
-// waiting on anything, so the walk always terminates.
+// and return the exclusive one.  Only the predecessors nearer than the nearest
+// published inclusive prefix are waited for (not the slowest of the 32 read).
+// Predecessors publish their aggregates without waiting on anything, so the
+// walk always terminates.
 __device__ __forceinline__ long long lookback_resolve(unsigned long long *st, int64_t tile, long long agg) {
   const int lane = threadIdx.x & 31;
   if (tile == 0) return 0;
   long long excl = 0;
   int64_t j = tile - 1;  // lanes look at tiles j, j-1, ..., j-31
+  unsigned ns = 32;
   for (;;) {
     const int64_t idx = j - lane;
-    unsigned long long w = idx >= 0 ? 0ull : 2ull;  // before tile 0: an inclusive prefix of 0
-    if (idx >= 0) {
-      w = ld_relaxed(st + idx);
-      while ((w & 3ull) == 0ull) {
-        __nanosleep(100);
-        w = ld_relaxed(st + idx);
-      }
-    }
+    const unsigned long long w = idx >= 0 ? ld_relaxed(st + idx) : 2ull;  // before tile 0: inclusive 0
     const unsigned m2 = __ballot_sync(kFull, (w & 3ull) == 2ull);
+    const unsigned m0 = __ballot_sync(kFull, (w & 3ull) == 0ull);
     const int last = m2 ? __ffs(m2) - 1 : 31;  // nearest predecessor with an inclusive prefix
+    const unsigned need = last == 31 ? kFull : ((2u << last) - 1u);
+    if (m0 & need) {  // a tile we need has not published yet: back off and re-read the window
+      __nanosleep(ns);
+      ns = ns < 1024 ? 2 * ns : ns;
+      continue;
+    }
     long long v = lane <= last ? (long long)(w >> 2) : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
