@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -37,7 +38,8 @@ def nvcc() -> str:
 
 def _compile(src: str, extra: list[str]) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    obj = os.path.join(BUILD, os.path.relpath(src, CSRC).replace(os.sep, "_") + ".o")
+    tag = ("_" + hashlib.sha1(" ".join(extra).encode()).hexdigest()[:8]) if extra else ""
+    obj = os.path.join(BUILD, os.path.relpath(src, CSRC).replace(os.sep, "_") + tag + ".o")
     deps = [src] + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj

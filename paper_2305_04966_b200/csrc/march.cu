@@ -11,6 +11,8 @@
 //   P(k) = m_k < far_r  and  l* exists  and  bit[l*][i]
 // The k range each warp scans is a conservative fp32 slab bound (±2 steps
 // around the padded outermost box); membership alone decides emission.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "lookback.cuh"
 
@@ -396,12 +398,22 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 // warp rarely waits) and writes that tile's packed_info and samples from the
 // other buffer with coalesced stores.  A ray whose k-list overflowed is
 // traversed again when its tile is written.
-constexpr int kFWarps = 4, kFRaysPerWarp = 8, kFKCap = 1024;
+#ifndef NACC_MARCH_KCAP
+#define NACC_MARCH_KCAP 1024
+#endif
+constexpr int kFWarps = 4, kFRaysPerWarp = 8, kFKCap = NACC_MARCH_KCAP;
+#ifndef NACC_MARCH_PIPE
+#define NACC_MARCH_PIPE 1
+#endif
+// pipeline depth: a tile is resolved and written after the warp has traversed kFPipe more tiles
+constexpr int kFPipe = NACC_MARCH_PIPE;
+constexpr int kFBufs = kFPipe + 1;
+
 static_assert(kFRaysPerWarp <= 32, "one lane holds one ray's metadata");
 
 struct FusedTile {  // per-lane metadata of a tile in flight (lane j: ray j)
   int64_t tile;
-  int32_t c, kb, lpos;
+  int32_t c, kb, lpos, buf;
   long long incl, agg;
 };
 
@@ -413,20 +425,24 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
     const float *__restrict__ tab, LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info,
     int64_t *__restrict__ total, int64_t capacity, int32_t *__restrict__ status_out, float *__restrict__ t0,
     float *__restrict__ t1, int32_t *__restrict__ ray_id) {
-  __shared__ uint16_t kbuf[kFWarps][2][kFKCap];
+  __shared__ uint16_t kbuf[kFWarps][kFBufs][kFKCap];
   __shared__ int seglist[kFWarps][32];
-  __shared__ RaySetup s_setup[kFWarps][2][kFRaysPerWarp];
+  __shared__ RaySetup s_setup[kFWarps][kFBufs][kFRaysPerWarp];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  FusedTile prev;
-  prev.tile = -1;
+  FusedTile pend[kFPipe > 0 ? kFPipe : 1];  // tiles traversed but not yet written, oldest first
+#pragma unroll
+  for (int i = 0; i < (kFPipe > 0 ? kFPipe : 1); ++i) pend[i].tile = -1;
   int buf = 0;
+  bool more = true;
 #pragma unroll 1
   for (;;) {
     unsigned int tile32 = 0;
-    if (lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
-    const int64_t tile = __shfl_sync(kFull, tile32, 0);
+    if (more && lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
+    const int64_t tile = more ? (int64_t)__shfl_sync(kFull, tile32, 0) : n_tiles;
+    more = tile < n_tiles;
     FusedTile cur;
-    cur.tile = tile < n_tiles ? tile : -1;
+    cur.tile = more ? tile : -1;
+    cur.buf = buf;
     if (cur.tile >= 0) {
       // ---- phase 1 of `tile`: lane j < kFRaysPerWarp sets up ray r_base + j, the warp walks the rays in order
       const int64_t r_base = tile * kFRaysPerWarp;
@@ -470,9 +486,16 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
       cur.agg = __shfl_sync(kFull, incl, 31);
       lookback_publish(lb->status, tile, cur.agg);
     }
+    // the tile to write now: the oldest pending one (or the one just traversed)
+    FusedTile prev = kFPipe ? pend[0] : cur;
+    if (kFPipe) {
+#pragma unroll
+      for (int i = 0; i + 1 < kFPipe; ++i) pend[i] = pend[i + 1];
+      pend[kFPipe > 0 ? kFPipe - 1 : 0] = cur;
+    }
     if (prev.tile >= 0) {
-      // ---- phase 2 of the previous tile (buffer buf ^ 1)
-      const int pb = buf ^ 1;
+      // ---- phase 2 of that tile (its own buffer)
+      const int pb = prev.buf;
       const int64_t ptile = prev.tile;
       const long long excl = lookback_resolve(lb->status, ptile, prev.agg);
       if (ptile == n_tiles - 1 && lane == 0) {
@@ -527,9 +550,11 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
       }
       __syncwarp();  // buffer pb is refilled next iteration
     }
-    if (cur.tile < 0) break;
-    prev = cur;
-    buf ^= 1;
+    bool pending = false;
+#pragma unroll
+    for (int i = 0; i < (kFPipe > 0 ? kFPipe : 1); ++i) pending |= kFPipe > 0 && pend[i].tile >= 0;
+    if (!more && !pending) break;
+    buf = buf + 1 == kFBufs ? 0 : buf + 1;
   }
 }
 
@@ -598,8 +623,13 @@ static unsigned fused_blocks(int64_t n_tiles, bool cone, bool skip, bool l1) {
       case 6: fn = (const void *)march_fused_kernel<true, true, false>; break;
       default: fn = (const void *)march_fused_kernel<true, true, true>; break;
     }
+    // experiment hooks: NACC_MARCH_CARVEOUT (% of the unified L1/shared array given to shared
+    // memory) and NACC_MARCH_BPS (resident blocks per SM)
+    if (const char *e = getenv("NACC_MARCH_CARVEOUT"))
+      cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(e));
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kFWarps * 32, 0);
+    if (const char *e = getenv("NACC_MARCH_BPS")) b = atoi(e) < b ? atoi(e) : b;
     per_sm[v] = b > 0 ? b : 1;
   }
   const int64_t want = ceil_div(n_tiles, (int64_t)kFWarps);
