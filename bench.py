@@ -325,9 +325,10 @@ class Pipeline:
 
 def run_extras(device, reps=20):
     """Secondary measurements of the other §8 rows (not the headline): the
-    CFG3 cascaded cone march (640k rays, 4 levels) and the CFG4 proposal path
+    CFG3 cascaded cone march (640k rays, 4 levels), the CFG4 proposal path
     (2^16 rays, 256 -> 96 -> 48 inverse-CDF resampling, then a 48-sample render
-    fwd+bwd).  Device time per call with CUDA events, inputs resident."""
+    fwd+bwd) and the P:86 no-gradient-filtering comparison on CFG2.  Device
+    time per call with CUDA events, inputs resident."""
     import torch
 
     import workloads as W
@@ -401,6 +402,40 @@ def run_extras(device, reps=20):
                             "render_fwd_ms": ms_f, "render_bwd_ms": ms_r,
                             "rendered_samples_per_s": n4 * 48 / ((ms_f + ms_r) / 1e3),
                             "rays_per_s": n4 / ((ms_a + ms_b + ms_f + ms_r) / 1e3)}
+    # ---- P:86 no-gradient filtering on CFG2: render fwd+bwd over every marched sample versus
+    # filter + render over the kept ones (library time; the harness field's share reported apart)
+    c2 = W.cfg2(n_rays=RAYS_PER_GPU)
+    spec2 = N.GridSpec(roi=c2.roi, res=c2.res, levels=c2.levels)
+    bits2 = N.prepare_bits(spec2, torch.from_numpy(W.pack_bits(c2.occ).view(np.int32)).to(device))
+    o2, d2 = torch.from_numpy(c2.rays_o).to(device), torch.from_numpy(c2.rays_d).to(device)
+    fld = H.TextureField(torch.from_numpy(c2.scene.data.reshape(-1, 4)).to(device), c2.scene.lo, c2.scene.hi)
+    s_all = N.sampling_occgrid(o2, d2, spec2, bits2, N.MarchParams(step=c2.step))
+    sg_all, rgb_all = fld.at_samples(o2, d2, s_all.t0, s_all.t1, s_all.ray_id)
+    g_all = torch.randn((RAYS_PER_GPU, 3), device=device)
+
+    def unfiltered():
+        col, _, _, cx = N.render_fwd(s_all, sg_all, rgb_all, EPS)
+        return N.render_bwd(s_all, sg_all, rgb_all, cx, g_all, None, None, EPS)
+
+    f_kept = N.filter_early_stop(s_all, sg_all, EPS, sync=False)  # capacity-sized, device total
+    sg_k, rgb_k = fld.at_samples(o2, d2, f_kept.t0, f_kept.t1, f_kept.ray_id, n_dev=f_kept.total)
+
+    def filtered():
+        f = N.filter_early_stop(s_all, sg_all, EPS, sync=False)
+        col, _, _, cx = N.render_fwd(f, sg_k, rgb_k, EPS)
+        return N.render_bwd(f, sg_k, rgb_k, cx, g_all, None, None, EPS)
+
+    ms_u, _ = timed(unfiltered)
+    ms_k, _ = timed(filtered)
+    ms_fu, _ = timed(lambda: fld.at_samples(o2, d2, s_all.t0, s_all.t1, s_all.ray_id))
+    ms_fs, _ = timed(lambda: fld.at_samples(o2, d2, s_all.t0, s_all.t1, s_all.ray_id, want_rgb=False))
+    ms_fk, _ = timed(lambda: fld.at_samples(o2, d2, f_kept.t0, f_kept.t1, f_kept.ray_id, n_dev=f_kept.total))
+    out["no_grad_filter_P86"] = {
+        "samples_marched": s_all.n_samples, "samples_kept": int(f_kept.total.item()),
+        "render_fwd_bwd_all_ms": ms_u, "filter_plus_render_fwd_bwd_kept_ms": ms_k,
+        "library_speedup": ms_u / ms_k,
+        "harness_field_all_sigma_rgb_ms": ms_fu, "harness_field_sigma_all_plus_sigma_rgb_kept_ms": ms_fs + ms_fk,
+        "speedup_with_harness_field": (ms_u + ms_fu) / (ms_k + ms_fs + ms_fk)}
     return out
 
 

@@ -236,6 +236,24 @@ def weights_bwd(packed_info, t0, t1, sigma, g_weights, g_trans=None, neg_log_eps
     return gs
 
 
+def weights_alpha_fwd(packed_info, alpha, neg_log_eps=np.inf):
+    """Alpha compositing (oracle.h or_weights_alpha_fwd): returns (w, T)."""
+    pi = _i64(packed_info).reshape(-1, 2)
+    w = np.zeros(len(alpha))
+    T = np.zeros(len(alpha))
+    lib().or_weights_alpha_fwd(_p(pi), C.c_int64(pi.shape[0]), _p(_f64(alpha)), C.c_double(neg_log_eps), _p(w),
+                               _p(T))
+    return w, T
+
+
+def weights_alpha_bwd(packed_info, alpha, g_weights, g_trans=None, neg_log_eps=np.inf):
+    pi = _i64(packed_info).reshape(-1, 2)
+    ga = np.zeros(len(alpha))
+    lib().or_weights_alpha_bwd(_p(pi), C.c_int64(pi.shape[0]), _p(_f64(alpha)), C.c_double(neg_log_eps),
+                               _p(_f64(g_weights)), _p(_f64(g_trans)), _p(ga))
+    return ga
+
+
 def accumulate(packed_info, weights, values=None, C_=1):
     pi = _i64(packed_info).reshape(-1, 2)
     n = pi.shape[0]

@@ -456,6 +456,55 @@ void or_weights_bwd(const int64_t *packed_info, int64_t n_rays, const double *t0
 }
 
 /* ------------------------------------------------------------------------ */
+/* Alpha compositing.                       */
+/* ------------------------------------------------------------------------ */
+void or_weights_alpha_fwd(const int64_t *packed_info, int64_t n_rays, const double *alpha,
+                          double neg_log_eps, double *weights, double *trans) {
+  const double eps_T = exp(-neg_log_eps);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t r = 0; r < n_rays; ++r) {
+    int64_t s = packed_info[2 * r], cnt = packed_info[2 * r + 1];
+    double T = 1.0;
+    for (int64_t i = 0; i < cnt; ++i) {
+      int64_t q = s + i;
+      int live = !(T < eps_T);
+      weights[q] = live ? T * alpha[q] : 0.0;
+      if (trans) trans[q] = T;
+      T *= 1.0 - alpha[q];
+    }
+  }
+}
+
+void or_weights_alpha_bwd(const int64_t *packed_info, int64_t n_rays, const double *alpha,
+                          double neg_log_eps, const double *g_weights, const double *g_trans,
+                          double *g_alpha) {
+  const double eps_T = exp(-neg_log_eps);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t r = 0; r < n_rays; ++r) {
+    int64_t s = packed_info[2 * r], cnt = packed_info[2 * r + 1];
+    double *Tv = (double *)malloc(sizeof(double) * (cnt > 0 ? cnt : 1));
+    int *live = (int *)malloc(sizeof(int) * (cnt > 0 ? cnt : 1));
+    double T = 1.0;
+    for (int64_t i = 0; i < cnt; ++i) {
+      Tv[i] = T;
+      live[i] = !(T < eps_T);
+      T *= 1.0 - alpha[s + i];
+    }
+    for (int64_t k = 0; k < cnt; ++k) {
+      double g = live[k] ? g_weights[s + k] * Tv[k] : 0.0;
+      double P = Tv[k]; /* Π_{j<i, j≠k} (1 − α_j) for i = k + 1 */
+      for (int64_t i = k + 1; i < cnt; ++i) {
+        double c = (live[i] ? g_weights[s + i] * alpha[s + i] : 0.0) + (g_trans ? g_trans[s + i] : 0.0);
+        g -= c * P;
+        P *= 1.0 - alpha[s + i];
+      }
+      g_alpha[s + k] = g;
+    }
+    free(Tv); free(live);
+  }
+}
+
+/* ------------------------------------------------------------------------ */
 /* accumulate_along_rays (Alg. 1 outputs): segmented sums.           */
 /* ------------------------------------------------------------------------ */
 void or_accumulate(const int64_t *packed_info, int64_t n_rays, const double *weights,

@@ -27,6 +27,7 @@
  *   or_filter_early_stop  pinned (monotonicity, P:86 bound)
  *   or_render_fwd/bwd     pinned (closed forms, finite differences)
  *   or_accumulate_*       pinned (closed forms)
+ *   or_weights_alpha_*    pinned (closed form, density-path equivalence, telescoping, finite differences)
  *   or_importance_sample  pinned (KS, strata, backward error)
  *   or_occgrid_*          pinned
  */
@@ -119,6 +120,22 @@ void or_render_bwd(const int64_t *packed_info, int64_t n_rays, const double *t0,
 void or_weights_bwd(const int64_t *packed_info, int64_t n_rays, const double *t0, const double *t1,
                     const double *sigma, double neg_log_eps, const double *g_weights,
                     const double *g_trans /* NULL allowed */, double *g_sigma);
+
+/* Alpha compositing for fields that supply α per interval (SDF-based fields,
+ * P:61; "accumulating them through alpha-composition"; SURVEY §8(f)
+ * row 2): T_i = Π_{j<i} (1 − α_j), sequential fp64 product; w_i = T_i α_i for
+ * live samples, 0 once T_i < ε_T with ε_T = exp(−neg_log_eps) (DESIGN.md
+ * reading #27).  trans may be NULL. */
+void or_weights_alpha_fwd(const int64_t *packed_info, int64_t n_rays, const double *alpha,
+                          double neg_log_eps, double *weights, double *trans);
+
+/* Its backward, the product rule written out (no division, so α = 1 is
+ * safe): g_α_k = [live_k] g_w_k T_k − Σ_{i>k} ([live_i] g_w_i α_i + g_T_i)
+ * Π_{j<i, j≠k} (1 − α_j); the liveness mask is a constant (reading #28).
+ * O(n²) per ray.  g_trans may be NULL. */
+void or_weights_alpha_bwd(const int64_t *packed_info, int64_t n_rays, const double *alpha,
+                          double neg_log_eps, const double *g_weights, const double *g_trans,
+                          double *g_alpha);
 
 /* accumulate_along_rays: out[r][c] = Σ_i w_i v_i[c] (values NULL = ones). */
 void or_accumulate(const int64_t *packed_info, int64_t n_rays, const double *weights,
