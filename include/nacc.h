@@ -179,6 +179,26 @@ nacc_status nacc_render_weights_bwd(const int64_t *packed_info, int64_t n_rays, 
                                     double neg_log_eps, const float *g_weights,
                                     const float *g_trans, float *g_sigma, cudaStream_t stream);
 
+/* Alpha compositing for fields that supply α per interval (SDF-based fields,
+ * P:61; "accumulating them through alpha-composition"; DESIGN.md
+ * readings #16-#17):  T_i = Π_{j<i} (1 − α_j),  w_i = T_i α_i, and w_i = 0
+ * once T_i < exp(−neg_log_eps) (+inf disables).  alphas [n_samples] f32 in
+ * [0, 1]; weights [n_samples] out; trans [n_samples] out (NULL allowed),
+ * unmasked.  fp64 products inside. */
+nacc_status nacc_render_weights_alpha_fwd(const int64_t *packed_info, int64_t n_rays,
+                                          const float *alphas, int64_t n_samples,
+                                          double neg_log_eps, float *weights, float *trans,
+                                          cudaStream_t stream);
+/* Workspace for the alpha backward: 8 bytes per sample (fp64 T). */
+size_t nacc_render_weights_alpha_bwd_workspace_bytes(int64_t n_samples);
+/* g_α_k = [live_k] g_w_k T_k − T_k Λ_k,  Λ_k = Σ_{i>k} ([live_i] g_w_i α_i + g_T_i)
+ * Π_{k<j<i} (1 − α_j)  (no division: α = 1 is safe).  g_trans may be NULL. */
+nacc_status nacc_render_weights_alpha_bwd(const int64_t *packed_info, int64_t n_rays,
+                                          const float *alphas, int64_t n_samples,
+                                          double neg_log_eps, const float *g_weights,
+                                          const float *g_trans, float *g_alphas, void *ws,
+                                          size_t ws_bytes, cudaStream_t stream);
+
 /* accumulate_along_rays: out[r][c] = Σ_i w_i v_i[c]; values == NULL means ones
  * (opacity, C must be 1).  1 <= C <= 64. */
 nacc_status nacc_accumulate_along_rays(const int64_t *packed_info, int64_t n_rays,

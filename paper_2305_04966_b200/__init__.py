@@ -18,6 +18,7 @@ from .api import (  # noqa: F401
     owner_slab,
     prepare_bits,
     render_weights,
+    render_weights_alpha,
     render_fwd,
     render_bwd,
     rendering,

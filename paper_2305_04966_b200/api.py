@@ -316,6 +316,40 @@ def render_weights(samples: PackedSamples, sigma: torch.Tensor, eps: Optional[fl
     return _WeightsFn.apply(samples.packed_info, samples.t0, samples.t1, sigma, neg_log_eps(eps))
 
 
+class _AlphaWeightsFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, packed_info, alphas, nle):
+        n, N = packed_info.shape[0], alphas.numel()
+        w = torch.empty_like(alphas)
+        T = torch.empty_like(alphas)
+        check(L.lib().nacc_render_weights_alpha_fwd(_ptr(packed_info), n, _ptr(alphas), N, nle, _ptr(w), _ptr(T),
+                                                    _stream()), "nacc_render_weights_alpha_fwd")
+        ctx.save_for_backward(packed_info, alphas)
+        ctx.nle = nle
+        ctx.set_materialize_grads(False)
+        return w, T
+
+    @staticmethod
+    def backward(ctx, g_w, g_T):
+        packed_info, alphas = ctx.saved_tensors
+        n, N = packed_info.shape[0], alphas.numel()
+        g_a = torch.empty_like(alphas)
+        gw = torch.zeros_like(alphas) if g_w is None else g_w.contiguous().float()
+        gT = None if g_T is None else g_T.contiguous().float()
+        ws = _ws(L.lib().nacc_render_weights_alpha_bwd_workspace_bytes(N), alphas.device)
+        check(L.lib().nacc_render_weights_alpha_bwd(_ptr(packed_info), n, _ptr(alphas), N, ctx.nle, _ptr(gw), _ptr(gT),
+                                                    _ptr(g_a), _ptr(ws), ws.numel(), _stream()),
+              "nacc_render_weights_alpha_bwd")
+        return None, g_a, None
+
+
+def render_weights_alpha(samples: PackedSamples, alphas: torch.Tensor, eps: Optional[float] = None):
+    """Alpha compositing for fields that return α per interval (SDF-based
+    fields): returns (weights, trans), differentiable w.r.t. α."""
+    alphas = _req(alphas, torch.float32, "alphas", samples.n_samples)
+    return _AlphaWeightsFn.apply(samples.packed_info, alphas, neg_log_eps(eps))
+
+
 class _AccumFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, packed_info, weights, values, C_):

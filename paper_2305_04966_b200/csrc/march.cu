@@ -16,6 +16,10 @@
 #include "common.cuh"
 #include "lookback.cuh"
 
+#ifndef NACC_MARCH_PREFETCH
+#define NACC_MARCH_PREFETCH 0  // build parameter: L1 prefetch of interior segments' bit words
+#endif
+
 namespace nacc {
 
 struct GridConst {
@@ -339,6 +343,23 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
         const float B[3] = {__fmaf_rn(mb, s.dx, s.ox), __fmaf_rn(mb, s.dy, s.oy), __fmaf_rn(mb, s.dz, s.oz)};
         code = segment_test<kL1>(g, mask2, M, A, B);
         flag = code != 0;
+#if NACC_MARCH_PREFETCH
+        if (code == 1) {  // interior segment: warm L1 with the bit words its points will read
+          const int R = g.res;
+          int ia[3], ib[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            ia[a] = min(max((int)floorf((A[a] - g.lo[0][a]) * g.s[0][a]), 0), R - 1);
+            ib[a] = min(max((int)floorf((B[a] - g.lo[0][a]) * g.s[0][a]), 0), R - 1);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t q = (uint32_t)ia[0] + (uint32_t)R * ((uint32_t)((c & 1) ? ib[1] : ia[1]) +
+                                                                (uint32_t)R * (uint32_t)((c & 2) ? ib[2] : ia[2]));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(bits + (q >> 5)));
+          }
+        }
+#endif
       }
       const unsigned F = __ballot_sync(kFull, flag);
       if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : 0);
@@ -402,6 +423,8 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 #define NACC_MARCH_KCAP 1024
 #endif
 constexpr int kFWarps = 4, kFRaysPerWarp = 8, kFKCap = NACC_MARCH_KCAP;
+// cone lattices and cascades give long rays (hundreds of samples): half the rays per tile
+constexpr int fused_rpt(bool cone, bool l1) { return (cone || !l1) ? kFRaysPerWarp / 2 : kFRaysPerWarp; }
 #ifndef NACC_MARCH_PIPE
 #define NACC_MARCH_PIPE 1
 #endif
@@ -425,7 +448,9 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
     const float *__restrict__ tab, LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info,
     int64_t *__restrict__ total, int64_t capacity, int32_t *__restrict__ status_out, float *__restrict__ t0,
     float *__restrict__ t1, int32_t *__restrict__ ray_id) {
-  __shared__ uint16_t kbuf[kFWarps][kFBufs][kFKCap];
+  constexpr int kCap = kFKCap;
+  constexpr int kRpt = fused_rpt(kCone, kL1);  // rays per tile
+  __shared__ uint16_t kbuf[kFWarps][kFBufs][kCap];
   __shared__ int seglist[kFWarps][32];
   __shared__ RaySetup s_setup[kFWarps][kFBufs][kFRaysPerWarp];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -444,18 +469,18 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
     cur.tile = more ? tile : -1;
     cur.buf = buf;
     if (cur.tile >= 0) {
-      // ---- phase 1 of `tile`: lane j < kFRaysPerWarp sets up ray r_base + j, the warp walks the rays in order
-      const int64_t r_base = tile * kFRaysPerWarp;
-      if (lane < kFRaysPerWarp && r_base + lane < n_rays)
+      // ---- phase 1 of `tile`: lane j < kRpt sets up ray r_base + j, the warp walks the rays in order
+      const int64_t r_base = tile * kRpt;
+      if (lane < kRpt && r_base + lane < n_rays)
         s_setup[warp][buf][lane] = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r_base + lane);
       __syncwarp();
       cur.c = 0;
       cur.kb = 0;
       cur.lpos = -1;
-      int pos = 0;  // warp-uniform fill level of the k-list; kFKCap + 1 once it overflowed
+      int pos = 0;  // warp-uniform fill level of the k-list
       uint16_t *kl = kbuf[warp][buf];
 #pragma unroll 1
-      for (int j = 0; j < kFRaysPerWarp; ++j) {
+      for (int j = 0; j < kRpt; ++j) {
         if (r_base + j >= n_rays) break;
         const RaySetup s = s_setup[warp][buf][j];
         const int start = pos;
@@ -465,11 +490,12 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
                                              [&](unsigned b, bool pred, int k, int32_t cnt) {
                                                const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
                                                const int off = k - kb0;
-                                               if (pred && q < kFKCap && off < 65536) kl[q] = (uint16_t)off;
+                                               if (pred && q < kCap && off < 65536) kl[q] = (uint16_t)off;
                                              });
         // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
-        const bool usable = start + c <= kFKCap && ke0 - kb0 <= 65536;
-        pos = usable ? start + c : kFKCap + 1;
+        // (an unusable list leaves its space to the tile's next rays; the ray is traversed again)
+        const bool usable = start + c <= kCap && ke0 - kb0 <= 65536;
+        pos = usable ? start + c : start;
         if (lane == j) {
           cur.c = c;
           cur.kb = kb0;
@@ -506,13 +532,13 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
           *status_out = stt;
         }
       }
-      const int64_t r_base = ptile * kFRaysPerWarp;
+      const int64_t r_base = ptile * kRpt;
       const int64_t my_run = excl + prev.incl - prev.c;
-      if (lane < kFRaysPerWarp && r_base + lane < n_rays)
+      if (lane < kRpt && r_base + lane < n_rays)
         reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(my_run, prev.c);
       if (t0 != nullptr && excl + prev.agg <= capacity) {
 #pragma unroll 1
-        for (int j = 0; j < kFRaysPerWarp; ++j) {
+        for (int j = 0; j < kRpt; ++j) {
           const int64_t r = r_base + j;
           if (r >= n_rays) break;
           const int32_t c = __shfl_sync(kFull, prev.c, j);
@@ -599,7 +625,7 @@ struct MarchWs {
   float *tab;
 };
 
-static int64_t fused_tiles(int64_t n) { return ceil_div(n, kFRaysPerWarp); }
+static int64_t fused_tiles(int64_t n, bool cone, bool l1) { return ceil_div(n, (int64_t)fused_rpt(cone, l1)); }
 
 // persistent grid: every warp resident at once (look-back needs no more; the
 // counter hands out tiles in order of arrival)
@@ -644,7 +670,7 @@ static size_t march_ws_layout(const nacc_grid &g, const nacc_march &p, int64_t n
     off += align_up(bytes, 256);
     return o;
   };
-  const size_t o_lb = take(8 + 8 * (size_t)fused_tiles(n));
+  const size_t o_lb = take(8 + 8 * (size_t)fused_tiles(n, p.cone_angle > 0.0f, g.levels == 1));
   size_t o_hdr = 0, o_tab = 0;
   const bool cone = p.cone_angle > 0.0f;
   if (cone) {
@@ -737,7 +763,7 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
     NACC_CHECK_LAUNCH();
   }
   if (!fill) {
-    const int64_t n_tiles = fused_tiles(n_rays);
+    const int64_t n_tiles = fused_tiles(n_rays, cone, l1);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
     NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, obox, rays_o,
                    rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,

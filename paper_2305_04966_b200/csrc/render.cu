@@ -646,6 +646,100 @@ __global__ void __launch_bounds__(256) weights_bwd_kernel(const int64_t *__restr
   }
 }
 
+// ------------------------------------------------------------------ alpha compositing
+// One warp per ray, chunks of 32 samples (readings #16-#17).  Forward: fp64
+// multiplicative warp scan of (1 − α) carried across chunks.  Backward: pass 1
+// recomputes T into the fp64 workspace; pass 2 walks the chunks from the end
+// with a warp suffix scan of the affine maps x -> c_k + (1 − α_k) x, which
+// yields Λ_k = Σ_{i>k} c_i Π_{k<j<i} (1 − α_j) without any division.
+__device__ __forceinline__ double warp_excl_prod(double v, double &total) {
+  const int lane = threadIdx.x & 31;
+  double incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl *= y;
+  }
+  double ex = __shfl_up_sync(kFull, incl, 1);
+  if (lane == 0) ex = 1.0;
+  total = __shfl_sync(kFull, incl, 31);
+  return ex;
+}
+
+__global__ void __launch_bounds__(256) weights_alpha_fwd_kernel(const int64_t *__restrict__ packed_info,
+                                                                int64_t n_rays, const float *__restrict__ alphas,
+                                                                double eps_T, float *__restrict__ weights,
+                                                                float *__restrict__ trans,
+                                                                double *__restrict__ trans64) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_rays) return;
+  const longlong2 pi = reinterpret_cast<const longlong2 *>(packed_info)[r];
+  const int64_t st = pi.x, cnt = pi.y;
+  double carry = 1.0;
+  for (int64_t base = 0; base < cnt; base += 32) {
+    const int64_t i = base + lane, q = st + i;
+    const bool valid = i < cnt;
+    const double a = valid ? (double)__ldg(alphas + q) : 0.0;
+    double tot;
+    const double T = carry * warp_excl_prod(1.0 - a, tot);
+    carry *= tot;
+    if (valid) {
+      if (weights) weights[q] = !(T < eps_T) ? (float)(T * a) : 0.f;
+      if (trans) trans[q] = (float)T;
+      if (trans64) trans64[q] = T;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) weights_alpha_bwd_kernel(const int64_t *__restrict__ packed_info,
+                                                                int64_t n_rays, const float *__restrict__ alphas,
+                                                                double eps_T, const float *__restrict__ g_weights,
+                                                                const float *__restrict__ g_trans,
+                                                                const double *__restrict__ trans64,
+                                                                float *__restrict__ g_alphas) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_rays) return;
+  const longlong2 pi = reinterpret_cast<const longlong2 *>(packed_info)[r];
+  const int64_t st = pi.x, cnt = pi.y;
+  double carry = 0.0;  // Λ of the last sample before the chunk processed next = M of its first sample
+  for (int64_t base = ((cnt - 1) / 32) * 32; base >= 0 && cnt > 0; base -= 32) {
+    const int64_t i = base + lane, q = st + i;
+    const bool valid = i < cnt;
+    double a = 1.0, c = 0.0, T = 0.0, gw = 0.0;  // identity map past the ray's end
+    bool live = false;
+    if (valid) {
+      const double al = (double)__ldg(alphas + q);
+      T = __ldg(trans64 + q);
+      live = !(T < eps_T);
+      gw = (double)__ldg(g_weights + q);
+      a = 1.0 - al;
+      c = (live ? gw * al : 0.0) + (g_trans ? (double)__ldg(g_trans + q) : 0.0);
+    }
+    // suffix composition of x -> c + a x over lanes lane..31 (inclusive)
+    double A = a, Bv = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double a2 = __shfl_down_sync(kFull, A, o), b2 = __shfl_down_sync(kFull, Bv, o);
+      if (lane + o < 32) {
+        Bv = Bv + A * b2;
+        A = A * a2;
+      }
+    }
+    // Λ_k = (maps of lanes > lane) applied to the carry: exclusive suffix
+    double Ae = __shfl_down_sync(kFull, A, 1), Be = __shfl_down_sync(kFull, Bv, 1);
+    if (lane == 31) {
+      Ae = 1.0;
+      Be = 0.0;
+    }
+    const double Lam = Be + Ae * carry;
+    if (valid) g_alphas[q] = (float)((live ? gw * T : 0.0) - T * Lam);
+    const double A0 = __shfl_sync(kFull, A, 0), B0 = __shfl_sync(kFull, Bv, 0);
+    carry = B0 + A0 * carry;
+  }
+}
+
 // ------------------------------------------------------------------ accumulate_along_rays
 template <int kC>
 __global__ void __launch_bounds__(256) accumulate_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
@@ -827,6 +921,50 @@ nacc_status nacc_render_weights_bwd(const int64_t *packed_info, int64_t n_rays, 
   weights_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma,
                                                                       neg_log_eps, g_weights, g_trans, g_sigma);
   count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+nacc_status nacc_render_weights_alpha_fwd(const int64_t *packed_info, int64_t n_rays, const float *alphas,
+                                          int64_t n_samples, double neg_log_eps, float *weights, float *trans,
+                                          cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_packed(packed_info, n_rays, n_samples);
+  if (s != NACC_OK) return s;
+  NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
+  if (n_rays == 0) return NACC_OK;
+  NACC_REQUIRE(n_samples == 0 || (alphas && weights), "alphas and weights must be non-NULL");
+  weights_alpha_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, alphas,
+                                                                            std::exp(-neg_log_eps), weights, trans,
+                                                                            nullptr);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+size_t nacc_render_weights_alpha_bwd_workspace_bytes(int64_t n_samples) {
+  return n_samples > 0 ? align_up((size_t)n_samples * 8, 256) : 256;
+}
+
+nacc_status nacc_render_weights_alpha_bwd(const int64_t *packed_info, int64_t n_rays, const float *alphas,
+                                          int64_t n_samples, double neg_log_eps, const float *g_weights,
+                                          const float *g_trans, float *g_alphas, void *ws, size_t ws_bytes,
+                                          cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_packed(packed_info, n_rays, n_samples);
+  if (s != NACC_OK) return s;
+  NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
+  if (n_rays == 0) return NACC_OK;
+  NACC_REQUIRE(n_samples == 0 || (alphas && g_weights && g_alphas), "alphas, g_weights, g_alphas must be non-NULL");
+  NACC_REQUIRE(ws && ws_bytes >= nacc_render_weights_alpha_bwd_workspace_bytes(n_samples) && aligned(ws, 8),
+               "workspace too small");
+  const double eps_T = std::exp(-neg_log_eps);
+  double *T64 = static_cast<double *>(ws);
+  weights_alpha_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, alphas, eps_T,
+                                                                            nullptr, nullptr, T64);
+  weights_alpha_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, alphas, eps_T,
+                                                                            g_weights, g_trans, T64, g_alphas);
+  count_launch(2);
   NACC_CHECK_LAUNCH();
   return NACC_OK;
 }

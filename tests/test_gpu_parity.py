@@ -395,6 +395,39 @@ def test_weights_and_accumulate(N):
         w.grad = None
 
 
+@pytest.mark.parametrize("eps", [None, 1e-4])
+def test_weights_alpha(N, eps):
+    """Alpha compositing (readings #16-#17) vs the oracle: ragged rays incl.
+    5000-sample ones, α with exact 0s and 1s (opaque samples), early stop."""
+    import torch
+
+    pk, _, _, _, _, _ = W.ragged_samples(1500, seed=21, long_rays=(2, 700), long_count=5000)
+    n_s = int(pk[:, 1].sum())
+    rng = np.random.default_rng(22)
+    a = rng.choice([0.0, 1.0, 0.02, 0.3], n_s, p=[0.3, 0.01, 0.5, 0.19]).astype(np.float32)
+    a *= rng.uniform(0.5, 1.0, n_s).astype(np.float32) ** (a < 1)
+    L = math.inf if eps is None else -math.log(float(np.float32(eps)))
+    s = N.PackedSamples(cuda(pk), cuda(np.zeros(n_s, np.float32)), cuda(np.zeros(n_s, np.float32)),
+                        cuda(np.zeros(n_s, np.int32)))
+    ag = cuda(a).requires_grad_()
+    w, T = N.render_weights_alpha(s, ag, eps=eps)
+    w_ref, T_ref = O.weights_alpha_fwd(pk, a, L)
+    # decisions within 1e-9 relative of ε_T are a tie band (product order differs)
+    eps_T = math.exp(-L)
+    tie = np.zeros(len(pk), bool)
+    if eps is not None:
+        near = np.abs(T_ref - eps_T) <= 1e-9 * eps_T
+        tie = np.add.reduceat(near.astype(np.int64), np.minimum(pk[:, 0], max(n_s - 1, 0))) > 0
+        tie &= pk[:, 1] > 0
+    ok = np.repeat(~tie, pk[:, 1])
+    assert np.all((np.abs(w.detach().cpu().numpy() - w_ref) <= 1e-5)[ok])
+    assert np.all(np.abs(T.detach().cpu().numpy() - T_ref) <= 1e-5)
+    gw, gT = rng.normal(size=n_s).astype(np.float32), rng.normal(size=n_s).astype(np.float32)
+    (w * cuda(gw)).sum().add_((T * cuda(gT)).sum()).backward()
+    ga = O.weights_alpha_bwd(pk, a, gw, gT, neg_log_eps=L)
+    assert np.all(grad_ok(ag.grad.cpu().numpy(), ga, pk)[ok])
+
+
 # ============================================================================ resample
 def check_resample(s_gpu, s_ref, F_ref, e, n_out, stratified=False, seed=0):
     n = len(s_gpu)
