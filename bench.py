@@ -69,7 +69,8 @@ def measured_peaks():
 
 
 NCU_KERNELS_OF_STAGE = {"march": ["march_fused"], "render_fwd": ["render_fwd_warp"], "render_bwd": ["render_bwd_warp"],
-                        "filter": ["filter_cut", "filter_copy"], "field_sigma": ["tex_samples"]}
+                        "filter": ["filter_cut", "filter_copy"], "field_sigma": ["tex_sigma4"],
+                        "field_sigma_rgb": ["field_samples"]}
 
 
 def ncu_traffic():
