@@ -232,6 +232,46 @@ def test_filter_ragged(N, seed):
         assert n_tie == 0
 
 
+def test_filter_exact_on_near_ties(N):
+    """Decisions within rounding of L: the parallel scan defers to the
+    definition's sequential order (one lane recomputes the ray), so cuts stay
+    bit-exact.  L is set to the sequential fp64 prefix itself (and 1 ulp off)."""
+    import ctypes as C
+
+    import torch
+    from paper_2305_04966_b200 import _lib as Lb
+
+    rng = np.random.default_rng(31)
+    counts = np.array([40, 3, 60, 17, 0, 33] * 20, np.int64)
+    pk = np.stack([np.concatenate([[0], np.cumsum(counts)[:-1]]), counts], 1).astype(np.int64)
+    n_s = int(counts.sum())
+    t0 = np.zeros(n_s, np.float32)
+    t1 = np.ones(n_s, np.float32)
+    sig = rng.choice(np.float32([0.1, 0.3, 0.7, 0.05]), n_s).astype(np.float32)
+    p = sig.astype(np.float64)  # δ = 1 exactly
+    S = 0.0
+    for i in range(19):  # sequential prefix of the first ray after 19 samples
+        S += p[i]
+    for L in (S, np.nextafter(S, 0), np.nextafter(S, 10), 2.0, 3.0):
+        ref = O.filter_early_stop(pk, t0, t1, sig, L)
+        dev = torch.device("cuda")
+        d_pk, d_t0, d_t1, d_sig = (torch.from_numpy(x).to(dev) for x in (pk, t0, t1, sig))
+        out_pk = torch.empty_like(d_pk)
+        o0, o1 = torch.empty_like(d_t0), torch.empty_like(d_t1)
+        orid = torch.empty(n_s, dtype=torch.int32, device=dev)
+        tot = torch.empty(1, dtype=torch.int64, device=dev)
+        lib = Lb.lib()
+        ws = torch.empty(lib.nacc_filter_workspace_bytes(len(pk)), dtype=torch.uint8, device=dev)
+        ptr = lambda x: C.c_void_p(x.data_ptr())
+        st = lib.nacc_filter_early_stop(ptr(d_pk), len(pk), ptr(d_t0), ptr(d_t1), ptr(d_sig), n_s, float(L),
+                                        ptr(out_pk), ptr(o0), ptr(o1), ptr(orid), n_s, ptr(tot), ptr(ws), ws.numel(),
+                                        None)
+        assert st == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(out_pk.cpu().numpy(), ref[0]), L
+        assert int(tot.item()) == len(ref[1])
+
+
 def test_filter_cfg2_full(N, cfg2):
     c, (pk, t0, t1, rid) = cfg2
     sig, _ = W.field_at_intervals(c.scene.sigma_rgb, c.rays_o, c.rays_d, t0, t1, rid)
