@@ -295,6 +295,36 @@ def importance_sample(s_edges, n_out, *, sigma=None, cdf=None, map_kind=1, t_nea
     return s_out, t_out
 
 
+def importance_sample_ranged(s_edges, n_out, t_near, t_far, *, sigma=None, cdf=None, map_kind=1, stratified=0,
+                             seed=0, want_t=True):
+    """O8 with per-ray [t_near, t_far] arrays (combined estimator, reading #19)."""
+    e = _f64(s_edges)
+    n, n_in = e.shape[0], e.shape[1] - 1
+    assert (sigma is None) != (cdf is None)
+    s_out = np.zeros((n, n_out + 1))
+    t_out = np.zeros((n, n_out + 1)) if want_t else None
+    lib().or_importance_sample_ranged(C.c_int64(n), C.c_int32(n_in), _p(e), _p(_f64(sigma)), _p(_f64(cdf)),
+                                      C.c_int(map_kind), _p(_f64(t_near)), _p(_f64(t_far)), C.c_int32(n_out),
+                                      C.c_int32(stratified), C.c_uint64(seed), _p(s_out), _p(t_out))
+    return s_out, t_out
+
+
+def ray_bounds(occ, levels, res, roi, rays_o, rays_d, *, near=0.0, far=1e10, step, max_step=1e10,
+               cone_angle=0.0, stratified=0, seed=0, t_min=None, t_max=None):
+    """Combined estimator, grid stage (reading #18): per-ray (t_near, t_far) f32 of the
+    intervals march() emits; (0, 0) for rays it culls."""
+    occ = np.ascontiguousarray(occ, dtype=np.uint8)
+    o, d = _f32(rays_o).reshape(-1, 3), _f32(rays_d).reshape(-1, 3)
+    n = o.shape[0]
+    t_min, t_max = _f32(t_min), _f32(t_max)
+    g, p = _grid(levels, res, roi), _march(near, far, step, max_step, cone_angle, stratified, seed)
+    tn = np.zeros(n, np.float32)
+    tf = np.zeros(n, np.float32)
+    lib().or_ray_bounds(C.byref(g), _p(occ), C.byref(p), _p(o), _p(d), _p(t_min), _p(t_max), C.c_int64(n),
+                        _p(tn), _p(tf))
+    return tn, tf
+
+
 def importance_cdf(s_edges, *, sigma=None, cdf=None, map_kind=1, t_near=0.2, t_far=1000.0):
     e = _f64(s_edges)
     n, n_in = e.shape[0], e.shape[1] - 1

@@ -583,46 +583,99 @@ void or_importance_cdf(int64_t n_rays, int32_t n_in, const double *s_edges, cons
                 cdf ? cdf + r * (n_in + 1) : NULL, map, t_near, t_far, cdf_hat + r * (n_in + 1));
 }
 
+/* One ray of O8 with its own [t_near, t_far]. */
+static void importance_ray(int64_t r, int32_t n_in, const double *s_edges, const double *sigma,
+                           const double *cdf, int map, double t_near, double t_far, int32_t n_out,
+                           int32_t stratified, const uint32_t key[2], double *s_out, double *t_out) {
+  const double *e = s_edges + r * (n_in + 1);
+  if (!(t_far > t_near)) {
+    /* culled ray (empty span, reading #19): uniform edges in s, every t at t_near */
+    for (int32_t i = 0; i <= n_out; ++i) {
+      s_out[r * (n_out + 1) + i] = e[0] + (e[n_in] - e[0]) * ((double)i / (double)n_out);
+      if (t_out) t_out[r * (n_out + 1) + i] = t_near;
+    }
+    return;
+  }
+  double *F = (double *)malloc(sizeof(double) * (n_in + 1));
+  cdf_hat_ray(n_in, e, sigma ? sigma + r * n_in : NULL, cdf ? cdf + r * (n_in + 1) : NULL, map,
+              t_near, t_far, F);
+  for (int32_t i = 0; i <= n_out; ++i) {
+    double u;
+    if (stratified) {
+      uint32_t ctr[4] = {(uint32_t)(r & 0xffffffffu), (uint32_t)((uint64_t)r >> 32), (uint32_t)i,
+                         1u},
+               out[4];
+      or_philox4x32_10(ctr, key, out);
+      u = ((double)i + or_u24(out[0])) / (double)(n_out + 1);
+    } else {
+      u = (double)i / (double)n_out;
+    }
+    double s;
+    if (u >= 1.0) {
+      /* u = 1: the end of the mass, smallest j with F̂_{j+1} = 1 */
+      int32_t j = 0;
+      while (j < n_in - 1 && F[j + 1] < 1.0) ++j;
+      s = (double)e[j + 1];
+    } else {
+      /* the unique j with F̂_j <= u < F̂_{j+1}: the largest j with F̂_j <= u */
+      int32_t j = 0;
+      for (int32_t k = 0; k < n_in; ++k)
+        if (F[k] <= u) j = k;
+      double ej = (double)e[j], ej1 = (double)e[j + 1];
+      s = ej + (u - F[j]) / (F[j + 1] - F[j]) * (ej1 - ej);
+    }
+    s_out[r * (n_out + 1) + i] = s;
+    if (t_out) t_out[r * (n_out + 1) + i] = or_contract(map, s, t_near, t_far);
+  }
+  free(F);
+}
+
 void or_importance_sample(int64_t n_rays, int32_t n_in, const double *s_edges, const double *sigma,
                           const double *cdf, int map, double t_near, double t_far, int32_t n_out,
                           int32_t stratified, uint64_t seed, double *s_out, double *t_out) {
   uint32_t key[2];
   philox_seed(seed, key);
 #pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t r = 0; r < n_rays; ++r)
+    importance_ray(r, n_in, s_edges, sigma, cdf, map, t_near, t_far, n_out, stratified, key, s_out,
+                   t_out);
+}
+
+void or_importance_sample_ranged(int64_t n_rays, int32_t n_in, const double *s_edges,
+                                 const double *sigma, const double *cdf, int map,
+                                 const double *t_near, const double *t_far, int32_t n_out,
+                                 int32_t stratified, uint64_t seed, double *s_out, double *t_out) {
+  uint32_t key[2];
+  philox_seed(seed, key);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t r = 0; r < n_rays; ++r)
+    importance_ray(r, n_in, s_edges, sigma, cdf, map, t_near[r], t_far[r], n_out, stratified, key,
+                   s_out, t_out);
+}
+
+/* Combined estimator, grid stage (reading #18): the span of
+ * the intervals nerfacc.sampling emits for the ray, by marching it. */
+void or_ray_bounds(const or_grid *g, const uint8_t *occ, const or_march *p, const float *rays_o,
+                   const float *rays_d, const float *t_min, const float *t_max, int64_t n_rays,
+                   float *t_near, float *t_far) {
+  gctx c;
+  grid_ctx(g, &c);
+#pragma omp parallel for schedule(dynamic, 64)
   for (int64_t r = 0; r < n_rays; ++r) {
-    double *F = (double *)malloc(sizeof(double) * (n_in + 1));
-    const double *e = s_edges + r * (n_in + 1);
-    cdf_hat_ray(n_in, e, sigma ? sigma + r * n_in : NULL, cdf ? cdf + r * (n_in + 1) : NULL, map,
-                t_near, t_far, F);
-    for (int32_t i = 0; i <= n_out; ++i) {
-      double u;
-      if (stratified) {
-        uint32_t ctr[4] = {(uint32_t)(r & 0xffffffffu), (uint32_t)((uint64_t)r >> 32), (uint32_t)i,
-                           1u},
-                 out[4];
-        or_philox4x32_10(ctr, key, out);
-        u = ((double)i + or_u24(out[0])) / (double)(n_out + 1);
-      } else {
-        u = (double)i / (double)n_out;
-      }
-      double s;
-      if (u >= 1.0) {
-        /* u = 1: the end of the mass, smallest j with F̂_{j+1} = 1 */
-        int32_t j = 0;
-        while (j < n_in - 1 && F[j + 1] < 1.0) ++j;
-        s = (double)e[j + 1];
-      } else {
-        /* the unique j with F̂_j <= u < F̂_{j+1}: the largest j with F̂_j <= u */
-        int32_t j = 0;
-        for (int32_t k = 0; k < n_in; ++k)
-          if (F[k] <= u) j = k;
-        double ej = (double)e[j], ej1 = (double)e[j + 1];
-        s = ej + (u - F[j]) / (F[j + 1] - F[j]) * (ej1 - ej);
-      }
-      s_out[r * (n_out + 1) + i] = s;
-      if (t_out) t_out[r * (n_out + 1) + i] = or_contract(map, s, t_near, t_far);
+    float nr = ray_near(p, t_min, r);
+    float fr = t_max ? t_max[r] : p->far_plane;
+    int64_t n = march_ray(&c, occ, p, rays_o + 3 * r, rays_d + 3 * r, nr, fr, 0, (int32_t)r, NULL,
+                          NULL, NULL);
+    t_near[r] = 0.0f;
+    t_far[r] = 0.0f;
+    if (n > 0) {
+      float *a = (float *)malloc(sizeof(float) * n), *b = (float *)malloc(sizeof(float) * n);
+      int32_t *id = (int32_t *)malloc(sizeof(int32_t) * n);
+      march_ray(&c, occ, p, rays_o + 3 * r, rays_d + 3 * r, nr, fr, 0, (int32_t)r, a, b, id);
+      t_near[r] = a[0];
+      t_far[r] = b[n - 1];
+      free(a); free(b); free(id);
     }
-    free(F);
   }
 }
 

@@ -29,6 +29,8 @@
  *   or_accumulate_*       pinned (closed forms)
  *   or_weights_alpha_*    pinned (closed form, density-path equivalence, telescoping, finite differences)
  *   or_importance_sample  pinned (KS, strata, backward error)
+ *   or_importance_sample_ranged, or_ray_bounds  pinned (reduction to the pinned
+ *                         scalar sampler / march, slab closed form, culling)
  *   or_occgrid_*          pinned
  */
 #ifndef NACC_ORACLE_H
@@ -151,6 +153,21 @@ void or_accumulate_bwd(const int64_t *packed_info, int64_t n_rays, const double 
 void or_importance_sample(int64_t n_rays, int32_t n_in, const double *s_edges, const double *sigma,
                           const double *cdf, int map, double t_near, double t_far, int32_t n_out,
                           int32_t stratified, uint64_t seed, double *s_out, double *t_out);
+/* The same with a per-ray [t_near_r, t_far_r] (the combined estimator's
+ * proposal stage); a ray with !(t_far_r > t_near_r) is culled:
+ * s_out uniform over [e_0, e_m], t_out = t_near_r (reading #19). */
+void or_importance_sample_ranged(int64_t n_rays, int32_t n_in, const double *s_edges,
+                                 const double *sigma, const double *cdf, int map,
+                                 const double *t_near, const double *t_far, int32_t n_out,
+                                 int32_t stratified, uint64_t seed, double *s_out, double *t_out);
+/* Combined estimator, grid stage ("stacking an occupancy grid on top
+ * of the proposal network ... reduce the number of rays and shrink the
+ * near-far plane"; reading #18): per ray, t_near = t0 of the first
+ * interval or_march emits and t_far = t1 of its last; both 0 when it emits
+ * none (the ray is culled). */
+void or_ray_bounds(const or_grid *g, const uint8_t *occ, const or_march *p, const float *rays_o,
+                   const float *rays_d, const float *t_min, const float *t_max, int64_t n_rays,
+                   float *t_near, float *t_far);
 /* the normalised CDF F̂ the sampler inverts (for backward-error checks) */
 void or_importance_cdf(int64_t n_rays, int32_t n_in, const double *s_edges, const double *sigma,
                        const double *cdf, int map, double t_near, double t_far, double *cdf_hat);
