@@ -242,6 +242,21 @@ nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, i
                             float *g_sigma, float *g_rgb, void *ws, size_t ws_bytes,
                             cudaStream_t stream);
 
+/* Combined estimator, grid stage ("stacking an occupancy grid on
+ * top of the proposal network ... reduce the number of rays and shrink the
+ * near-far plane"; reading #18).  Same inputs as
+ * nacc_sampling_occgrid; per ray t_near = t0 of the first interval it would
+ * emit and t_far = t1 of the last (bit-identical to those t0/t1), or
+ * t_near = t_far = 0 when it emits none (the ray is culled).
+ *   t_near, t_far  [n_rays] f32 out
+ *   n_alive        device uint64 out: rays with a span (NULL allowed)
+ *   ws             nacc_sampling_occgrid_workspace_bytes() bytes */
+nacc_status nacc_occgrid_ray_bounds(const nacc_grid *grid, const uint32_t *bits,
+                                   const nacc_march *params, const float *rays_o,
+                                   const float *rays_d, const float *t_min, const float *t_max,
+                                   int64_t n_rays, float *t_near, float *t_far, uint64_t *n_alive,
+                                   void *ws, size_t ws_bytes, cudaStream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* Proposal estimator: inverse-transform resampling (Eq. 1) of the  */
 /* CDF F = 1 - T (Eq. 3, "compute the CDF directly using 1 - T(t)", */
@@ -258,6 +273,16 @@ nacc_status nacc_importance_sample(int64_t n_rays, int32_t n_in, const float *s_
                                    double t_near, double t_far, int32_t n_out,
                                    int32_t stratified, uint64_t seed, float *s_out, float *t_out,
                                    cudaStream_t stream);
+/* The same with each ray's own span [t_near[r], t_far[r]] (f32 device arrays,
+ * e.g. from nacc_occgrid_ray_bounds; the combined estimator's proposal stage,
+ * reading #19).  A ray with !(t_far > t_near) is culled: s_out = uniform
+ * edges over [e_0, e_m], t_out = t_near.  Device precondition (unchecked):
+ * t_near > 0 on live rays for the lindisp map. */
+nacc_status nacc_importance_sample_ranged(int64_t n_rays, int32_t n_in, const float *s_edges,
+                                          const float *sigma, const float *cdf, nacc_map map,
+                                          const float *t_near, const float *t_far, int32_t n_out,
+                                          int32_t stratified, uint64_t seed, float *s_out,
+                                          float *t_out, cudaStream_t stream);
 
 /* ------------------------------------------------------------------------ */
 /* Occupancy-grid estimator update (EMA σ^k = γσ^{k-1} + (1-γ)σ_q,  */

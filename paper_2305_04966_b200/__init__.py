@@ -13,6 +13,7 @@ from .api import (  # noqa: F401
     accumulate_along_rays,
     filter_early_stop,
     importance_sample,
+    occgrid_ray_bounds,
     launch_count,
     neg_log_eps,
     owner_slab,

@@ -392,10 +392,12 @@ MAP_IDENTITY, MAP_LINDISP = 0, 1
 
 
 def importance_sample(s_edges: torch.Tensor, n_out: int, sigma: Optional[torch.Tensor] = None,
-                      cdf: Optional[torch.Tensor] = None, map_kind: int = MAP_LINDISP, t_near: float = 0.2,
-                      t_far: float = 1000.0, stratified: bool = False, seed: int = 0):
+                      cdf: Optional[torch.Tensor] = None, map_kind: int = MAP_LINDISP, t_near=0.2,
+                      t_far=1000.0, stratified: bool = False, seed: int = 0):
     """Inverse-CDF resampling of interval edges (Eq. 1 + Eq. 3; s-space
-    P:257).  s_edges [n, m+1]; returns (s_out, t_out) [n, n_out+1]."""
+    P:257).  s_edges [n, m+1]; returns (s_out, t_out) [n, n_out+1].  t_near /
+    t_far are scalars, or per-ray f32 tensors [n] (the combined estimator's
+    spans from ``occgrid_ray_bounds``; rays with t_far <= t_near are culled)."""
     n, m1 = s_edges.shape
     s_edges = _req(s_edges, torch.float32, "s_edges")
     if sigma is not None:
@@ -404,10 +406,45 @@ def importance_sample(s_edges: torch.Tensor, n_out: int, sigma: Optional[torch.T
         cdf = _req(cdf.detach(), torch.float32, "cdf", n * m1)
     s_out = torch.empty((n, n_out + 1), dtype=torch.float32, device=s_edges.device)
     t_out = torch.empty_like(s_out)
+    if isinstance(t_near, torch.Tensor) or isinstance(t_far, torch.Tensor):
+        tn = _req(t_near.detach(), torch.float32, "t_near", n)
+        tf = _req(t_far.detach(), torch.float32, "t_far", n)
+        check(L.lib().nacc_importance_sample_ranged(n, m1 - 1, _ptr(s_edges), _ptr(sigma), _ptr(cdf), int(map_kind),
+                                                    _ptr(tn), _ptr(tf), int(n_out), int(bool(stratified)), int(seed),
+                                                    _ptr(s_out), _ptr(t_out), _stream()),
+              "nacc_importance_sample_ranged")
+        return s_out, t_out
     check(L.lib().nacc_importance_sample(n, m1 - 1, _ptr(s_edges), _ptr(sigma), _ptr(cdf), int(map_kind),
                                          float(t_near), float(t_far), int(n_out), int(bool(stratified)), int(seed),
                                          _ptr(s_out), _ptr(t_out), _stream()), "nacc_importance_sample")
     return s_out, t_out
+
+
+def occgrid_ray_bounds(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec, bits: torch.Tensor,
+                       params: MarchParams, t_min: Optional[torch.Tensor] = None,
+                       t_max: Optional[torch.Tensor] = None):
+    """Combined estimator, grid stage (reading #18): per-ray span
+    (t_near, t_far) of the intervals ``sampling_occgrid`` would emit, (0, 0)
+    for culled rays, and the device count of live rays."""
+    lib = L.lib()
+    n = rays_o.shape[0]
+    dev = rays_o.device
+    rays_o = _req(rays_o, torch.float32, "rays_o", 3 * n)
+    rays_d = _req(rays_d, torch.float32, "rays_d", 3 * n)
+    bits = _req(bits, torch.int32, "bits")
+    if t_min is not None:
+        t_min = _req(t_min, torch.float32, "t_min", n)
+    if t_max is not None:
+        t_max = _req(t_max, torch.float32, "t_max", n)
+    g, p = grid.c(), params.c()
+    ws = _ws(lib.nacc_sampling_occgrid_workspace_bytes(C.byref(g), C.byref(p), n), dev)
+    tn = torch.empty(n, dtype=torch.float32, device=dev)
+    tf = torch.empty(n, dtype=torch.float32, device=dev)
+    alive = torch.empty(1, dtype=torch.int64, device=dev)
+    check(lib.nacc_occgrid_ray_bounds(C.byref(g), _ptr(bits), C.byref(p), _ptr(rays_o), _ptr(rays_d), _ptr(t_min),
+                                      _ptr(t_max), n, _ptr(tn), _ptr(tf), _ptr(alive), _ptr(ws), ws.numel(),
+                                      _stream()), "nacc_occgrid_ray_bounds")
+    return tn, tf, alive
 
 
 # ----------------------------------------------------------------------------- occupancy grid

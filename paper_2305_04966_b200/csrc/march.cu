@@ -618,6 +618,43 @@ __global__ void __launch_bounds__(256) march_fill_kernel(GridConst g, MarchConst
                                   });
 }
 
+// ---------------------------------------------------------------- per-ray span (combined estimator)
+// One warp per ray: the same traversal, keeping only the first and last
+// emitted lattice index (reading #18).
+template <bool kCone, bool kSkip, bool kL1>
+__global__ void __launch_bounds__(128) march_bounds_kernel(
+    GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
+    const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d,
+    const float *__restrict__ t_min, const float *__restrict__ t_max, int64_t n_rays,
+    const ConeHeader *__restrict__ hdr, const float *__restrict__ tab, float *__restrict__ t_near,
+    float *__restrict__ t_far, unsigned long long *__restrict__ n_alive) {
+  __shared__ int seglist[4][32];
+  const int lane = threadIdx.x & 31;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_rays) return;
+  const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r);
+  int kfirst = -1, klast = -1, kb0, ke0;
+  traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[threadIdx.x >> 5], kb0, ke0,
+                                  [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                    if (b) {
+                                      const int kf = __shfl_sync(kFull, k, __ffs(b) - 1);
+                                      klast = __shfl_sync(kFull, k, 31 - __clz(b));
+                                      if (kfirst < 0) kfirst = kf;
+                                    }
+                                  });
+  if (lane == 0) {
+    float ta = 0.f, tb = 0.f;
+    if (klast >= 0) {
+      float x, y;
+      lattice_ends<kCone>(p, s.near_r, tab, kfirst, ta, x);
+      lattice_ends<kCone>(p, s.near_r, tab, klast, y, tb);
+      if (n_alive) atomicAdd(n_alive, 1ull);
+    }
+    t_near[r] = ta;
+    t_far[r] = tb;
+  }
+}
+
 // -------------------------------------------------------------------------- host
 struct MarchWs {
   LookbackWs *lb;
@@ -738,12 +775,14 @@ static MarchConst make_march_const(const nacc_march &p) {
     else KERNEL<false, false, false><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);                     \
   } while (0)
 
-static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t *bits,
+enum MarchMode { kModeFused = 0, kModeFill = 1, kModeBounds = 2 };
+
+static nacc_status launch_march(int mode, const nacc_grid *grid, const uint32_t *bits,
                                 const nacc_march *params, const float *rays_o, const float *rays_d,
                                 const float *t_min, const float *t_max, int64_t n_rays,
                                 int64_t *packed_info, float *t0, float *t1, int32_t *ray_id,
                                 int64_t capacity, int64_t *total, int32_t *status_out, void *ws,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, unsigned long long *n_alive = nullptr) {
   MarchWs w;
   march_ws_layout(*grid, *params, n_rays, &w, ws);
   const GridConst g = make_grid_const(*grid);
@@ -762,7 +801,11 @@ static nacc_status launch_march(bool fill, const nacc_grid *grid, const uint32_t
     count_launch(2);
     NACC_CHECK_LAUNCH();
   }
-  if (!fill) {
+  if (mode == kModeBounds) {  // t0 / t1 carry t_near / t_far
+    if (n_alive) NACC_CUDA(cudaMemsetAsync(n_alive, 0, sizeof(unsigned long long), stream));
+    NACC_DISPATCH3(march_bounds_kernel, (unsigned)grid_for(n_rays * 32, 128), 128, stream, g, p, bits, mask2, M,
+                   obox, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, t0, t1, n_alive);
+  } else if (mode == kModeFused) {
     const int64_t n_tiles = fused_tiles(n_rays, cone, l1);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
     NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, obox, rays_o,
@@ -805,7 +848,7 @@ nacc_status nacc_sampling_occgrid(const nacc_grid *grid, const uint32_t *bits, c
   }
   NACC_REQUIRE(packed_info && aligned(packed_info, 16), "packed_info must be non-NULL and 16-byte aligned");
   NACC_REQUIRE((!t0 && !t1 && !ray_id) || (t0 && t1 && ray_id), "t0, t1, ray_id: all or none");
-  return launch_march(false, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays, packed_info, t0, t1,
+  return launch_march(kModeFused, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays, packed_info, t0, t1,
                       ray_id, capacity, total, status_out, ws, stream);
 }
 
@@ -820,8 +863,24 @@ nacc_status nacc_sampling_occgrid_fill(const nacc_grid *grid, const uint32_t *bi
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(packed_info && t0 && t1 && ray_id, "packed_info, t0, t1, ray_id must be non-NULL");
   // the cone table lives in the workspace; it is rebuilt here
-  return launch_march(true, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays,
+  return launch_march(kModeFill, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays,
                       const_cast<int64_t *>(packed_info), t0, t1, ray_id, 0, nullptr, nullptr, ws, stream);
+}
+
+nacc_status nacc_occgrid_ray_bounds(const nacc_grid *grid, const uint32_t *bits, const nacc_march *params,
+                                   const float *rays_o, const float *rays_d, const float *t_min,
+                                   const float *t_max, int64_t n_rays, float *t_near, float *t_far,
+                                   uint64_t *n_alive, void *ws, size_t ws_bytes, cudaStream_t stream) {
+  clear_error();
+  nacc_status st = validate(grid, bits, params, rays_o, rays_d, t_min, n_rays, ws, ws_bytes);
+  if (st != NACC_OK) return st;
+  if (n_rays == 0) {
+    if (n_alive) NACC_CUDA(cudaMemsetAsync(n_alive, 0, sizeof(uint64_t), stream));
+    return NACC_OK;
+  }
+  NACC_REQUIRE(t_near && t_far && aligned(t_near, 4) && aligned(t_far, 4), "t_near and t_far must be non-NULL");
+  return launch_march(kModeBounds, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays, nullptr, t_near, t_far,
+                      nullptr, 0, nullptr, nullptr, ws, stream, reinterpret_cast<unsigned long long *>(n_alive));
 }
 
 }  // extern "C"

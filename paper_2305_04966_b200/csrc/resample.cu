@@ -16,16 +16,29 @@ constexpr int kResampleWarps = 4;
 
 __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     int64_t n_rays, int n_in, const float *__restrict__ s_edges, const float *__restrict__ sigma,
-    const float *__restrict__ cdf, int map, double tn, double tf, int n_out, int stratified, uint32_t key0,
-    uint32_t key1, float *__restrict__ s_out, float *__restrict__ t_out) {
+    const float *__restrict__ cdf, int map, double tn, double tf, const float *__restrict__ tn_r,
+    const float *__restrict__ tf_r, int n_out, int stratified, uint32_t key0, uint32_t key1,
+    float *__restrict__ s_out, float *__restrict__ t_out) {
   extern __shared__ float smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r = (int64_t)blockIdx.x * kResampleWarps + warp;
   if (r >= n_rays) return;
   float *e = smem + (size_t)warp * 2 * (n_in + 1);
   float *F = e + (n_in + 1);
-  const double inv_tn = 1.0 / tn, inv_tf = isinf(tf) ? 0.0 : 1.0 / tf;
   const float *er = s_edges + r * (int64_t)(n_in + 1);
+  if (tn_r) {  // per-ray span (combined estimator, reading #19)
+    tn = (double)__ldg(tn_r + r);
+    tf = (double)__ldg(tf_r + r);
+    if (!(tf > tn)) {  // culled: uniform s edges, every t at t_near
+      const double e0 = (double)__ldg(er), em = (double)__ldg(er + n_in);
+      for (int i = lane; i <= n_out; i += 32) {
+        s_out[r * (int64_t)(n_out + 1) + i] = (float)(e0 + (em - e0) * ((double)i / (double)n_out));
+        if (t_out) t_out[r * (int64_t)(n_out + 1) + i] = (float)tn;
+      }
+      return;
+    }
+  }
+  const double inv_tn = 1.0 / tn, inv_tf = isinf(tf) ? 0.0 : 1.0 / tf;
   for (int j = lane; j <= n_in; j += 32) e[j] = __ldg(er + j);
   __syncwarp();
   bool uniform = false;
@@ -103,6 +116,35 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
   }
 }
 
+static nacc_status launch_importance(int64_t n_rays, int32_t n_in, const float *s_edges, const float *sigma,
+                                     const float *cdf, nacc_map map, double t_near, double t_far,
+                                     const float *tn_r, const float *tf_r, int32_t n_out, int32_t stratified,
+                                     uint64_t seed, float *s_out, float *t_out, cudaStream_t stream) {
+  NACC_REQUIRE(s_edges && s_out, "s_edges and s_out must be non-NULL");
+  const size_t smem = (size_t)kResampleWarps * 2 * (n_in + 1) * sizeof(float);
+  if (smem > 227 * 1024) {
+    set_error("nacc_importance_sample: n_in too large for shared memory");
+    return NACC_ERR_UNSUPPORTED;
+  }
+  if (smem > 48 * 1024)
+    NACC_CUDA(cudaFuncSetAttribute(importance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  importance_kernel<<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
+      n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, tn_r, tf_r, n_out, stratified,
+      (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), s_out, t_out);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+static nacc_status check_importance(int64_t n_rays, int32_t n_in, const float *sigma, const float *cdf, nacc_map map,
+                                    int32_t n_out) {
+  NACC_REQUIRE(n_rays >= 0, "n_rays must be >= 0");
+  NACC_REQUIRE(n_in >= 1 && n_out >= 1, "n_in and n_out must be >= 1");
+  NACC_REQUIRE((sigma != nullptr) != (cdf != nullptr), "exactly one of sigma / cdf must be non-NULL");
+  NACC_REQUIRE(map == NACC_MAP_IDENTITY || map == NACC_MAP_LINDISP, "unknown map");
+  return NACC_OK;
+}
+
 }  // namespace nacc
 
 using namespace nacc;
@@ -114,27 +156,26 @@ nacc_status nacc_importance_sample(int64_t n_rays, int32_t n_in, const float *s_
                                    int32_t stratified, uint64_t seed, float *s_out, float *t_out,
                                    cudaStream_t stream) {
   clear_error();
-  NACC_REQUIRE(n_rays >= 0, "n_rays must be >= 0");
-  NACC_REQUIRE(n_in >= 1 && n_out >= 1, "n_in and n_out must be >= 1");
-  NACC_REQUIRE((sigma != nullptr) != (cdf != nullptr), "exactly one of sigma / cdf must be non-NULL");
-  NACC_REQUIRE(map == NACC_MAP_IDENTITY || map == NACC_MAP_LINDISP, "unknown map");
+  nacc_status st = check_importance(n_rays, n_in, sigma, cdf, map, n_out);
+  if (st != NACC_OK) return st;
   NACC_REQUIRE(std::isfinite(t_near) && t_near > 0.0 && t_far > t_near, "need 0 < t_near < t_far");
   NACC_REQUIRE(map == NACC_MAP_LINDISP || std::isfinite(t_far), "identity map needs a finite t_far");
   if (n_rays == 0) return NACC_OK;
-  NACC_REQUIRE(s_edges && s_out, "s_edges and s_out must be non-NULL");
-  const size_t smem = (size_t)kResampleWarps * 2 * (n_in + 1) * sizeof(float);
-  if (smem > 227 * 1024) {
-    set_error("nacc_importance_sample: n_in too large for shared memory");
-    return NACC_ERR_UNSUPPORTED;
-  }
-  if (smem > 48 * 1024)
-    NACC_CUDA(cudaFuncSetAttribute(importance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  importance_kernel<<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
-      n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, n_out, stratified, (uint32_t)(seed & 0xffffffffu),
-      (uint32_t)(seed >> 32), s_out, t_out);
-  count_launch(1);
-  NACC_CHECK_LAUNCH();
-  return NACC_OK;
+  return launch_importance(n_rays, n_in, s_edges, sigma, cdf, map, t_near, t_far, nullptr, nullptr, n_out,
+                           stratified, seed, s_out, t_out, stream);
+}
+
+nacc_status nacc_importance_sample_ranged(int64_t n_rays, int32_t n_in, const float *s_edges, const float *sigma,
+                                          const float *cdf, nacc_map map, const float *t_near, const float *t_far,
+                                          int32_t n_out, int32_t stratified, uint64_t seed, float *s_out,
+                                          float *t_out, cudaStream_t stream) {
+  clear_error();
+  nacc_status st = check_importance(n_rays, n_in, sigma, cdf, map, n_out);
+  if (st != NACC_OK) return st;
+  if (n_rays == 0) return NACC_OK;
+  NACC_REQUIRE(t_near && t_far, "t_near and t_far must be non-NULL");
+  return launch_importance(n_rays, n_in, s_edges, sigma, cdf, map, 0.0, 0.0, t_near, t_far, n_out, stratified,
+                           seed, s_out, t_out, stream);
 }
 
 }  // extern "C"

@@ -541,6 +541,73 @@ def test_resample_cdf_input_stratified_and_degenerate(N):
     check_resample(sg.cpu().numpy(), sr, F, e, 17, stratified=True)
 
 
+# ============================================================================ combined estimator
+def gpu_bounds(N, occ, levels, res, roi, o, d, **kw):
+    import torch
+
+    spec = N.GridSpec(roi=roi, res=res, levels=levels)
+    bits = N.prepare_bits(spec, cuda(W.pack_bits(occ).view(np.int32)))
+    tn, tf, alive = N.occgrid_ray_bounds(cuda(o), cuda(d), spec, bits, N.MarchParams(**kw))
+    torch.cuda.synchronize()
+    return tn.cpu().numpy(), tf.cpu().numpy(), int(alive.item())
+
+
+def test_ray_bounds_bit_exact(N, cfg2):
+    """Readings #18: the span equals the first t0 / last t1 the march emits, bit-exactly."""
+    c, _ = cfg2
+    tn_r, tf_r = O.ray_bounds(c.occ, 1, 128, c.roi, c.rays_o, c.rays_d, step=c.step)
+    tn, tf, alive = gpu_bounds(N, c.occ, 1, 128, c.roi, c.rays_o, c.rays_d, step=c.step)
+    assert np.array_equal(tn, tn_r) and np.array_equal(tf, tf_r)
+    assert alive == int((tf_r > tn_r).sum()) > 1000
+    rng = np.random.default_rng(41)
+    o, d = random_rays(3000, rng)
+    roi = (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5)
+    for levels, res, cone in ((1, 16, 0), (3, 8, 1), (2, 13, 0)):
+        occ = (rng.random(levels * res**3) < 0.1).astype(np.uint8)
+        kw = dict(step=float(np.float32(0.005)))
+        if cone:
+            kw.update(cone_angle=float(np.float32(1 / 128)), max_step=float(np.float32(0.05)), near=0.02)
+        ref = O.ray_bounds(occ, levels, res, roi, o, d, **kw)
+        if "near" in kw:
+            kw["near_plane"] = kw.pop("near")
+        got = gpu_bounds(N, occ, levels, res, roi, o, d, **kw)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+    tn, tf, alive = gpu_bounds(N, np.zeros(8**3, np.uint8), 1, 8, roi, o, d, step=0.01)
+    assert alive == 0 and not tn.any() and not tf.any()
+
+
+def test_combined_estimator_cfg2(N, cfg2):
+    """Readings #18-#19 on CFG2 rays: grid spans, then one proposal round
+    (64 -> 32 edges, identity map inside each span) vs the oracle; culled
+    rays get uniform edges at t_near."""
+    import torch
+
+    c, _ = cfg2
+    sub = np.random.default_rng(42).choice(len(c.rays_o), 3000, replace=False)
+    o, d = c.rays_o[sub], c.rays_d[sub]
+    tn, tf = O.ray_bounds(c.occ, 1, 128, c.roi, o, d, step=c.step)
+    n, m = len(o), 64
+    e0 = np.tile(np.linspace(0, 1, m + 1, dtype=np.float32), (n, 1))
+    tm = tn[:, None].astype(np.float64) + 0.5 * (e0[:, :-1] + e0[:, 1:]) * (tf - tn)[:, None]
+    x = o[:, None, :].astype(np.float64) + tm[..., None] * d[:, None, :]
+    sig = c.scene.sigma_rgb(x.reshape(-1, 3))[0].reshape(n, m).astype(np.float32)
+    sg, tg = N.importance_sample(cuda(e0), 32, sigma=cuda(sig), map_kind=N.MAP_IDENTITY, t_near=cuda(tn),
+                                 t_far=cuda(tf))
+    sr, trr = O.importance_sample_ranged(e0, 32, tn, tf, sigma=sig, map_kind=0)
+    torch.cuda.synchronize()
+    sg, tg = sg.cpu().numpy(), tg.cpu().numpy()
+    live = tf > tn
+    assert live.sum() > 1000 and (~live).sum() > 100
+    assert np.array_equal(sg[~live], sr[~live].astype(np.float32)) and np.all(tg[~live] == tn[~live, None])
+    idx = np.nonzero(live)[0]
+    F = np.stack([O.importance_cdf(e0[r:r + 1], sigma=sig[r:r + 1], map_kind=0, t_near=float(tn[r]),
+                                   t_far=float(tf[r]))[0] for r in idx])
+    check_resample(sg[idx], sr[idx], F, e0[idx], 32)
+    # t_out = Φ_r(s_out) on each ray's own span
+    assert np.allclose(tg[idx], tn[idx, None] + sg[idx].astype(np.float64) * (tf - tn)[idx, None], rtol=2e-7,
+                       atol=1e-6)
+
+
 # ============================================================================ grid update
 def test_occgrid_points_bit_exact(N):
     import torch
