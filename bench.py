@@ -437,6 +437,32 @@ def run_extras(device, reps=20):
         "library_speedup": ms_u / ms_k,
         "harness_field_all_sigma_rgb_ms": ms_fu, "harness_field_sigma_all_plus_sigma_rgb_kept_ms": ms_fs + ms_fk,
         "speedup_with_harness_field": (ms_u + ms_fu) / (ms_k + ms_fs + ms_fk)}
+    # ---- P:120-122 combined estimator on CFG2 rays: grid spans (culling), then one proposal
+    # round 64 -> 32 edges inside each span (identity map), then a 32-sample render fwd+bwd
+    n2, m2 = RAYS_PER_GPU, 64
+    prm2 = N.MarchParams(step=c2.step)
+    ms_b, (tn2, tf2, alive2) = timed(lambda: N.occgrid_ray_bounds(o2, d2, spec2, bits2, prm2))
+    e64 = torch.linspace(0, 1, m2 + 1, device=device).repeat(n2, 1).contiguous()
+    tm = tn2[:, None] + 0.5 * (e64[:, :-1] + e64[:, 1:]) * (tf2 - tn2)[:, None]
+    rid64 = torch.arange(n2, device=device, dtype=torch.int32).repeat_interleave(m2)
+    sig64, _ = fld.at_samples(o2, d2, tm.reshape(-1).contiguous(), tm.reshape(-1).contiguous(), rid64,
+                              want_rgb=False)
+    ms_p, (s32, t32) = timed(lambda: N.importance_sample(e64, 32, sigma=sig64.view(n2, m2), map_kind=N.MAP_IDENTITY,
+                                                         t_near=tn2, t_far=tf2))
+    pk32 = torch.stack([torch.arange(n2, device=device, dtype=torch.int64) * 32,
+                        torch.full((n2,), 32, device=device, dtype=torch.int64)], 1).contiguous()
+    rid32 = torch.arange(n2, device=device, dtype=torch.int32).repeat_interleave(32)
+    samp32 = N.PackedSamples(pk32, t32[:, :-1].contiguous().view(-1), t32[:, 1:].contiguous().view(-1), rid32)
+    sg32, rgb32 = fld.at_samples(o2, d2, samp32.t0, samp32.t1, rid32)
+    ms_rf, (col32, _, _, cx32) = timed(lambda: N.render_fwd(samp32, sg32, rgb32, EPS))
+    ms_rb, _ = timed(lambda: N.render_bwd(samp32, sg32, rgb32, cx32, g_all, None, None, EPS))
+    n_alive = int(alive2.item())
+    out["combined_estimator_P120"] = {
+        "rays": n2, "rays_alive_after_grid": n_alive, "culled_fraction": 1.0 - n_alive / n2,
+        "mean_span_alive": float(((tf2 - tn2)[tf2 > tn2]).mean().item()), "ray_bounds_ms": ms_b, "proposal_64_to_32_ms": ms_p,
+        "render_fwd_ms": ms_rf, "render_bwd_ms": ms_rb,
+        "library_ms": ms_b + ms_p + ms_rf + ms_rb,
+        "rays_per_s": n2 / ((ms_b + ms_p + ms_rf + ms_rb) / 1e3)}
     return out
 
 
