@@ -345,6 +345,17 @@ def occgrid_points(levels, res, roi, seed, step, jitter, cell_begin=0, cell_coun
     return xyz
 
 
+def occgrid_times(levels, res, roi, seed, step, draw, cell_begin=0, cell_count=None):
+    """Per-cell timestamps of draw `draw` for dynamic scenes (reading #20)."""
+    g = _grid(levels, res, roi)
+    if cell_count is None:
+        cell_count = levels * res ** 3 - cell_begin
+    t = np.zeros(cell_count, np.float32)
+    lib().or_occgrid_times(C.byref(g), C.c_uint64(seed), C.c_int64(step), C.c_int32(draw), C.c_int64(cell_begin),
+                           C.c_int64(cell_count), _p(t))
+    return t
+
+
 def occgrid_update(levels, res, roi, density, fresh, *, rule=0, decay=0.95, threshold=0.01,
                    thresh_rule=0):
     """O9.  Returns (density' f32, bits uint8, mean)."""

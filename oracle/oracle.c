@@ -709,6 +709,21 @@ void or_occgrid_points(const or_grid *g, uint64_t seed, int64_t step, int32_t ji
   }
 }
 
+void or_occgrid_times(const or_grid *g, uint64_t seed, int64_t step, int32_t draw,
+                      int64_t cell_begin, int64_t cell_count, float *times) {
+  uint32_t key[2];
+  philox_seed(seed, key);
+  const int64_t R = g->res, R3 = R * R * R;
+#pragma omp parallel for schedule(static)
+  for (int64_t q = 0; q < cell_count; ++q) {
+    int64_t cell = cell_begin + q;
+    int64_t l = cell / R3, idx = cell % R3;
+    uint32_t ctr[4] = {(uint32_t)idx, (uint32_t)step, (uint32_t)l, 16u + (uint32_t)draw}, out[4];
+    or_philox4x32_10(ctr, key, out);
+    times[q] = (float)or_u24(out[0]);
+  }
+}
+
 void or_occgrid_update(const or_grid *g, float *density, const float *fresh, int32_t rule,
                        float decay, float threshold, int32_t thresh_rule, uint8_t *occ_bits,
                        double *mean_out) {

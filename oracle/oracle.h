@@ -32,6 +32,7 @@
  *   or_importance_sample_ranged, or_ray_bounds  pinned (reduction to the pinned
  *                         scalar sampler / march, slab closed form, culling)
  *   or_occgrid_*          pinned
+ *   or_occgrid_times      pinned (Philox KAT via or_philox4x32_10, u24 grid, uniformity)
  */
 #ifndef NACC_ORACLE_H
 #define NACC_ORACLE_H
@@ -177,6 +178,13 @@ void or_importance_cdf(int64_t n_rays, int32_t n_in, const double *s_edges, cons
  * or ξ = 1/2 when jitter == 0. */
 void or_occgrid_points(const or_grid *g, uint64_t seed, int64_t step, int32_t jitter,
                        int64_t cell_begin, int64_t cell_count, float *xyz);
+/* Dynamic scenes (one grid shared across frames holds "the maximum
+ * opacity at this area over all the timestamps"; reading
+ * #20): draw j of the per-cell timestamp, t = u24(Philox(seed, (i_cell, step,
+ * l, 16 + j)).x) in [0, 1).  The caller evaluates σ(x, t) per draw and merges
+ * the draws with MAX before the update. */
+void or_occgrid_times(const or_grid *g, uint64_t seed, int64_t step, int32_t draw,
+                      int64_t cell_begin, int64_t cell_count, float *times);
 /* rule 0 = EMA, 1 = max-decay; thresh_rule 0 = fixed τ, 1 = min(τ, mean).
  * density is updated in place; occ_bits receives one uint8 per cell. */
 void or_occgrid_update(const or_grid *g, float *density, const float *fresh, int32_t rule,

@@ -186,3 +186,51 @@ def test_owner_computes_max_merge_equals_single_rank():
         merged = np.maximum.reduce(bufs)
         got = O.occgrid_update(3, 8, ROI, dens, merged, decay=0.95, threshold=0.5)
         assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+
+
+def test_dynamic_timestamps_uniform_and_reproducible():
+    """reading #20: per-cell timestamps on the 2^-24 grid in [0, 1), uniform
+    (KS), independent across draws, sub-ranges are slices of the full range."""
+    from scipy import stats
+
+    R = 32
+    t0 = O.occgrid_times(1, R, ROI, seed=7, step=16, draw=0)
+    t1 = O.occgrid_times(1, R, ROI, seed=7, step=16, draw=1)
+    for t in (t0, t1):
+        assert t.min() >= 0 and t.max() < 1
+        assert np.array_equal(t * 2.0**24, np.floor(t * 2.0**24))
+        assert stats.kstest(t.astype(np.float64), "uniform").pvalue > 1e-3
+    assert abs(np.corrcoef(t0, t1)[0, 1]) < 0.03
+    assert np.array_equal(O.occgrid_times(1, R, ROI, seed=7, step=16, draw=1, cell_begin=100, cell_count=50),
+                          t1[100:150])
+    assert not np.array_equal(t0, O.occgrid_times(1, R, ROI, seed=7, step=32, draw=0))
+
+
+def test_dynamic_grid_holds_the_max_over_time():
+    """the shared grid marks the maximum opacity over all timestamps.  A
+    sphere moving along x over t in [0, 1): cells it covers at every t are
+    occupied after one draw, cells it never reaches never are, and with many
+    draws the occupied set approaches the swept volume."""
+    R = 32
+    xyz = O.occgrid_points(1, R, ROI, seed=0, step=0, jitter=0).astype(np.float64)
+
+    rad = 0.25
+
+    def sigma(x, t):  # radius 0.25, centre (0.35 + 0.3 t, 0.5, 0.5)
+        c = np.stack([0.35 + 0.3 * t, np.full_like(t, 0.5), np.full_like(t, 0.5)], 1)
+        return np.where(np.linalg.norm(x - c, axis=1) < rad, 10.0, 0.0).astype(np.float32)
+
+    fresh = None
+    for j in range(48):
+        v = sigma(xyz, O.occgrid_times(1, R, ROI, seed=3, step=0, draw=j).astype(np.float64))
+        fresh = v if fresh is None else np.maximum(fresh, v)
+    _, bits, _ = O.occgrid_update(1, R, ROI, np.zeros(R**3, np.float32), fresh, decay=0.0, threshold=1.0)
+    dy = np.linalg.norm(xyz[:, 1:] - 0.5, axis=1)
+    # |x − c(t)|² is convex in t, so a point inside at t = 0 and at t = 1 is inside for every t
+    c0, c1 = np.array([0.35, 0.5, 0.5]), np.array([0.65, 0.5, 0.5])
+    always = (np.linalg.norm(xyz - c0, axis=1) < rad - 1e-3) & (np.linalg.norm(xyz - c1, axis=1) < rad - 1e-3)
+    never = np.linalg.norm(np.stack([np.clip(xyz[:, 0], 0.35, 0.65) - xyz[:, 0], dy], 1), axis=1) > rad
+    assert always.sum() > 0 and np.all(bits[always] == 1)
+    assert np.all(bits[never] == 0)
+    swept = ~never
+    assert bits[swept].mean() > 0.9  # 48 draws cover nearly the whole swept volume
