@@ -308,6 +308,17 @@ nacc_status nacc_occgrid_update(const nacc_grid *grid, float *density, const flo
                                 nacc_thresh_rule thresh_rule, uint32_t *bits, double *mean,
                                 void *ws, size_t ws_bytes, cudaStream_t stream);
 /* (bits: the full nacc_grid_bits_bytes() buffer; its private region is rebuilt.) */
+/* Dynamic scenes (one grid shared across frames holds "the maximum
+ * opacity at this area over all the timestamps"; reading #20).
+ * times[q] = draw `draw` of cell (cell_begin + q)'s timestamp in [0, 1):
+ * u24(Philox4x32-10(seed, (cell index in level, step, level, 16 + draw)).x).
+ * The caller evaluates σ(x, t) at (nacc_occgrid_points, times) for each draw
+ * and folds the draws into `fresh` with nacc_max_merge before the update. */
+nacc_status nacc_occgrid_times(const nacc_grid *grid, uint64_t seed, int64_t step, int32_t draw,
+                               int64_t cell_begin, int64_t cell_count, float *times,
+                               cudaStream_t stream);
+/* dst[i] = max(dst[i], src[i]) for i < n (device f32 arrays). */
+nacc_status nacc_max_merge(float *dst, const float *src, int64_t n, cudaStream_t stream);
 
 #ifdef __cplusplus
 }

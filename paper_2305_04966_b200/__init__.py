@@ -14,6 +14,7 @@ from .api import (  # noqa: F401
     filter_early_stop,
     importance_sample,
     occgrid_ray_bounds,
+    max_merge,
     launch_count,
     neg_log_eps,
     owner_slab,

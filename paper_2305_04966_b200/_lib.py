@@ -72,6 +72,8 @@ SIGNATURES = {
     "nacc_importance_sample": (C.c_int, [I64, I32, P, P, P, C.c_int, D, D, I32, I32, U64, P, P, P]),
     "nacc_importance_sample_ranged": (C.c_int, [I64, I32, P, P, P, C.c_int, P, P, I32, I32, U64, P, P, P]),
     "nacc_occgrid_ray_bounds": (C.c_int, [GP, P, MP, P, P, P, P, I64, P, P, P, P, SZ, P]),
+    "nacc_occgrid_times": (C.c_int, [GP, U64, I64, I32, I64, I64, P, P]),
+    "nacc_max_merge": (C.c_int, [P, P, I64, P]),
     "nacc_occgrid_points": (C.c_int, [GP, U64, I64, I32, I64, I64, P, P]),
     "nacc_occgrid_workspace_bytes": (SZ, [GP]),
     "nacc_occgrid_update": (C.c_int, [GP, P, P, C.c_int, F, F, C.c_int, P, P, P, SZ, P]),

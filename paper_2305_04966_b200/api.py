@@ -493,6 +493,16 @@ class OccupancyGrid:
                                           int(cell_count), _ptr(xyz), _stream()), "nacc_occgrid_points")
         return xyz
 
+    def times(self, step: int, draw: int, cell_begin: int = 0, cell_count: Optional[int] = None):
+        """Per-cell timestamps in [0, 1) of draw `draw` (dynamic scenes; reading #20)."""
+        if cell_count is None:
+            cell_count = self.spec.n_cells - cell_begin
+        t = torch.empty(cell_count, dtype=torch.float32, device=self.device)
+        g = self.spec.c()
+        check(L.lib().nacc_occgrid_times(C.byref(g), self.seed, int(step), int(draw), int(cell_begin),
+                                         int(cell_count), _ptr(t), _stream()), "nacc_occgrid_times")
+        return t
+
     def update(self, fresh: torch.Tensor):
         fresh = _req(fresh, torch.float32, "fresh", self.spec.n_cells)
         g = self.spec.c()
@@ -501,13 +511,16 @@ class OccupancyGrid:
                                           _ptr(self.bits), _ptr(self.mean), _ptr(self._ws), self._ws.numel(),
                                           _stream()), "nacc_occgrid_update")
 
-    def update_every_n_steps(self, step: int, occ_eval_fn: Callable[[torch.Tensor], torch.Tensor], n: int = 16,
-                             jitter: bool = True, process_group=None) -> bool:
+    def update_every_n_steps(self, step: int, occ_eval_fn: Callable[..., torch.Tensor], n: int = 16,
+                             jitter: bool = True, process_group=None, time_draws: int = 0) -> bool:
         """Alg. 1 ``estimator.update_every_n_steps``: every n steps,
         owner-computes the fresh values σ(x)·Δt on this rank's cell slab,
         merges them with a MAX all-reduce over the process group (the path's
         one collective; non-owners contribute 0 since σ >= 0) and applies
-        the identical update on every rank."""
+        the identical update on every rank.  With time_draws = K > 0 the
+        scene is dynamic: occ_eval_fn(x, t) is evaluated at K
+        per-cell timestamps and the draws are merged with MAX, so the grid
+        holds the maximum opacity over time."""
         if step % n != 0:
             return False
         world, rank = 1, 0
@@ -516,14 +529,35 @@ class OccupancyGrid:
             rank = torch.distributed.get_rank(process_group)
         C_ = self.spec.n_cells
         lo, hi = owner_slab(C_, rank, world)
-        vals = occ_eval_fn(self.points(step, jitter, lo, hi - lo)) if hi > lo else \
-            torch.zeros(0, dtype=torch.float32, device=self.device)
+        if hi <= lo:
+            vals = torch.zeros(0, dtype=torch.float32, device=self.device)
+        elif time_draws <= 0:
+            vals = occ_eval_fn(self.points(step, jitter, lo, hi - lo))
+        else:
+            x = self.points(step, jitter, lo, hi - lo)
+            vals = None
+            for j in range(int(time_draws)):
+                v = _req(occ_eval_fn(x, self.times(step, j, lo, hi - lo)), torch.float32, "occ", hi - lo)
+                if vals is None:
+                    vals = v.clone()
+                else:
+                    max_merge(vals, v)
         self.update(merge_fresh(vals, lo, hi, C_, process_group))
         return True
 
     def state_dict(self):
         return {"density": self.density.clone(), "spec": dataclasses.asdict(self.spec), "decay": self.decay,
                 "threshold": self.threshold, "rule": self.rule, "thresh_rule": self.thresh_rule, "seed": self.seed}
+
+
+def max_merge(dst: torch.Tensor, src: torch.Tensor) -> torch.Tensor:
+    """dst = max(dst, src) in place (nacc_max_merge)."""
+    n = dst.numel()
+    if not (dst.is_contiguous() and dst.dtype == torch.float32):
+        raise ValueError("dst must be a contiguous float32 tensor")
+    src = _req(src, torch.float32, "src", n)
+    check(L.lib().nacc_max_merge(_ptr(dst), _ptr(src), n, _stream()), "nacc_max_merge")
+    return dst
 
 
 def launch_count() -> int:

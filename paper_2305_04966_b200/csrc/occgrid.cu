@@ -54,6 +54,39 @@ __global__ void __launch_bounds__(256) points_kernel(LevelBoxes b, uint32_t key0
   }
 }
 
+// dynamic scenes (reading #20): draw j of the per-cell timestamp
+__global__ void __launch_bounds__(256) times_kernel(int R, uint32_t key0, uint32_t key1, uint32_t step, uint32_t draw,
+                                                    int64_t cell_begin, int64_t cell_count, float *__restrict__ t) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= cell_count) return;
+  const int64_t R3 = (int64_t)R * R * R;
+  const int64_t cell = cell_begin + q;
+  const int l = (int)(cell / R3);
+  const int64_t idx = cell - (int64_t)l * R3;
+  const u32x4 rnd = philox4x32_10(u32x4{(uint32_t)idx, step, (uint32_t)l, 16u + draw}, key0, key1);
+  t[q] = (float)u24(rnd.x);
+}
+
+// fresh = max(fresh, v): merge of time draws (and the shape of the cross-rank MAX)
+__global__ void __launch_bounds__(256) max_merge_kernel(float *__restrict__ dst, const float *__restrict__ src,
+                                                        int64_t n) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i + 3 < n && ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    float4 a = *reinterpret_cast<float4 *>(dst + i);
+    const float4 b = __ldg(reinterpret_cast<const float4 *>(src + i));
+    a.x = b.x > a.x ? b.x : a.x;
+    a.y = b.y > a.y ? b.y : a.y;
+    a.z = b.z > a.z ? b.z : a.z;
+    a.w = b.w > a.w ? b.w : a.w;
+    *reinterpret_cast<float4 *>(dst + i) = a;
+  } else {
+    for (int64_t j = i; j < i + 4 && j < n; ++j) {
+      const float b = __ldg(src + j);
+      if (b > dst[j]) dst[j] = b;
+    }
+  }
+}
+
 constexpr int kUpdThreads = 256;
 
 // EMA / max-decay; optional direct binarisation (fixed τ); per-block fp64 sums
@@ -180,6 +213,35 @@ nacc_status nacc_occgrid_update(const nacc_grid *grid, float *density, const flo
   }
   NACC_CHECK_LAUNCH();
   NACC_CUDA(grid_prepare(*grid, bits, stream));  // refresh the march's skip mask
+  return NACC_OK;
+}
+
+nacc_status nacc_occgrid_times(const nacc_grid *grid, uint64_t seed, int64_t step, int32_t draw,
+                               int64_t cell_begin, int64_t cell_count, float *times, cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_grid(grid);
+  if (s != NACC_OK) return s;
+  const int64_t n = (int64_t)grid->levels * grid->res * grid->res * grid->res;
+  NACC_REQUIRE(cell_begin >= 0 && cell_count >= 0 && cell_begin + cell_count <= n, "cell range out of bounds");
+  NACC_REQUIRE(draw >= 0, "draw must be >= 0");
+  if (cell_count == 0) return NACC_OK;
+  NACC_REQUIRE(times && aligned(times, 4), "times must be non-NULL");
+  times_kernel<<<grid_for(cell_count, 256), 256, 0, stream>>>(grid->res, (uint32_t)(seed & 0xffffffffu),
+                                                             (uint32_t)(seed >> 32), (uint32_t)step, (uint32_t)draw,
+                                                             cell_begin, cell_count, times);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+nacc_status nacc_max_merge(float *dst, const float *src, int64_t n, cudaStream_t stream) {
+  clear_error();
+  NACC_REQUIRE(n >= 0, "n must be >= 0");
+  if (n == 0) return NACC_OK;
+  NACC_REQUIRE(dst && src && aligned(dst, 4) && aligned(src, 4), "dst and src must be non-NULL");
+  max_merge_kernel<<<grid_for(ceil_div(n, 4), 256), 256, 0, stream>>>(dst, src, n);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
   return NACC_OK;
 }
 

@@ -662,3 +662,48 @@ def test_update_every_n_steps_single_rank(N):
     torch.cuda.synchronize()
     bits = np.unpackbits(g.bits.cpu().numpy().view(np.uint8), bitorder="little")[: spec.n_cells]
     assert bits.mean() == 0.125  # 3 updates with γ = 0.95: 0.3·(1-0.95^3) > 0.01
+
+
+def test_dynamic_grid_times_and_max_merge(N):
+    """Reading #20: per-cell timestamps bit-exact vs the oracle (both sides run
+    Philox4x32-10); the MAX merge of draws and the update on the merged values
+    bit-exact; update_every_n_steps(time_draws=K) reproduces the oracle grid."""
+    import torch
+
+    levels, R = 2, 16
+    roi = (0, 0, 0, 1, 1, 1)
+    spec = N.GridSpec(roi=roi, res=R, levels=levels)
+    g = N.OccupancyGrid(spec, seed=11, decay=0.9, threshold=0.1)  # one update: occ = 0.1 σ
+    for draw in (0, 5):
+        t_gpu = g.times(step=32, draw=draw).cpu().numpy()
+        assert np.array_equal(t_gpu, O.occgrid_times(levels, R, roi, 11, 32, draw))
+    part = g.times(step=32, draw=1, cell_begin=1000, cell_count=777).cpu().numpy()
+    assert np.array_equal(part, O.occgrid_times(levels, R, roi, 11, 32, 1, cell_begin=1000, cell_count=777))
+    rng = np.random.default_rng(12)
+    a, b = rng.uniform(0, 1, 1001).astype(np.float32), rng.uniform(0, 1, 1001).astype(np.float32)
+    da = cuda(a.copy())
+    N.max_merge(da, cuda(b))
+    assert np.array_equal(da.cpu().numpy(), np.maximum(a, b))
+    # a moving sphere, K = 6 draws, one update at step 0
+    K = 6
+
+    def sphere(x, t):
+        c = torch.stack([0.3 + 0.4 * t, torch.full_like(t, 0.5), torch.full_like(t, 0.5)], 1)
+        return ((x - c).norm(dim=1) < 0.2).float() * 3.0
+
+    g.update_every_n_steps(0, sphere, n=16, jitter=True, time_draws=K)
+    torch.cuda.synchronize()
+    xyz = O.occgrid_points(levels, R, roi, 11, 0, 1).astype(np.float64)
+    fresh = None
+    for j in range(K):
+        t = O.occgrid_times(levels, R, roi, 11, 0, j).astype(np.float32)
+        c = np.stack([np.float32(0.3) + np.float32(0.4) * t, np.full_like(t, 0.5), np.full_like(t, 0.5)], 1)
+        v = np.where(np.linalg.norm(xyz.astype(np.float32) - c, axis=1) < 0.2, 3.0, 0.0).astype(np.float32)
+        fresh = v if fresh is None else np.maximum(fresh, v)
+    dens, bits, _ = O.occgrid_update(levels, R, roi, np.zeros(spec.n_cells, np.float32), fresh, decay=0.9,
+                                     threshold=0.1)
+    # cells whose distance to a drawn centre is within fp32 rounding of 0.2 may differ between
+    # the torch (GPU) and numpy distance evaluations of the caller's field: compare the rest
+    got = np.unpackbits(g.bits.cpu().numpy().view(np.uint8), bitorder="little")[: spec.n_cells]
+    assert got.sum() > 50 and np.mean(got == bits) > 0.995
+    assert np.mean((g.density.cpu().numpy() > 0) == (dens > 0)) > 0.995
