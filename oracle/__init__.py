@@ -334,6 +334,25 @@ def importance_cdf(s_edges, *, sigma=None, cdf=None, map_kind=1, t_near=0.2, t_f
     return F
 
 
+def pdf_loss(t, w, th, wh, eps=1e-7):
+    """Proposal supervision loss per ray (reading #21): t [n, nf+1], w [n, nf], th [n, np+1], wh [n, np]."""
+    t, w, th, wh = (np.ascontiguousarray(x, np.float64) for x in (t, w, th, wh))
+    n, nf, np_ = t.shape[0], w.shape[1], wh.shape[1]
+    loss = np.zeros(n)
+    lib().or_pdf_loss(C.c_int64(n), C.c_int32(nf), _p(t), _p(w), C.c_int32(np_), _p(th), _p(wh), C.c_double(eps),
+                      _p(loss))
+    return loss
+
+
+def pdf_loss_bwd(t, w, th, wh, g_loss, eps=1e-7):
+    t, w, th, wh = (np.ascontiguousarray(x, np.float64) for x in (t, w, th, wh))
+    n, nf, np_ = t.shape[0], w.shape[1], wh.shape[1]
+    g = np.zeros((n, np_))
+    lib().or_pdf_loss_bwd(C.c_int64(n), C.c_int32(nf), _p(t), _p(w), C.c_int32(np_), _p(th), _p(wh),
+                          C.c_double(eps), _p(_f64(g_loss)), _p(g))
+    return g
+
+
 # --------------------------------------------------------------------------- grid update
 def occgrid_points(levels, res, roi, seed, step, jitter, cell_begin=0, cell_count=None):
     g = _grid(levels, res, roi)

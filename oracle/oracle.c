@@ -680,6 +680,48 @@ void or_ray_bounds(const or_grid *g, const uint8_t *occ, const or_march *p, cons
 }
 
 /* ------------------------------------------------------------------------ */
+/* Proposal supervision loss (reading #21 [ext]): the definition, O(nf·np).   */
+/* ------------------------------------------------------------------------ */
+static double pdf_bound(int32_t np, const double *th, const double *wh, double a, double b) {
+  double B = 0.0;
+  for (int32_t j = 0; j < np; ++j)
+    if (th[j] < b && th[j + 1] > a) B += wh[j];
+  return B;
+}
+
+void or_pdf_loss(int64_t n_rays, int32_t nf, const double *t, const double *w, int32_t np,
+                 const double *th, const double *wh, double eps, double *loss) {
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t r = 0; r < n_rays; ++r) {
+    const double *tr = t + r * (nf + 1), *wr = w + r * nf, *hr = th + r * (np + 1), *vr = wh + r * np;
+    double L = 0.0;
+    for (int32_t i = 0; i < nf; ++i) {
+      double res = wr[i] - pdf_bound(np, hr, vr, tr[i], tr[i + 1]);
+      if (res > 0.0) L += res * res / (wr[i] + eps);
+    }
+    loss[r] = L;
+  }
+}
+
+void or_pdf_loss_bwd(int64_t n_rays, int32_t nf, const double *t, const double *w, int32_t np,
+                     const double *th, const double *wh, double eps, const double *g_loss,
+                     double *g_wh) {
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t r = 0; r < n_rays; ++r) {
+    const double *tr = t + r * (nf + 1), *wr = w + r * nf, *hr = th + r * (np + 1), *vr = wh + r * np;
+    double *gr = g_wh + r * np;
+    for (int32_t j = 0; j < np; ++j) gr[j] = 0.0;
+    for (int32_t i = 0; i < nf; ++i) {
+      double res = wr[i] - pdf_bound(np, hr, vr, tr[i], tr[i + 1]);
+      if (!(res > 0.0)) continue;
+      double c = -2.0 * g_loss[r] * res / (wr[i] + eps);
+      for (int32_t j = 0; j < np; ++j)
+        if (hr[j] < tr[i + 1] && hr[j + 1] > tr[i]) gr[j] += c;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------ */
 /* O9: occupancy-grid estimator update (P:240-241 EMA and threshold;          */
 /* S:251-268; readings #20-#23).                                             */
 /* ------------------------------------------------------------------------ */

@@ -33,6 +33,7 @@
  *                         scalar sampler / march, slab closed form, culling)
  *   or_occgrid_*          pinned
  *   or_occgrid_times      pinned (Philox KAT via or_philox4x32_10, u24 grid, uniformity)
+ *   or_pdf_loss(_bwd)     pinned (self-bound zero, single-bin closed form, coarsening bound, FD)
  */
 #ifndef NACC_ORACLE_H
 #define NACC_ORACLE_H
@@ -172,6 +173,20 @@ void or_ray_bounds(const or_grid *g, const uint8_t *occ, const or_march *p, cons
 /* the normalised CDF F̂ the sampler inverts (for backward-error checks) */
 void or_importance_cdf(int64_t n_rays, int32_t n_in, const double *s_edges, const double *sigma,
                        const double *cdf, int map, double t_near, double t_far, double *cdf_hat);
+
+/* Proposal supervision (the paper names Mip-NeRF 360's
+ * "PDF matching loss" that trains the proposal network; its form is
+ * [ext], reading #21).  Dense per-ray histograms: final edges t
+ * [n][nf+1] with weights w [n][nf]; proposal edges th [n][np+1] with weights
+ * wh [n][np].  B_i = Σ_j wh_j over the proposal intervals overlapping
+ * (t_i, t_{i+1}) (th_j < t_{i+1} and th_{j+1} > t_i); loss_r = Σ_i
+ * max(0, w_i − B_i)² / (w_i + eps).  The backward returns g_wh only (w is a
+ * stop-gradient target): g_wh_j = −2 g_loss_r Σ_{i overlapping j} max(0, w_i − B_i) / (w_i + eps). */
+void or_pdf_loss(int64_t n_rays, int32_t nf, const double *t, const double *w, int32_t np,
+                 const double *th, const double *wh, double eps, double *loss);
+void or_pdf_loss_bwd(int64_t n_rays, int32_t nf, const double *t, const double *w, int32_t np,
+                     const double *th, const double *wh, double eps, const double *g_loss,
+                     double *g_wh);
 
 /* O9 occupancy-grid update (readings #20-23).
  * Points: x = lo_l + (i + ξ)(hi_l - lo_l)/R with ξ from Philox(seed, (i_cell, step, l, 0)),
