@@ -257,6 +257,22 @@ nacc_status nacc_occgrid_ray_bounds(const nacc_grid *grid, const uint32_t *bits,
                                    int64_t n_rays, float *t_near, float *t_far, uint64_t *n_alive,
                                    void *ws, size_t ws_bytes, cudaStream_t stream);
 
+/* Proposal supervision (the "PDF matching loss" that trains the proposal
+ * network; form [ext] Mip-NeRF 360, reading #21).  Dense
+ * per-ray histograms, edges ascending per ray:
+ *   t [n_rays][nf+1], w [n_rays][nf]      final intervals and weights
+ *   th [n_rays][np+1], wh [n_rays][np]    proposal intervals and weights
+ *   B_i = Σ wh_j over proposal intervals overlapping (t_i, t_{i+1})
+ *   loss[r] = Σ_i max(0, w_i − B_i)² / (w_i + eps)       (f32 out, fp64 inside)
+ * The backward treats w as a constant target and writes g_wh [n_rays][np]
+ * from g_loss [n_rays].  nf, np >= 1; eps > 0. */
+nacc_status nacc_pdf_loss(int64_t n_rays, int32_t nf, const float *t, const float *w, int32_t np,
+                          const float *th, const float *wh, double eps, float *loss,
+                          cudaStream_t stream);
+nacc_status nacc_pdf_loss_bwd(int64_t n_rays, int32_t nf, const float *t, const float *w,
+                              int32_t np, const float *th, const float *wh, double eps,
+                              const float *g_loss, float *g_wh, cudaStream_t stream);
+
 /* ------------------------------------------------------------------------ */
 /* Proposal estimator: inverse-transform resampling (Eq. 1) of the  */
 /* CDF F = 1 - T (Eq. 3, "compute the CDF directly using 1 - T(t)", */

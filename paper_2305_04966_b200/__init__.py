@@ -15,6 +15,7 @@ from .api import (  # noqa: F401
     importance_sample,
     occgrid_ray_bounds,
     max_merge,
+    pdf_loss,
     launch_count,
     neg_log_eps,
     owner_slab,

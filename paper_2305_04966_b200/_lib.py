@@ -71,6 +71,8 @@ SIGNATURES = {
     "nacc_render_bwd_workspace_bytes": (SZ, [I64]),
     "nacc_importance_sample": (C.c_int, [I64, I32, P, P, P, C.c_int, D, D, I32, I32, U64, P, P, P]),
     "nacc_importance_sample_ranged": (C.c_int, [I64, I32, P, P, P, C.c_int, P, P, I32, I32, U64, P, P, P]),
+    "nacc_pdf_loss": (C.c_int, [I64, I32, P, P, I32, P, P, D, P, P]),
+    "nacc_pdf_loss_bwd": (C.c_int, [I64, I32, P, P, I32, P, P, D, P, P, P]),
     "nacc_occgrid_ray_bounds": (C.c_int, [GP, P, MP, P, P, P, P, I64, P, P, P, P, SZ, P]),
     "nacc_occgrid_times": (C.c_int, [GP, U64, I64, I32, I64, I64, P, P]),
     "nacc_max_merge": (C.c_int, [P, P, I64, P]),

@@ -420,6 +420,41 @@ def importance_sample(s_edges: torch.Tensor, n_out: int, sigma: Optional[torch.T
     return s_out, t_out
 
 
+class _PdfLossFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, t, w, th, wh, eps):
+        n, nf1 = t.shape
+        np1 = th.shape[1]
+        loss = torch.empty(n, dtype=torch.float32, device=t.device)
+        check(L.lib().nacc_pdf_loss(n, nf1 - 1, _ptr(t), _ptr(w), np1 - 1, _ptr(th), _ptr(wh), float(eps), _ptr(loss),
+                                    _stream()), "nacc_pdf_loss")
+        ctx.save_for_backward(t, w, th, wh)
+        ctx.eps = eps
+        return loss
+
+    @staticmethod
+    def backward(ctx, g_loss):
+        t, w, th, wh = ctx.saved_tensors
+        n, nf1 = t.shape
+        np1 = th.shape[1]
+        g = torch.empty_like(wh)
+        g_loss = g_loss.contiguous().float()
+        check(L.lib().nacc_pdf_loss_bwd(n, nf1 - 1, _ptr(t), _ptr(w), np1 - 1, _ptr(th), _ptr(wh), float(ctx.eps),
+                                        _ptr(g_loss), _ptr(g), _stream()), "nacc_pdf_loss_bwd")
+        return None, None, None, g, None
+
+
+def pdf_loss(t: torch.Tensor, w: torch.Tensor, t_prop: torch.Tensor, w_prop: torch.Tensor, eps: float = 1e-7):
+    """Proposal supervision (PDF-matching / histogram-bound loss, reading #21):
+    per-ray loss [n]; differentiable w.r.t. the proposal weights only."""
+    n = t.shape[0]
+    t = _req(t.detach(), torch.float32, "t")
+    w = _req(w.detach(), torch.float32, "w", n * (t.shape[1] - 1))
+    th = _req(t_prop.detach(), torch.float32, "t_prop")
+    wh = _req(w_prop, torch.float32, "w_prop", n * (th.shape[1] - 1))
+    return _PdfLossFn.apply(t, w.view(n, -1), th, wh.view(n, -1), float(eps))
+
+
 def occgrid_ray_bounds(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec, bits: torch.Tensor,
                        params: MarchParams, t_min: Optional[torch.Tensor] = None,
                        t_max: Optional[torch.Tensor] = None):

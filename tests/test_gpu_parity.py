@@ -707,3 +707,35 @@ def test_dynamic_grid_times_and_max_merge(N):
     got = np.unpackbits(g.bits.cpu().numpy().view(np.uint8), bitorder="little")[: spec.n_cells]
     assert got.sum() > 50 and np.mean(got == bits) > 0.995
     assert np.mean((g.density.cpu().numpy() > 0) == (dens > 0)) > 0.995
+
+
+def test_pdf_loss(N):
+    """Reading #21: proposal-supervision loss and its backward vs the oracle on
+    CFG4-shaped histograms (48 final vs 96 / 256 proposal bins) incl. shared
+    edges and violated bounds."""
+    import torch
+
+    rng = np.random.default_rng(61)
+    n = 4096
+    for nf, np_ in ((48, 96), (48, 256), (32, 8)):
+        t = np.sort(rng.uniform(0, 1, (n, nf + 1)), axis=1).astype(np.float32)
+        t[:, 0], t[:, -1] = 0, 1
+        w = (rng.dirichlet(np.ones(nf), n) * rng.uniform(0.3, 1, (n, 1))).astype(np.float32)
+        th = np.sort(rng.uniform(0, 1, (n, np_ + 1)), axis=1).astype(np.float32)
+        th[:, 0], th[:, -1] = 0, 1
+        k = min(nf, np_) // 2  # rows 0..9 share k final edges (boundary ties), still ascending
+        th[:10] = np.sort(np.concatenate([t[:10, 1 : k + 1], rng.uniform(0, 1, (10, np_ + 1 - k))], 1), axis=1)
+        th[:10, 0], th[:10, -1] = 0, 1
+        wh = (rng.dirichlet(np.ones(np_), n) * rng.uniform(0.2, 1, (n, 1))).astype(np.float32)
+        whg = cuda(wh).requires_grad_()
+        loss = N.pdf_loss(cuda(t), cuda(w), cuda(th), whg)
+        g = rng.normal(size=n).astype(np.float32)
+        (loss * cuda(g)).sum().backward()
+        torch.cuda.synchronize()
+        ref = O.pdf_loss(t, w, th, wh)
+        gref = O.pdf_loss_bwd(t, w, th, wh, g)
+        assert np.all(np.abs(loss.detach().cpu().numpy() - ref) <= 1e-4 * np.abs(ref) + 1e-7)
+        ga = whg.grad.cpu().numpy()
+        scale = np.abs(gref).max(axis=1, keepdims=True) + 1e-6
+        assert np.all(np.abs(ga - gref) <= 1e-4 * np.abs(gref) + 1e-5 * scale)
+        assert (ref > 0).mean() > 0.5
