@@ -456,6 +456,37 @@ def run_extras(device, reps=20):
     sg32, rgb32 = fld.at_samples(o2, d2, samp32.t0, samp32.t1, rid32)
     ms_rf, (col32, _, _, cx32) = timed(lambda: N.render_fwd(samp32, sg32, rgb32, EPS))
     ms_rb, _ = timed(lambda: N.render_bwd(samp32, sg32, rgb32, cx32, g_all, None, None, EPS))
+    # ---- alpha path (SDF-style fields) on the kept CFG2 samples, and the proposal-supervision
+    # loss on CFG4-shaped histograms (48 final vs 96 proposal bins, 2^16 rays)
+    n_kept = int(f_kept.total.item())
+    pk_k = N.PackedSamples(f_kept.packed_info, f_kept.t0[:n_kept], f_kept.t1[:n_kept], f_kept.ray_id[:n_kept])
+    alph = (-torch.expm1(-sg_k[:n_kept] * (pk_k.t1 - pk_k.t0))).contiguous()
+    alph_g = alph.clone().requires_grad_()
+    gw_a = torch.randn_like(alph)
+
+    def alpha_fwd_bwd():
+        w_a, _ = N.render_weights_alpha(pk_k, alph_g, eps=EPS)
+        (w_a * gw_a).sum().backward()
+        return w_a
+
+    ms_al, _ = timed(alpha_fwd_bwd)
+    tf48 = torch.sort(torch.rand(n4, 49, device=device), dim=1).values.contiguous()
+    w48 = torch.rand(n4, 48, device=device)
+    w48 = (w48 / w48.sum(1, keepdim=True)).contiguous()
+    tp96 = torch.sort(torch.rand(n4, 97, device=device), dim=1).values.contiguous()
+    wp96 = torch.rand(n4, 96, device=device)
+    wp96 = (0.7 * wp96 / wp96.sum(1, keepdim=True)).contiguous().requires_grad_()
+
+    def pdf_fwd_bwd():
+        lp = N.pdf_loss(tf48, w48, tp96, wp96)
+        lp.sum().backward()
+        return lp
+
+    ms_pdf, _ = timed(pdf_fwd_bwd)
+    out["alpha_path"] = {"samples": n_kept, "weights_alpha_fwd_bwd_ms": ms_al,
+                         "samples_per_s": n_kept / (ms_al / 1e3), "note": "includes autograd glue"}
+    out["pdf_loss"] = {"rays": n4, "final_bins": 48, "proposal_bins": 96, "fwd_bwd_ms": ms_pdf,
+                       "rays_per_s": n4 / (ms_pdf / 1e3), "note": "includes autograd glue"}
     n_alive = int(alive2.item())
     out["combined_estimator_P120"] = {
         "rays": n2, "rays_alive_after_grid": n_alive, "culled_fraction": 1.0 - n_alive / n2,
