@@ -70,3 +70,46 @@ def test_owner_slabs_partition_cells():
             slabs = [owner_slab(n, r, world) for r in range(world)]
             assert slabs[0][0] == 0 and slabs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+
+
+def _worker_dynamic(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle as O
+    from paper_2305_04966_b200.api import merge_fresh, owner_slab
+
+    levels, res, roi, K = 1, 16, (0, 0, 0, 1, 1, 1), 5
+    n = levels * res**3
+    lo, hi = owner_slab(n, rank, world)
+    xyz = O.occgrid_points(levels, res, roi, seed=9, step=0, jitter=1, cell_begin=lo, cell_count=hi - lo)
+    slab = None
+    for j in range(K):  # dynamic scene (reading #20): max over time draws, then the cross-rank MAX
+        t = O.occgrid_times(levels, res, roi, 9, 0, j, cell_begin=lo, cell_count=hi - lo).astype(np.float64)
+        c = np.stack([0.3 + 0.4 * t, np.full_like(t, 0.5), np.full_like(t, 0.5)], 1)
+        v = np.where(np.linalg.norm(xyz - c, axis=1) < 0.2, 2.0, 0.0).astype(np.float32)
+        slab = v if slab is None else np.maximum(slab, v)
+    fresh = merge_fresh(torch.from_numpy(slab), lo, hi, n).numpy()
+    np.save(os.path.join(out_dir, f"dyn{rank}.npy"), fresh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_dynamic_grid_merge_gloo(tmp_path):
+    """Time draws merged by MAX on each rank's slab, then the cross-rank MAX:
+    identical on both ranks and equal to the one-rank max over the draws."""
+    port = _free_port()
+    mp.spawn(_worker_dynamic, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    a, b = np.load(tmp_path / "dyn0.npy"), np.load(tmp_path / "dyn1.npy")
+    assert np.array_equal(a, b)
+    import oracle as O
+
+    xyz = O.occgrid_points(1, 16, (0, 0, 0, 1, 1, 1), seed=9, step=0, jitter=1)
+    ref = None
+    for j in range(5):
+        t = O.occgrid_times(1, 16, (0, 0, 0, 1, 1, 1), 9, 0, j).astype(np.float64)
+        c = np.stack([0.3 + 0.4 * t, np.full_like(t, 0.5), np.full_like(t, 0.5)], 1)
+        v = np.where(np.linalg.norm(xyz - c, axis=1) < 0.2, 2.0, 0.0).astype(np.float32)
+        ref = v if ref is None else np.maximum(ref, v)
+    assert np.array_equal(a, ref) and ref.max() == 2.0
