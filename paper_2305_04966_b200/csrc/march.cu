@@ -144,12 +144,11 @@ __device__ __forceinline__ bool occupied_interior(const GridConst &g, const uint
                                                   float ox, float oy, float oz, float dx, float dy, float dz) {
   const float x = __fmaf_rn(m, dx, ox), y = __fmaf_rn(m, dy, oy), z = __fmaf_rn(m, dz, oz);
   const int R = g.res;
-  int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[0][0]), g.s[0][0]));
-  int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[0][1]), g.s[0][1]));
-  int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[0][2]), g.s[0][2]));
-  ix = min(max(ix, 0), R - 1);
-  iy = min(max(iy, 0), R - 1);
-  iz = min(max(iz, 0), R - 1);
+  // inside the box by >= 4e-3 cells (segment_test's margin, far above the fp32
+  // error of u), so floor(u) is already in [0, R-1]: the clamp is the identity
+  const int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[0][0]), g.s[0][0]));
+  const int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[0][1]), g.s[0][1]));
+  const int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[0][2]), g.s[0][2]));
   const uint32_t q = (uint32_t)ix + (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
   return (__ldg(bits + (q >> 5)) >> (q & 31u)) & 1u;
 }
@@ -490,7 +489,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
                                              [&](unsigned b, bool pred, int k, int32_t cnt) {
                                                const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
                                                const int off = k - kb0;
-                                               if (pred && q < kCap && off < 65536) kl[q] = (uint16_t)off;
+                                               if (pred && q < kCap) kl[q] = (uint16_t)off;  // an out-of-range ray is discarded below
                                              });
         // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
         // (an unusable list leaves its space to the tile's next rays; the ray is traversed again)
