@@ -16,6 +16,9 @@
 #include "common.cuh"
 #include "lookback.cuh"
 
+#ifndef NACC_MARCH_FLATW
+#define NACC_MARCH_FLATW 0  // build parameter: write a tile's samples as one run (vs ray by ray)
+#endif
 #ifndef NACC_MARCH_PREFETCH
 #define NACC_MARCH_PREFETCH 0  // build parameter: L1 prefetch of interior segments' bit words
 #endif
@@ -535,7 +538,33 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
       const int64_t my_run = excl + prev.incl - prev.c;
       if (lane < kRpt && r_base + lane < n_rays)
         reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(my_run, prev.c);
-      if (t0 != nullptr && excl + prev.agg <= capacity) {
+      // every list usable: the tile's lists are contiguous in k-list order = output order, so
+      // the warp writes the whole tile as one coalesced run (ray of item i by comparing i with
+      // the rays' inclusive counts)
+      const bool flat = NACC_MARCH_FLATW && __all_sync(kFull, lane >= kRpt || prev.c == 0 || prev.lpos >= 0);
+      if (t0 != nullptr && excl + prev.agg <= capacity && flat) {
+        long long inc[kRpt];
+#pragma unroll
+        for (int jj = 0; jj < kRpt; ++jj) inc[jj] = __shfl_sync(kFull, prev.incl, jj);
+        const uint16_t *kl = kbuf[warp][pb];
+        for (int base = 0; base < (int)prev.agg; base += 32) {  // warp-uniform trip count
+          const int i = base + lane;
+          int j = 0;
+#pragma unroll
+          for (int jj = 0; jj < kRpt; ++jj) j += inc[jj] <= (long long)i;
+          j = min(j, kRpt - 1);
+          const int kb = __shfl_sync(kFull, prev.kb, j);
+          if (i < (int)prev.agg) {
+            const float nr = s_setup[warp][pb][j].near_r;
+            const int k = kb + (int)kl[i];
+            float ta, tb;
+            lattice_ends<kCone>(p, nr, tab, k, ta, tb);
+            t0[excl + i] = ta;
+            t1[excl + i] = tb;
+            ray_id[excl + i] = (int32_t)(r_base + j);
+          }
+        }
+      } else if (t0 != nullptr && excl + prev.agg <= capacity) {
 #pragma unroll 1
         for (int j = 0; j < kRpt; ++j) {
           const int64_t r = r_base + j;

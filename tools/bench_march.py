@@ -10,16 +10,20 @@ import workloads as W
 import paper_2305_04966_b200 as N
 
 
-def timed(fn, n=20):
+def timed(fn, n=40, batches=7):
+    """median over batches of the mean per-call device time (ms)"""
     fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(n):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / n
+    res = []
+    for _ in range(batches):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        res.append(e0.elapsed_time(e1) / n)
+    return float(np.median(res))
 
 
 for name, c in (("cfg2", W.cfg2()), ("cfg3", W.cfg3())):
