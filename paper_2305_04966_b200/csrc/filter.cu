@@ -13,24 +13,19 @@ namespace nacc {
 // kept prefix plus a few samples are read.  Each block also reduces its cuts.
 constexpr int kFiltRays = 256;
 
-__device__ __forceinline__ int64_t block_sum_i64(int64_t v, int64_t *sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum_i64(v);
-  if (lane == 0) sm[warp] = v;
-  __syncthreads();
-  int64_t tot = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += sm[w];
-  return tot;
-}
 
-__global__ void __launch_bounds__(kFiltRays) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
-                                                               const float *__restrict__ t0,
-                                                               const float *__restrict__ t1,
-                                                               const float *__restrict__ sigma, double L,
-                                                               int32_t *__restrict__ cut_out,
-                                                               int64_t *__restrict__ block_sums) {
-  __shared__ int64_t sm[kFiltRays / 32];
-  const int64_t r = (int64_t)blockIdx.x * kFiltRays + threadIdx.x;
+// Small blocks (two warps) and per-warp atomic adds into the 256-ray group
+// sums: rays of very different lengths no longer hold a 256-thread block (and
+// its resources) at a barrier until the longest one is done.
+constexpr int kCutThreads = 64;
+
+__global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
+                                                                 const float *__restrict__ t0,
+                                                                 const float *__restrict__ t1,
+                                                                 const float *__restrict__ sigma, double L,
+                                                                 int32_t *__restrict__ cut_out,
+                                                                 int64_t *__restrict__ block_sums) {
+  const int64_t r = (int64_t)blockIdx.x * kCutThreads + threadIdx.x;
   int64_t cut = 0;
   if (r < n_rays) {
     const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
@@ -62,8 +57,10 @@ __global__ void __launch_bounds__(kFiltRays) filter_cut_kernel(const int64_t *__
     }
     cut_out[r] = (int32_t)cut;
   }
-  const int64_t tot = block_sum_i64(cut, sm);
-  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
+  const int64_t tot = warp_sum_i64(cut);
+  const int64_t r_warp = r - (threadIdx.x & 31);
+  if ((threadIdx.x & 31) == 0 && tot)
+    atomicAdd(reinterpret_cast<unsigned long long *>(block_sums + r_warp / kFiltRays), (unsigned long long)tot);
 }
 
 // Pass 2 (one block): exclusive scan of the block sums in place; *total.
@@ -100,7 +97,7 @@ __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
     const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
     const float *__restrict__ t1, const int32_t *__restrict__ cuts, const int64_t *__restrict__ block_off,
     const int64_t *__restrict__ total, int64_t capacity, int64_t *__restrict__ packed_out,
-    float *__restrict__ t0_out, float *__restrict__ t1_out, int32_t *__restrict__ ray_id_out) {
+    float *__restrict__ t0_out, float *__restrict__ t1_out, int32_t *__restrict__ ray_id_out, int vec) {
   __shared__ int64_t s_out[kFiltRays + 1];
   __shared__ int64_t s_in[kFiltRays];
   __shared__ int64_t s_w[kFiltRays / 32];
@@ -123,17 +120,46 @@ __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
   __syncthreads();
   if (t0_out == nullptr || *total > capacity) return;
   const int64_t p0 = s_out[0], p1 = s_out[nr];
-  for (int64_t p = p0 + t; p < p1; p += kFiltRays) {
-    int lo = 0, hi = nr - 1;  // largest k with s_out[k] <= p
+  // four consecutive outputs per thread: one binary search, then a forward walk; the
+  // stores of a full aligned quad are float4 / int4
+  for (int64_t p4 = (p0 & ~(int64_t)3) + 4 * (int64_t)t; p4 < p1; p4 += 4 * kFiltRays) {
+    const int64_t pa = p4 > p0 ? p4 : p0;
+    int lo = 0, hi = nr - 1;  // largest k with s_out[k] <= pa
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (s_out[mid] <= p) lo = mid;
+      if (s_out[mid] <= pa) lo = mid;
       else hi = mid - 1;
     }
-    const int64_t src = s_in[lo] + (p - s_out[lo]);
-    t0_out[p] = __ldg(t0 + src);
-    t1_out[p] = __ldg(t1 + src);
-    ray_id_out[p] = (int32_t)(r0 + lo);
+    float a[4], b[4];
+    int32_t id[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t p = p4 + j;
+      a[j] = b[j] = 0.f;
+      id[j] = 0;
+      if (p >= p0 && p < p1) {
+        while (lo + 1 < nr && s_out[lo + 1] <= p) ++lo;
+        const int64_t src = s_in[lo] + (p - s_out[lo]);
+        a[j] = __ldg(t0 + src);
+        b[j] = __ldg(t1 + src);
+        id[j] = (int32_t)(r0 + lo);
+      }
+    }
+    if (vec && p4 >= p0 && p4 + 3 < p1) {
+      *reinterpret_cast<float4 *>(t0_out + p4) = make_float4(a[0], a[1], a[2], a[3]);
+      *reinterpret_cast<float4 *>(t1_out + p4) = make_float4(b[0], b[1], b[2], b[3]);
+      *reinterpret_cast<int4 *>(ray_id_out + p4) = make_int4(id[0], id[1], id[2], id[3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t p = p4 + j;
+        if (p >= p0 && p < p1) {
+          t0_out[p] = a[j];
+          t1_out[p] = b[j];
+          ray_id_out[p] = id[j];
+        }
+      }
+    }
   }
 }
 
@@ -180,12 +206,15 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   int64_t *bsums;
   filter_ws_layout(n_rays, &cuts, &bsums, ws);
   const int64_t nb = ceil_div(n_rays, kFiltRays);
-  filter_cut_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts,
-                                                             bsums);
+  NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)nb, stream));
+  filter_cut_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
+      packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts, bsums);
   block_sums_scan_kernel<<<1, 1024, 0, stream>>>(bsums, nb, total);
   filter_copy_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, cuts, bsums, total, capacity,
                                                              packed_info_out, capacity > 0 ? t0_out : nullptr, t1_out,
-                                                             ray_id_out);
+                                                             ray_id_out,
+                                                             aligned(t0_out, 16) && aligned(t1_out, 16) &&
+                                                                 aligned(ray_id_out, 16));
   count_launch(2);
   count_launch(1);
   NACC_CHECK_LAUNCH();
