@@ -397,23 +397,23 @@ __global__ void __launch_bounds__(256, 3) render_fwd_warp_kernel(
     const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
     float *__restrict__ depth, double *__restrict__ ctx) {
   const int lane = threadIdx.x & 31;
-  const int64_t wt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (wt >= n_wtiles) {  // rays without samples
-    for (int64_t r = (wt - n_wtiles) * 32 + lane; r < n_rays; r += 1ll << 62) {
-      if (packed_info[2 * r + 1] == 0) {
-        if (color) { color[3 * r] = 0.f; color[3 * r + 1] = 0.f; color[3 * r + 2] = 0.f; }
-        if (opacity) opacity[r] = 0.f;
-        if (depth) depth[r] = 0.f;
-        if (ctx) for (int k = 0; k < 5; ++k) ctx[5 * r + k] = 0.0;
-      }
-      break;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw * 32 + lane; r < n_rays; r += nw * 32) {  // rays without samples
+    if (packed_info[2 * r + 1] == 0) {
+      if (color) { color[3 * r] = 0.f; color[3 * r + 1] = 0.f; color[3 * r + 2] = 0.f; }
+      if (opacity) opacity[r] = 0.f;
+      if (depth) depth[r] = 0.f;
+      if (ctx) for (int k = 0; k < 5; ++k) ctx[5 * r + k] = 0.0;
     }
-    return;
   }
+  // persistent warps stride over the tiles in use (N from packed_info: the launch is sized by
+  // the resident capacity, not by the arrays' capacity)
   const int64_t N = packed_end(packed_info, n_rays);
+  for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
   const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
   const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
-  if (B >= E) return;
+  if (B >= E) continue;
   Seg<1> carryS = seg_identity<1>();
   SegM carryC = segm_identity();
   int32_t carry_rid = -1;
@@ -446,6 +446,20 @@ __global__ void __launch_bounds__(256, 3) render_fwd_warp_kernel(
     const SegM enter = warp_segm_excl(cur, carryC);
     if (lead_r >= 0) render_fwd_out(segm_combine(enter, lead), lead_r, color, opacity, depth, ctx);
   }
+  }
+}
+
+// persistent grid for the tile kernels: all resident at once (3 blocks of 256 per SM)
+static unsigned resident_blocks(int64_t want) {
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 1;
+  }
+  const int64_t cap = (int64_t)n_sm * 3;
+  return (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
 struct RayGrad {
@@ -495,12 +509,13 @@ __global__ void __launch_bounds__(256, 3) render_bwd_warp_kernel(
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, const float4 *__restrict__ gcv, const double2 *__restrict__ gq,
     float *__restrict__ g_sigma, float *__restrict__ g_rgb) {
-  const int64_t wt = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (wt >= n_wtiles) return;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t N = packed_end(packed_info, n_rays);
+  for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
   const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
   const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
-  if (B >= E) return;
+  if (B >= E) continue;
   Seg<1> carryS = seg_identity<1>(), carryP = seg_identity<1>();
   int32_t carry_rid = -1;
   for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
@@ -573,6 +588,7 @@ __global__ void __launch_bounds__(256, 3) render_bwd_warp_kernel(
           for (int ch = 0; ch < 3; ++ch) g_rgb[3 * (it.q0 + j) + ch] = gr[3 * j + ch];
       }
     }
+  }
   }
 }
 
@@ -830,10 +846,10 @@ nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, i
   NACC_REQUIRE(!ctx || aligned(ctx, 8), "ctx must be 8-byte aligned");
   if (ray_id && rgb) {
     const int64_t n_wtiles = ceil_div(n_samples, kWarpTile);
-    const int64_t warps = n_wtiles + ceil_div(n_rays, 32);
+    const int64_t warps = n_wtiles > ceil_div(n_rays, 32) ? n_wtiles : ceil_div(n_rays, 32);
     const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(rgb, 16) &&
                      aligned(ray_id, 16);
-    const unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
+    const unsigned blocks = resident_blocks(ceil_div(warps * 32, 256));
     if (vec)
       render_fwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
                                                                rgb, neg_log_eps, color, opacity, depth, ctx);
@@ -868,7 +884,7 @@ nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, i
     const int64_t n_wtiles = ceil_div(n_samples, kWarpTile);
     const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(rgb, 16) &&
                      aligned(ray_id, 16) && aligned(g_sigma, 16) && (!g_rgb || aligned(g_rgb, 16));
-    const unsigned blocks = (unsigned)ceil_div(n_wtiles * 32, 256);
+    const unsigned blocks = resident_blocks(ceil_div(n_wtiles * 32, 256));
     if (vec)
       render_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
                                                                rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb);
