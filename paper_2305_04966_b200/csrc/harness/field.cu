@@ -168,19 +168,20 @@ __global__ void field_samples_kernel(const float4 *__restrict__ lat, int R, floa
                                      const float *__restrict__ t0, const float *__restrict__ t1,
                                      const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
                                      float *__restrict__ sigma, float *__restrict__ rgb) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n || (n_dev && i >= *n_dev)) return;
-  const int64_t r = __ldg(rid + i);
-  const float m = 0.5f * (__ldg(t0 + i) + __ldg(t1 + i));
-  const float x = __ldg(o + 3 * r) + m * __ldg(d + 3 * r);
-  const float y = __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1);
-  const float z = __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2);
-  const float4 v = lattice_at(lat, R, lo, hi, contracted, x, y, z);
-  sigma[i] = v.x;
-  if (rgb) {
-    rgb[3 * i] = v.y;
-    rgb[3 * i + 1] = v.z;
-    rgb[3 * i + 2] = v.w;
+  const int64_t nn = n_dev ? min(n, *n_dev) : n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nn; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = __ldg(rid + i);
+    const float m = 0.5f * (__ldg(t0 + i) + __ldg(t1 + i));
+    const float x = __ldg(o + 3 * r) + m * __ldg(d + 3 * r);
+    const float y = __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1);
+    const float z = __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2);
+    const float4 v = lattice_at(lat, R, lo, hi, contracted, x, y, z);
+    sigma[i] = v.x;
+    if (rgb) {
+      rgb[3 * i] = v.y;
+      rgb[3 * i + 1] = v.z;
+      rgb[3 * i + 2] = v.w;
+    }
   }
 }
 
@@ -199,6 +200,18 @@ __global__ void mse_grad_kernel(const float *__restrict__ c, const float *__rest
 }
 
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + 255) / 256); }
+// grid-stride kernels driven by a device count: cap the launch at a few waves
+inline unsigned blocks_capped(int64_t n) {
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 1;
+  }
+  const int64_t b = (n + 255) / 256, cap = (int64_t)n_sm * 32;
+  return (unsigned)(b < cap ? (b > 0 ? b : 1) : cap);
+}
 }  // namespace
 
 extern "C" {
@@ -210,7 +223,7 @@ nacc_status naccx_field_at_samples(const float *lattice, int32_t res, float lo, 
   if (n < 0 || res < 2 || !(hi > lo)) return NACC_ERR_INVALID_ARGUMENT;
   if (n == 0) return NACC_OK;
   if (!lattice || !rays_o || !rays_d || !t0 || !t1 || !ray_id || !sigma) return NACC_ERR_INVALID_ARGUMENT;
-  field_samples_kernel<<<blocks_for(n), 256, 0, stream>>>(reinterpret_cast<const float4 *>(lattice), res, lo, hi,
+  field_samples_kernel<<<n_dev ? blocks_capped(n) : blocks_for(n), 256, 0, stream>>>(reinterpret_cast<const float4 *>(lattice), res, lo, hi,
                                                           contracted, rays_o, rays_d, t0, t1, ray_id, n, n_dev, sigma,
                                                           rgb);
   g_launches++;
@@ -368,10 +381,10 @@ __global__ void tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, floa
                                   const float *__restrict__ t0, const float *__restrict__ t1,
                                   const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
                                   float *__restrict__ sigma) {
-  const int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t nn = n_dev ? min(n, *n_dev) : n;
-  if (q0 >= nn) return;
   const float sc = (float)R / (hi - lo);
+  for (int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; q0 < nn;
+       q0 += (int64_t)gridDim.x * blockDim.x * 4) {
   float a[4], b[4], out[4];
   int32_t ri[4];
   const bool full = q0 + 3 < nn;
@@ -407,6 +420,7 @@ __global__ void tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, floa
     for (int j = 0; j < 4; ++j)
       if (q0 + j < nn) sigma[q0 + j] = out[j];
   }
+  }
 }
 
 extern "C" nacc_status naccx_tex_at_samples(uint64_t handle, float lo, float hi, int32_t contracted, const float *rays_o,
@@ -420,7 +434,7 @@ extern "C" nacc_status naccx_tex_at_samples(uint64_t handle, float lo, float hi,
                                                                 t0, t1, ray_id, n, n_dev, sigma, rgb);
   else if (((reinterpret_cast<uintptr_t>(t0) | reinterpret_cast<uintptr_t>(t1) | reinterpret_cast<uintptr_t>(ray_id) |
               reinterpret_cast<uintptr_t>(sigma)) & 15) == 0)
-    tex_sigma4_kernel<<<blocks_for((n + 3) / 4), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
+    tex_sigma4_kernel<<<n_dev ? blocks_capped((n + 3) / 4) : blocks_for((n + 3) / 4), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
                                                                     t0, t1, ray_id, n, n_dev, sigma);
   else
     tex_samples_kernel<false><<<blocks_for(n), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
