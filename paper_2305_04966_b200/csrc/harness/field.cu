@@ -404,13 +404,22 @@ __global__ void tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, floa
       ri[j] = in ? __ldg(rid + q0 + j) : 0;
     }
   }
+  float ox = 0.f, oy = 0.f, oz = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int64_t r = ri[j];
+    if (j == 0 || ri[j] != ri[j - 1]) {  // samples are grouped by ray: reload only on a new ray
+      ox = __ldg(o + 3 * r);
+      oy = __ldg(o + 3 * r + 1);
+      oz = __ldg(o + 3 * r + 2);
+      dx = __ldg(d + 3 * r);
+      dy = __ldg(d + 3 * r + 1);
+      dz = __ldg(d + 3 * r + 2);
+    }
     const float m = 0.5f * (a[j] + b[j]);
-    float x = __ldg(o + 3 * r) + m * __ldg(d + 3 * r);
-    float y = __ldg(o + 3 * r + 1) + m * __ldg(d + 3 * r + 1);
-    float z = __ldg(o + 3 * r + 2) + m * __ldg(d + 3 * r + 2);
+    float x = ox + m * dx;
+    float y = oy + m * dy;
+    float z = oz + m * dz;
     const bool in = tex_coord(lo, hi, sc, contracted, x, y, z);
     out[j] = in ? tex3D<float>(tex, x, y, z) : 0.f;
   }
