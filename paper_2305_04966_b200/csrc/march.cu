@@ -98,7 +98,12 @@ __device__ __forceinline__ bool occupied(const GridConst &g, const uint32_t *__r
 // segment's bounding box holds no occupied cell.  Points of the segment lie on
 // the segment AB (monotone lattice), so they share its bounding box; positions
 // use the same fp32 ops as P(k) and a 1e-3 macro-cell margin covers rounding.
-constexpr int kSeg = 8;    // lattice points per segment
+#ifndef NACC_MARCH_SEG
+#define NACC_MARCH_SEG 8
+#endif
+constexpr int kSeg = NACC_MARCH_SEG;  // lattice points per segment (8 or 16; build parameter)
+constexpr int kSegPerPass = 32 / kSeg;  // segments evaluated per 32-lane pass
+static_assert(kSeg == 8 || kSeg == 16, "segment length");
 constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
 constexpr float kSegEps = 1e-3f;
 
@@ -368,12 +373,12 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
       __syncwarp();
       nseg = __popc(F);
     }
-    // lane (lane & 7) of segment list entry idx: its point k and P(k)
+    // lane (lane % kSeg) of segment list entry idx: its point k and P(k)
     auto eval = [&](int idx, int &k) -> bool {
       bool interior = false;
       if (kSkip) {
         const int e = idx < nseg ? seglist[idx] : 0;
-        k = idx < nseg ? k0 + (e & 0xff) * kSeg + (lane & 7) : ke;
+        k = idx < nseg ? k0 + (e & 0xff) * kSeg + (lane % kSeg) : ke;
         interior = kL1 && (e & 0x100);
       } else {
         k = k0 + lane;
@@ -388,11 +393,11 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
       return pred;
     };
     // two passes of 4 segments per iteration (independent chains for ILP), emitted in k order
-    for (int first = 0; first < nseg; first += (kSkip ? 8 : 32)) {
+    for (int first = 0; first < nseg; first += (kSkip ? 2 * kSegPerPass : 32)) {
       int ka, kb2;
-      const bool pa = eval(first + (lane >> 3), ka);
-      if (kSkip && first + 4 < nseg) {
-        const bool pb = eval(first + 4 + (lane >> 3), kb2);
+      const bool pa = eval(first + lane / kSeg, ka);
+      if (kSkip && first + kSegPerPass < nseg) {
+        const bool pb = eval(first + kSegPerPass + lane / kSeg, kb2);
         const unsigned ba = __ballot_sync(kFull, pa);
         emit(ba, pa, ka, cnt);
         cnt += __popc(ba);
