@@ -52,7 +52,11 @@ def _compile(src: str, extra: list[str]) -> str:
 
 
 def _link(objs: list[str], out: str) -> None:
-    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(o) for o in objs):
+    # relink when any object is newer or the object set changed (other build flags)
+    stamp = out + ".objs"
+    listing = "\n".join(objs)
+    same = os.path.exists(stamp) and open(stamp).read() == listing
+    if same and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(o) for o in objs):
         return
     tmp = out + f".tmp{os.getpid()}"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
@@ -60,6 +64,8 @@ def _link(objs: list[str], out: str) -> None:
     if r.returncode != 0:
         raise RuntimeError(f"link failed for {out}:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, out)
+    with open(stamp, "w") as f:
+        f.write(listing)
 
 
 def build(verbose: bool = False, extra: list[str] | None = None) -> tuple[str, str]:

@@ -224,7 +224,13 @@ struct Items {
 // walks them in chunks of 32 lanes x 4 consecutive samples (float4 loads);
 // fp64 warp-level segmented scans (no shared memory, no block barriers) carry
 // the open ray across chunks.  Extra warps zero the outputs of empty rays.
-constexpr int64_t kWarpTile = 256;
+#ifndef NACC_RENDER_TILE
+#define NACC_RENDER_TILE 256
+#endif
+#ifndef NACC_RENDER_BPS
+#define NACC_RENDER_BPS 3
+#endif
+constexpr int64_t kWarpTile = NACC_RENDER_TILE;  // samples per warp tile (build parameter)
 constexpr int kWarpChunk = 128;
 
 template <bool kVec>
@@ -391,7 +397,7 @@ __device__ __forceinline__ void render_fwd_out(const SegM &v, int64_t r, float *
 }
 
 template <bool kVec>
-__global__ void __launch_bounds__(256, 3) render_fwd_warp_kernel(
+__global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
@@ -458,7 +464,7 @@ static unsigned resident_blocks(int64_t want) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm <= 0) n_sm = 1;
   }
-  const int64_t cap = (int64_t)n_sm * 3;
+  const int64_t cap = (int64_t)n_sm * NACC_RENDER_BPS;
   return (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
@@ -504,7 +510,7 @@ __global__ void __launch_bounds__(256) ray_grad_kernel(int64_t n_rays, const dou
 }
 
 template <bool kVec>
-__global__ void __launch_bounds__(256, 3) render_bwd_warp_kernel(
+__global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, const float4 *__restrict__ gcv, const double2 *__restrict__ gq,

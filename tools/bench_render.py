@@ -1,0 +1,41 @@
+"""Time nacc_render_fwd / nacc_render_bwd alone on CFG2 post-filter samples
+(oracle march + filter, harness-free numpy field): median device µs."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import oracle as O
+import workloads as W
+import paper_2305_04966_b200 as N
+
+c = W.cfg2()
+pk, t0, t1, rid = O.march(c.occ, 1, 128, c.roi, c.rays_o, c.rays_d, step=c.step)
+sig, _ = W.field_at_intervals(c.scene.sigma_rgb, c.rays_o, c.rays_d, t0, t1, rid)
+pk2, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, sig, -np.log(np.float32(1e-4)))
+s2, rgb2 = W.field_at_intervals(c.scene.sigma_rgb, c.rays_o, c.rays_d, a0, a1, r2)
+cu = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+S = N.PackedSamples(cu(pk2), cu(a0), cu(a1), cu(r2))
+sg, rgb = cu(s2), cu(rgb2)
+g = torch.randn(len(pk2), 3, device="cuda")
+
+
+def timed(fn, n=40, batches=7):
+    fn()
+    torch.cuda.synchronize()
+    res = []
+    for _ in range(batches):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        res.append(e0.elapsed_time(e1) / n)
+    return float(np.median(res)), out
+
+
+ms_f, (col, _, _, cx) = timed(lambda: N.render_fwd(S, sg, rgb, 1e-4))
+ms_b, _ = timed(lambda: N.render_bwd(S, sg, rgb, cx, g, None, None, 1e-4))
+print(f"samples {len(a0)} render fwd {ms_f * 1e3:.1f} us bwd {ms_b * 1e3:.1f} us")
