@@ -417,41 +417,41 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
   // the resident capacity, not by the arrays' capacity)
   const int64_t N = packed_end(packed_info, n_rays);
   for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
-  const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
-  const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
-  if (B >= E) continue;
-  Seg<1> carryS = seg_identity<1>();
-  SegM carryC = segm_identity();
-  int32_t carry_rid = -1;
-  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
-    Items it;
-    load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
-    double s[4], S[4];
-    warp_items_S(it, s, S, carryS);
-    float col[12];
-    load_rgb4(col, it, rgb, kVec);
-    // One pass over the items: a ray whose head lies in this lane is summed
-    // here and written at its tail; only the lane's leading run (the ray
-    // entering from earlier lanes) waits for the warp scan.
-    SegM cur = segm_identity();  // sums since the lane start or its last head
-    SegM lead;                   // the leading run up to its tail, if that tail is in this lane
-    int64_t lead_r = -1;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool live = it.valid[j] && !(S[j] > L);
-      const double w = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
-      cur = segm_combine(cur, segm_item(it, j, w, col));
-      if (it.tail[j]) {
-        if (cur.f) render_fwd_out(cur, it.rid[j], color, opacity, depth, ctx);
-        else {
-          lead = cur;
-          lead_r = it.rid[j];
+    const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+    const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+    if (B >= E) continue;
+    Seg<1> carryS = seg_identity<1>();
+    SegM carryC = segm_identity();
+    int32_t carry_rid = -1;
+    for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+      Items it;
+      load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
+      double s[4], S[4];
+      warp_items_S(it, s, S, carryS);
+      float col[12];
+      load_rgb4(col, it, rgb, kVec);
+      // One pass over the items: a ray whose head lies in this lane is summed
+      // here and written at its tail; only the lane's leading run (the ray
+      // entering from earlier lanes) waits for the warp scan.
+      SegM cur = segm_identity();  // sums since the lane start or its last head
+      SegM lead;                   // the leading run up to its tail, if that tail is in this lane
+      int64_t lead_r = -1;
+  #pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool live = it.valid[j] && !(S[j] > L);
+        const double w = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
+        cur = segm_combine(cur, segm_item(it, j, w, col));
+        if (it.tail[j]) {
+          if (cur.f) render_fwd_out(cur, it.rid[j], color, opacity, depth, ctx);
+          else {
+            lead = cur;
+            lead_r = it.rid[j];
+          }
         }
       }
+      const SegM enter = warp_segm_excl(cur, carryC);
+      if (lead_r >= 0) render_fwd_out(segm_combine(enter, lead), lead_r, color, opacity, depth, ctx);
     }
-    const SegM enter = warp_segm_excl(cur, carryC);
-    if (lead_r >= 0) render_fwd_out(segm_combine(enter, lead), lead_r, color, opacity, depth, ctx);
-  }
   }
 }
 
@@ -519,82 +519,82 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t N = packed_end(packed_info, n_rays);
   for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
-  const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
-  const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
-  if (B >= E) continue;
-  Seg<1> carryS = seg_identity<1>(), carryP = seg_identity<1>();
-  int32_t carry_rid = -1;
-  for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
-    Items it;
-    load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
-    double s[4], S[4];
-    warp_items_S(it, s, S, carryS);
-    // phase A: per item g_w w (scan input), w and g_w T (1-α); the only state kept
-    double w[4], gwTea[4];
-    unsigned live = 0;
-    Seg<1> agg = seg_identity<1>();
-    {
-      float col[12];
-      load_rgb4(col, it, rgb, kVec);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        w[j] = 0.0;
-        gwTea[j] = 0.0;
-        double v = 0.0;
-        if (it.valid[j] && !(S[j] > L)) {
-          live |= 1u << j;
-          const float4 gc = __ldg(gcv + it.rid[j]);
-          const double2 gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
-          const double T = exp(-S[j]), ea = exp(-s[j]);
-          w[j] = T * (1.0 - ea);
-          const double gw = (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2] +
-                            gon.x + gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-          v = gw * w[j];
-          gwTea[j] = gw * T * ea;
+    const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+    const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+    if (B >= E) continue;
+    Seg<1> carryS = seg_identity<1>(), carryP = seg_identity<1>();
+    int32_t carry_rid = -1;
+    for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+      Items it;
+      load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
+      double s[4], S[4];
+      warp_items_S(it, s, S, carryS);
+      // phase A: per item g_w w (scan input), w and g_w T (1-α); the only state kept
+      double w[4], gwTea[4];
+      unsigned live = 0;
+      Seg<1> agg = seg_identity<1>();
+      {
+        float col[12];
+        load_rgb4(col, it, rgb, kVec);
+  #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          w[j] = 0.0;
+          gwTea[j] = 0.0;
+          double v = 0.0;
+          if (it.valid[j] && !(S[j] > L)) {
+            live |= 1u << j;
+            const float4 gc = __ldg(gcv + it.rid[j]);
+            const double2 gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
+            const double T = exp(-S[j]), ea = exp(-s[j]);
+            w[j] = T * (1.0 - ea);
+            const double gw = (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2] +
+                              gon.x + gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+            v = gw * w[j];
+            gwTea[j] = gw * T * ea;
+          }
+          s[j] = v;
+          Seg<1> x;
+          x.f = it.head[j];
+          x.v[0] = v;
+          agg = seg_combine(agg, x);
         }
-        s[j] = v;
-        Seg<1> x;
-        x.f = it.head[j];
-        x.v[0] = v;
-        agg = seg_combine(agg, x);
       }
-    }
-    Seg<1> run = warp_seg_excl<1>(agg, carryP);
-    float gs[4], gr[12];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + s[j];
-      gs[j] = 0.f;
-      gr[3 * j] = gr[3 * j + 1] = gr[3 * j + 2] = 0.f;
-      if (live & (1u << j)) {
-        const float4 gc = __ldg(gcv + it.rid[j]);
-        const double R = __ldg(gq + 2 * (int64_t)it.rid[j] + 1).x;
-        const double Q = R - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
-        gs[j] = (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q));
-        gr[3 * j] = (float)(w[j] * gc.x);
-        gr[3 * j + 1] = (float)(w[j] * gc.y);
-        gr[3 * j + 2] = (float)(w[j] * gc.z);
-      }
-    }
-    if (kVec && it.valid[0] && it.valid[3]) {
-      *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
-      if (g_rgb) {
-        float4 *pp = reinterpret_cast<float4 *>(g_rgb + 3 * it.q0);
-        pp[0] = make_float4(gr[0], gr[1], gr[2], gr[3]);
-        pp[1] = make_float4(gr[4], gr[5], gr[6], gr[7]);
-        pp[2] = make_float4(gr[8], gr[9], gr[10], gr[11]);
-      }
-    } else {
-#pragma unroll
+      Seg<1> run = warp_seg_excl<1>(agg, carryP);
+      float gs[4], gr[12];
+  #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (!it.valid[j]) continue;
-        g_sigma[it.q0 + j] = gs[j];
-        if (g_rgb)
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) g_rgb[3 * (it.q0 + j) + ch] = gr[3 * j + ch];
+        run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + s[j];
+        gs[j] = 0.f;
+        gr[3 * j] = gr[3 * j + 1] = gr[3 * j + 2] = 0.f;
+        if (live & (1u << j)) {
+          const float4 gc = __ldg(gcv + it.rid[j]);
+          const double R = __ldg(gq + 2 * (int64_t)it.rid[j] + 1).x;
+          const double Q = R - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
+          gs[j] = (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q));
+          gr[3 * j] = (float)(w[j] * gc.x);
+          gr[3 * j + 1] = (float)(w[j] * gc.y);
+          gr[3 * j + 2] = (float)(w[j] * gc.z);
+        }
+      }
+      if (kVec && it.valid[0] && it.valid[3]) {
+        *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
+        if (g_rgb) {
+          float4 *pp = reinterpret_cast<float4 *>(g_rgb + 3 * it.q0);
+          pp[0] = make_float4(gr[0], gr[1], gr[2], gr[3]);
+          pp[1] = make_float4(gr[4], gr[5], gr[6], gr[7]);
+          pp[2] = make_float4(gr[8], gr[9], gr[10], gr[11]);
+        }
+      } else {
+  #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!it.valid[j]) continue;
+          g_sigma[it.q0 + j] = gs[j];
+          if (g_rgb)
+  #pragma unroll
+            for (int ch = 0; ch < 3; ++ch) g_rgb[3 * (it.q0 + j) + ch] = gr[3 * j + ch];
+        }
       }
     }
-  }
   }
 }
 
