@@ -16,6 +16,9 @@
 #include "common.cuh"
 #include "lookback.cuh"
 
+#ifndef NACC_MARCH_MAGICFLOOR
+#define NACC_MARCH_MAGICFLOOR 0  // build parameter: floor by FADD.RZ instead of F2I for interior points
+#endif
 #ifndef NACC_MARCH_FLATW
 #define NACC_MARCH_FLATW 0  // build parameter: write a tile's samples as one run (vs ray by ray)
 #endif
@@ -154,9 +157,17 @@ __device__ __forceinline__ bool occupied_interior(const GridConst &g, const uint
   const int R = g.res;
   // inside the box by >= 4e-3 cells (segment_test's margin, far above the fp32
   // error of u), so floor(u) is already in [0, R-1]: the clamp is the identity
+#if NACC_MARCH_MAGICFLOOR
+  // floor of u in [0, 2^23) without the conversion unit: u + 2^23 rounded toward zero holds
+  // floor(u) in its mantissa (bit-identical to floorf there)
+  const int ix = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(x, g.lo[0][0]), g.s[0][0]), 8388608.0f)) - 0x4B000000;
+  const int iy = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(y, g.lo[0][1]), g.s[0][1]), 8388608.0f)) - 0x4B000000;
+  const int iz = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(z, g.lo[0][2]), g.s[0][2]), 8388608.0f)) - 0x4B000000;
+#else
   const int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[0][0]), g.s[0][0]));
   const int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[0][1]), g.s[0][1]));
   const int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[0][2]), g.s[0][2]));
+#endif
   const uint32_t q = (uint32_t)ix + (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
   return (__ldg(bits + (q >> 5)) >> (q & 31u)) & 1u;
 }
