@@ -376,6 +376,8 @@ __global__ void tex_samples_kernel(cudaTextureObject_t tex, int R, float lo, flo
 
 // density only, 4 consecutive samples per thread (vector loads/stores, four
 // independent texture fetches in flight)
+constexpr int kTexQuads = 1;  // quads of samples per thread and iteration (2 measured slower)
+
 __global__ void tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, float hi, int contracted,
                                   const float *__restrict__ o, const float *__restrict__ d,
                                   const float *__restrict__ t0, const float *__restrict__ t1,
@@ -383,52 +385,59 @@ __global__ void tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, floa
                                   float *__restrict__ sigma) {
   const int64_t nn = n_dev ? min(n, *n_dev) : n;
   const float sc = (float)R / (hi - lo);
-  for (int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; q0 < nn;
-       q0 += (int64_t)gridDim.x * blockDim.x * 4) {
-  float a[4], b[4], out[4];
-  int32_t ri[4];
-  const bool full = q0 + 3 < nn;
-  if (full) {
-    const float4 A = __ldg(reinterpret_cast<const float4 *>(t0 + q0));
-    const float4 Bv = __ldg(reinterpret_cast<const float4 *>(t1 + q0));
-    const int4 Ri = __ldg(reinterpret_cast<const int4 *>(rid + q0));
-    a[0] = A.x; a[1] = A.y; a[2] = A.z; a[3] = A.w;
-    b[0] = Bv.x; b[1] = Bv.y; b[2] = Bv.z; b[3] = Bv.w;
-    ri[0] = Ri.x; ri[1] = Ri.y; ri[2] = Ri.z; ri[3] = Ri.w;
-  } else {
+  constexpr int kS = 4 * kTexQuads;
+  for (int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kS; q0 < nn;
+       q0 += (int64_t)gridDim.x * blockDim.x * kS) {
+    float a[kS], b[kS], out[kS];
+    int32_t ri[kS];
+    const bool full = q0 + kS - 1 < nn;
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool in = q0 + j < nn;
-      a[j] = in ? __ldg(t0 + q0 + j) : 0.f;
-      b[j] = in ? __ldg(t1 + q0 + j) : 0.f;
-      ri[j] = in ? __ldg(rid + q0 + j) : 0;
-    }
-  }
-  float ox = 0.f, oy = 0.f, oz = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
+      for (int g = 0; g < kTexQuads; ++g) {
+        const float4 A = __ldg(reinterpret_cast<const float4 *>(t0 + q0) + g);
+        const float4 Bv = __ldg(reinterpret_cast<const float4 *>(t1 + q0) + g);
+        const int4 Ri = __ldg(reinterpret_cast<const int4 *>(rid + q0) + g);
+        a[4 * g] = A.x; a[4 * g + 1] = A.y; a[4 * g + 2] = A.z; a[4 * g + 3] = A.w;
+        b[4 * g] = Bv.x; b[4 * g + 1] = Bv.y; b[4 * g + 2] = Bv.z; b[4 * g + 3] = Bv.w;
+        ri[4 * g] = Ri.x; ri[4 * g + 1] = Ri.y; ri[4 * g + 2] = Ri.z; ri[4 * g + 3] = Ri.w;
+      }
+    } else {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int64_t r = ri[j];
-    if (j == 0 || ri[j] != ri[j - 1]) {  // samples are grouped by ray: reload only on a new ray
-      ox = __ldg(o + 3 * r);
-      oy = __ldg(o + 3 * r + 1);
-      oz = __ldg(o + 3 * r + 2);
-      dx = __ldg(d + 3 * r);
-      dy = __ldg(d + 3 * r + 1);
-      dz = __ldg(d + 3 * r + 2);
+      for (int j = 0; j < kS; ++j) {
+        const bool in = q0 + j < nn;
+        a[j] = in ? __ldg(t0 + q0 + j) : 0.f;
+        b[j] = in ? __ldg(t1 + q0 + j) : 0.f;
+        ri[j] = in ? __ldg(rid + q0 + j) : 0;
+      }
     }
-    const float m = 0.5f * (a[j] + b[j]);
-    float x = ox + m * dx;
-    float y = oy + m * dy;
-    float z = oz + m * dz;
-    const bool in = tex_coord(lo, hi, sc, contracted, x, y, z);
-    out[j] = in ? tex3D<float>(tex, x, y, z) : 0.f;
-  }
-  if (full) {
-    *reinterpret_cast<float4 *>(sigma + q0) = make_float4(out[0], out[1], out[2], out[3]);
-  } else {
-    for (int j = 0; j < 4; ++j)
-      if (q0 + j < nn) sigma[q0 + j] = out[j];
-  }
+    float ox = 0.f, oy = 0.f, oz = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
+#pragma unroll
+    for (int j = 0; j < kS; ++j) {
+      const int64_t r = ri[j];
+      if (j == 0 || ri[j] != ri[j - 1]) {  // samples are grouped by ray: reload only on a new ray
+        ox = __ldg(o + 3 * r);
+        oy = __ldg(o + 3 * r + 1);
+        oz = __ldg(o + 3 * r + 2);
+        dx = __ldg(d + 3 * r);
+        dy = __ldg(d + 3 * r + 1);
+        dz = __ldg(d + 3 * r + 2);
+      }
+      const float m = 0.5f * (a[j] + b[j]);
+      float x = ox + m * dx;
+      float y = oy + m * dy;
+      float z = oz + m * dz;
+      const bool in = tex_coord(lo, hi, sc, contracted, x, y, z);
+      out[j] = in ? tex3D<float>(tex, x, y, z) : 0.f;
+    }
+    if (full) {
+#pragma unroll
+      for (int g = 0; g < kTexQuads; ++g)
+        reinterpret_cast<float4 *>(sigma + q0)[g] = make_float4(out[4 * g], out[4 * g + 1], out[4 * g + 2],
+                                                                out[4 * g + 3]);
+    } else {
+      for (int j = 0; j < kS; ++j)
+        if (q0 + j < nn) sigma[q0 + j] = out[j];
+    }
   }
 }
 
@@ -443,7 +452,8 @@ extern "C" nacc_status naccx_tex_at_samples(uint64_t handle, float lo, float hi,
                                                                 t0, t1, ray_id, n, n_dev, sigma, rgb);
   else if (((reinterpret_cast<uintptr_t>(t0) | reinterpret_cast<uintptr_t>(t1) | reinterpret_cast<uintptr_t>(ray_id) |
               reinterpret_cast<uintptr_t>(sigma)) & 15) == 0)
-    tex_sigma4_kernel<<<n_dev ? blocks_capped((n + 3) / 4) : blocks_for((n + 3) / 4), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
+    tex_sigma4_kernel<<<n_dev ? blocks_capped((n + 4 * kTexQuads - 1) / (4 * kTexQuads))
+                                    : blocks_for((n + 4 * kTexQuads - 1) / (4 * kTexQuads)), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
                                                                     t0, t1, ray_id, n, n_dev, sigma);
   else
     tex_samples_kernel<false><<<blocks_for(n), 256, 0, stream>>>(f->t_sig, f->res, lo, hi, contracted, rays_o, rays_d,
