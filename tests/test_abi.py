@@ -101,6 +101,25 @@ def test_host_validation_rejects_before_launch(lib):
     assert lib.nacc_occgrid_points(C.byref(g), 0, 0, 1, 0, 16**3 + 1, fake, None) == 1
     assert lib.nacc_filter_early_stop(fake, 4, fake, fake, fake, 10, float("nan"), fake, fake, fake, fake, 10, fake,
                                       fake, 1 << 20, None) == 1
+    # rows beyond the core path (alpha compositing, combined estimator, dynamic grid, proposal loss)
+    assert lib.nacc_render_weights_alpha_fwd(fake, 4, None, 10, 1.0, fake, None, None) == 1  # alphas NULL
+    assert lib.nacc_render_weights_alpha_fwd(fake, 4, fake, 10, float("nan"), fake, None, None) == 1
+    assert lib.nacc_render_weights_alpha_bwd(fake, 4, fake, 10, 1.0, fake, None, fake, fake, 8, None) == 1  # ws
+    assert b"workspace" in lib.nacc_last_error()
+    assert lib.nacc_render_weights_alpha_bwd_workspace_bytes(1000) >= 8000
+    assert lib.nacc_importance_sample_ranged(4, 8, fake, fake, None, 0, None, None, 4, 0, 0, fake, None, None) == 1
+    assert lib.nacc_importance_sample_ranged(4, 8, fake, fake, fake, 0, fake, fake, 4, 0, 0, fake, None, None) == 1
+    assert lib.nacc_occgrid_ray_bounds(C.byref(g), fake, C.byref(pc), fake, fake, None, None, 10, None, fake, None,
+                                       fake, 1 << 20, None) == 1  # t_near NULL
+    assert lib.nacc_occgrid_times(C.byref(g), 0, 0, -1, 0, 10, fake, None) == 1  # negative draw
+    assert lib.nacc_occgrid_times(C.byref(g), 0, 0, 0, 0, 16**3 + 1, fake, None) == 1  # range
+    assert lib.nacc_max_merge(None, fake, 10, None) == 1
+    assert lib.nacc_pdf_loss(4, 0, fake, fake, 8, fake, fake, 1e-7, fake, None) == 1  # nf < 1
+    assert lib.nacc_pdf_loss(4, 8, fake, fake, 8, fake, fake, 0.0, fake, None) == 1  # eps <= 0
+    assert lib.nacc_pdf_loss_bwd(4, 8, fake, fake, 8, fake, fake, 1e-7, None, fake, None) == 1  # g_loss NULL
+    # zero-size calls succeed without launching
+    assert lib.nacc_pdf_loss(0, 8, None, None, 8, None, None, 1e-7, None, None) == 0
+    assert lib.nacc_max_merge(None, None, 0, None) == 0
 
 
 def test_product_has_no_oracle_dependency():
