@@ -14,6 +14,7 @@ __device__ __forceinline__ double phi(int map, double s, double tn, double inv_t
 
 constexpr int kResampleWarps = 4;
 
+template <bool kRanged>
 __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     int64_t n_rays, int n_in, const float *__restrict__ s_edges, const float *__restrict__ sigma,
     const float *__restrict__ cdf, int map, double tn, double tf, const float *__restrict__ tn_r,
@@ -26,7 +27,7 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
   float *e = smem + (size_t)warp * 2 * (n_in + 1);
   float *F = e + (n_in + 1);
   const float *er = s_edges + r * (int64_t)(n_in + 1);
-  if (tn_r) {  // per-ray span (combined estimator, reading #19)
+  if (kRanged) {  // per-ray span (combined estimator, reading #19)
     tn = (double)__ldg(tn_r + r);
     tf = (double)__ldg(tf_r + r);
     if (!(tf > tn)) {  // culled: uniform s edges, every t at t_near
@@ -126,11 +127,20 @@ static nacc_status launch_importance(int64_t n_rays, int32_t n_in, const float *
     set_error("nacc_importance_sample: n_in too large for shared memory");
     return NACC_ERR_UNSUPPORTED;
   }
-  if (smem > 48 * 1024)
-    NACC_CUDA(cudaFuncSetAttribute(importance_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  importance_kernel<<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
-      n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, tn_r, tf_r, n_out, stratified,
-      (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), s_out, t_out);
+  const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
+  if (tn_r) {
+    if (smem > 48 * 1024)
+      NACC_CUDA(cudaFuncSetAttribute(importance_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    importance_kernel<true><<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
+        n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, tn_r, tf_r, n_out, stratified, k0, k1, s_out,
+        t_out);
+  } else {
+    if (smem > 48 * 1024)
+      NACC_CUDA(cudaFuncSetAttribute(importance_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    importance_kernel<false><<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
+        n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, nullptr, nullptr, n_out, stratified, k0, k1,
+        s_out, t_out);
+  }
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;
