@@ -85,6 +85,17 @@ def ncu_traffic():
             if all(k in by_kernel for k in ks)}
 
 
+def ncu_warp_instructions(kernel="march_fused"):
+    """warp instructions per launch of `kernel` from the newest committed ncu summary, if any"""
+    rounds = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_{kernel}.txt")))
+    if not rounds:
+        return None
+    for ln in open(rounds[-1]):
+        if ln.startswith("total warp instructions"):
+            return float(ln.split()[-1])
+    return None
+
+
 # ----------------------------------------------------------------------------- clocks (NVML)
 class ClockSampler:
     def __init__(self, index):
@@ -715,6 +726,17 @@ def run_nacc(args):
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": tr, "kernel": dom, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": byts,
                     "ms_per_launch": lib_stages[dom]}
+            # the march is bound by instruction issue, not HBM (DESIGN.md §6/§10): its warp
+            # instructions per launch (committed ncu capture) over the issue peak of 148 SMs x 4
+            # schedulers x 1 warp-instruction per cycle at the sampled SM clock
+            winst = ncu_warp_instructions() if dom == "march" else None
+            if winst:
+                sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+                n_sm = torch.cuda.get_device_properties(device).multi_processor_count
+                issue_peak = n_sm * 4 * sm_mhz * 1e6
+                got = winst / (lib_stages[dom] / 1e3)
+                roof["issue"] = {"warp_instructions_per_launch": winst, "achieved": got / 1e9,
+                                 "peak": issue_peak / 1e9, "unit": "G warp-instr/s", "frac": got / issue_peak}
         cpu = None
         if not args.no_cpu_baseline and not args.profile and world == 1:
             cpu = cpu_baseline()
