@@ -6,6 +6,13 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef NACC_LB_NS0
+#define NACC_LB_NS0 256  // first back-off of a look-back wait (ns); doubles up to NACC_LB_NSMAX (swept)
+#endif
+#ifndef NACC_LB_NSMAX
+#define NACC_LB_NSMAX 4096
+#endif
+
 namespace nacc {
 
 struct LookbackWs {
@@ -43,7 +50,7 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long *st, in
   if (tile == 0) return 0;
   long long excl = 0;
   int64_t j = tile - 1;  // lanes look at tiles j, j-1, ..., j-31
-  unsigned ns = 32;
+  unsigned ns = NACC_LB_NS0;
   for (;;) {
     const int64_t idx = j - lane;
     const unsigned long long w = idx >= 0 ? ld_relaxed(st + idx) : 2ull;  // before tile 0: inclusive 0
@@ -53,7 +60,7 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long *st, in
     const unsigned need = last == 31 ? kFull : ((2u << last) - 1u);
     if (m0 & need) {  // a tile we need has not published yet: back off and re-read the window
       __nanosleep(ns);
-      ns = ns < 1024 ? 2 * ns : ns;
+      ns = ns < NACC_LB_NSMAX ? 2 * ns : ns;
       continue;
     }
     long long v = lane <= last ? (long long)(w >> 2) : 0;
