@@ -230,6 +230,20 @@ struct Items {
 #ifndef NACC_RENDER_BPS
 #define NACC_RENDER_BPS 3
 #endif
+#ifndef NACC_RENDER_TPROD
+#define NACC_RENDER_TPROD 1  // build parameter: T_{j+1} = T_j e^{-s_j} within a thread's items
+#endif
+#ifndef NACC_RENDER_F32A
+#define NACC_RENDER_F32A 0  // build parameter: alpha = -expm1f(-s) in fp32 (experiment)
+#endif
+// e^{-s} of one interval (1 - alpha)
+__device__ __forceinline__ double interval_ea(double s) {
+#if NACC_RENDER_F32A
+  return 1.0 + (double)expm1f(-(float)s);
+#else
+  return exp(-s);
+#endif
+}
 constexpr int64_t kWarpTile = NACC_RENDER_TILE;  // samples per warp tile (build parameter)
 constexpr int kWarpChunk = 128;
 
@@ -436,10 +450,16 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
       SegM cur = segm_identity();  // sums since the lane start or its last head
       SegM lead;                   // the leading run up to its tail, if that tail is in this lane
       int64_t lead_r = -1;
+      // T of the thread's first item from its optical depth, later items by the product
+      // T_{j+1} = T_j e^{-s_j} (one fp64 exp per item instead of two)
+      double Tn = exp(-S[0]);
   #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool live = it.valid[j] && !(S[j] > L);
-        const double w = live ? exp(-S[j]) * (1.0 - exp(-s[j])) : 0.0;
+        const double ea = interval_ea(s[j]);
+        const double T = NACC_RENDER_TPROD ? ((j > 0 && it.head[j]) ? 1.0 : Tn) : exp(-S[j]);
+        Tn = T * ea;
+        const double w = live ? T * (1.0 - ea) : 0.0;
         cur = segm_combine(cur, segm_item(it, j, w, col));
         if (it.tail[j]) {
           if (cur.f) render_fwd_out(cur, it.rid[j], color, opacity, depth, ctx);
@@ -536,16 +556,19 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
       {
         float col[12];
         load_rgb4(col, it, rgb, kVec);
+        double Tn = exp(-S[0]);  // T_{j+1} = T_j e^{-s_j}, as in the forward
   #pragma unroll
         for (int j = 0; j < 4; ++j) {
           w[j] = 0.0;
           gwTea[j] = 0.0;
           double v = 0.0;
+          const double ea = interval_ea(s[j]);
+          const double T = NACC_RENDER_TPROD ? ((j > 0 && it.head[j]) ? 1.0 : Tn) : exp(-S[j]);
+          Tn = T * ea;
           if (it.valid[j] && !(S[j] > L)) {
             live |= 1u << j;
             const float4 gc = __ldg(gcv + it.rid[j]);
             const double2 gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
-            const double T = exp(-S[j]), ea = exp(-s[j]);
             w[j] = T * (1.0 - ea);
             const double gw = (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2] +
                               gon.x + gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
