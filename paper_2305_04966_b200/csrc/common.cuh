@@ -117,6 +117,8 @@ constexpr int kMacroCells = 4;  // fine cells per macro cell and axis
 bool grid_skip_enabled(const nacc_grid &g);
 int64_t grid_aux_offset_words(const nacc_grid &g);   // start of the private region (gridaux.cu)
 int64_t grid_mask2_offset_words(const nacc_grid &g);  // the macro skip mask
+bool grid_fine_mask_enabled(const nacc_grid &g);      // single level: fine dilated mask present
+int64_t grid_mask3_offset_words(const nacc_grid &g);  // the fine (3-cell dilated) skip mask
 constexpr int kAuxHeaderWords = 64;                  // per-level occupied index boxes + world box
 constexpr int kAuxBoxWord = 48;                      // 6 floats: padded world box of all occupied cells
 cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream);

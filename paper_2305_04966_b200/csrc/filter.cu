@@ -18,6 +18,13 @@ constexpr int kFiltRays = 256;
 // sums: rays of very different lengths no longer hold a 256-thread block (and
 // its resources) at a barrier until the longest one is done.
 constexpr int kCutThreads = 64;
+// Samples read per step of a ray's walk: 4 at first, doubling up to kCutBatch, so
+// short rays overread little while long ones (which set the kernel's tail) take
+// fewer dependent round trips to memory.
+#ifndef NACC_FILTER_BATCH
+#define NACC_FILTER_BATCH 16
+#endif
+constexpr int kCutBatch = NACC_FILTER_BATCH;
 
 __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
                                                                  const float *__restrict__ t0,
@@ -32,19 +39,20 @@ __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *
     const int64_t st = pi.x, cnt = pi.y;
     double S = 0.0;
     cut = cnt;
-    for (int64_t i = 0; i < cnt; i += 4) {
-      float a[4], b[4], c[4];
+    int nb = 4;
+    for (int64_t i = 0; i < cnt; i += nb, nb = min(2 * nb, kCutBatch)) {
+      float a[kCutBatch], b[kCutBatch], c[kCutBatch];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool in = i + j < cnt;
+      for (int j = 0; j < kCutBatch; ++j) {
+        const bool in = j < nb && i + j < cnt;
         a[j] = in ? __ldg(t0 + st + i + j) : 0.f;
         b[j] = in ? __ldg(t1 + st + i + j) : 0.f;
         c[j] = in ? __ldg(sigma + st + i + j) : 0.f;
       }
       bool done = false;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (!done && i + j < cnt) {
+      for (int j = 0; j < kCutBatch; ++j) {
+        if (!done && j < nb && i + j < cnt) {
           if (S > L) {
             cut = i + j;
             done = true;

@@ -9,7 +9,11 @@
 //     of every level, padded (6 floats at word 48; lo > hi when none is);
 //   mask2 (when skipping is enabled): for every macro cell m (4^3 fine cells)
 //     of every level, the OR of the fine bits of macro cells m + {0,1}^3,
-//     i.e. of the fine cells [4m, 4m + 8)^3 clipped to the level.
+//     i.e. of the fine cells [4m, 4m + 8)^3 clipped to the level;
+//   mask3 (single-level grids with skipping): for every fine cell c the OR of
+//     the fine bits of cells c + {0,1,2}^3 clipped to the grid, at the fine
+//     resolution (the march's segment test for 8-point segments, which span at
+//     most 3 cells per axis).
 #include "common.cuh"
 
 namespace nacc {
@@ -23,10 +27,20 @@ int64_t grid_aux_offset_words(const nacc_grid &g) {
 
 int64_t grid_mask2_offset_words(const nacc_grid &g) { return grid_aux_offset_words(g) + kAuxHeaderWords; }
 
+static int64_t mask2_words(const nacc_grid &g) {
+  const int64_t M = g.res / kMacroCells;
+  return ceil_div(ceil_div((int64_t)g.levels * M * M * M, 32), 64) * 64;
+}
+
+bool grid_fine_mask_enabled(const nacc_grid &g) { return grid_skip_enabled(g) && g.levels == 1; }
+
+int64_t grid_mask3_offset_words(const nacc_grid &g) { return grid_mask2_offset_words(g) + mask2_words(g); }
+
 static int64_t grid_aux_words(const nacc_grid &g) {
   if (!grid_skip_enabled(g)) return kAuxHeaderWords;
-  const int64_t M = g.res / kMacroCells;
-  return kAuxHeaderWords + ceil_div((int64_t)g.levels * M * M * M, 32);
+  const int64_t w = kAuxHeaderWords + mask2_words(g);
+  if (!grid_fine_mask_enabled(g)) return w;
+  return w + ceil_div((int64_t)g.res * g.res * g.res, 32);
 }
 
 __global__ void bbox_init_kernel(int32_t *__restrict__ hdr, int levels, int R) {
@@ -141,6 +155,28 @@ __global__ void mask2_kernel(uint32_t *__restrict__ bits, int levels, int R, int
   if ((threadIdx.x & 31) == 0 && q < n) bits[aux_off + (q >> 5)] = b;
 }
 
+// thread per fine cell: OR of the bits of cells c + {0,1,2}^3 clipped to the grid (one level)
+__global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits, int R, int64_t off) {
+  const int64_t n = (int64_t)R * R * R;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool on = false;
+  if (q < n) {
+    const int x = (int)(q % R), y = (int)((q / R) % R), z = (int)(q / ((int64_t)R * R));
+    const int nx = min(3, R - x);
+    const uint32_t xmask = (1u << nx) - 1u;
+    for (int zz = z; zz < min(z + 3, R) && !on; ++zz)
+      for (int yy = y; yy < min(y + 3, R) && !on; ++yy) {
+        const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
+        const int o = (int)(s & 31);
+        uint32_t v = __ldg(bits + (s >> 5)) >> o;
+        if (o + nx > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
+        on = (v & xmask) != 0u;
+      }
+  }
+  const unsigned b = __ballot_sync(kFull, on);
+  if ((threadIdx.x & 31) == 0 && q < n) bits[off + (q >> 5)] = b;
+}
+
 cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream) {
   int32_t *hdr = reinterpret_cast<int32_t *>(bits + grid_aux_offset_words(g));
   const int64_t cells = (int64_t)g.levels * g.res * g.res * g.res;
@@ -161,6 +197,11 @@ cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream
     const int M = g.res / kMacroCells;
     const int64_t n = (int64_t)g.levels * M * M * M;
     mask2_kernel<<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, grid_mask2_offset_words(g));
+    count_launch(1);
+  }
+  if (grid_fine_mask_enabled(g)) {
+    const int64_t n = (int64_t)g.res * g.res * g.res;
+    mask3_kernel<<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
     count_launch(1);
   }
   return cudaGetLastError();

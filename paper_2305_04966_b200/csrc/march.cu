@@ -22,6 +22,9 @@
 #ifndef NACC_MARCH_FLATW
 #define NACC_MARCH_FLATW 0  // build parameter: write a tile's samples as one run (vs ray by ray)
 #endif
+#ifndef NACC_MARCH_FINEMASK
+#define NACC_MARCH_FINEMASK 1  // build parameter: single-level segment test on the fine 3-cell dilated mask
+#endif
 #ifndef NACC_MARCH_PREFETCH
 #define NACC_MARCH_PREFETCH 0  // build parameter: L1 prefetch of interior segments' bit words
 #endif
@@ -146,6 +149,35 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
                      (uint32_t)M * ((uint32_t)i0[1] + (uint32_t)M * (uint32_t)i0[2]);
   if (!((__ldg(mask2 + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
   return kL1 ? 1 : 2;
+}
+
+// Single-level grids: the same decision at the fine resolution.  The points of
+// a segment have positions x and cell coordinates u = (x - lo) * s computed by
+// the normative fp32 ops of P(k), each of which is monotone in m (RN rounding
+// is monotone), so every point's floor(u) lies between the endpoints' floors,
+// exactly, per axis.  With at most 3 cells per axis that range lies in
+// c + {0,1,2}^3, c = the clamped low corner, and mask3[c] (the OR of those 27
+// fine bits) being 0 proves no point is emitted.  A segment whose floors lie in
+// [0, R-2] on every axis is inside the box (u >= 0 <=> x >= lo exactly; u < R-1
+// keeps x below hi by a cell), so its points skip the box test and the clamp.
+__device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ mask3,
+                                                 const float A[3], const float B[3]) {
+  const int R = g.res;
+  int c[3];
+  bool interior = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int ia = (int)floorf(__fmul_rn(__fsub_rn(A[a], g.lo[0][a]), g.s[0][a]));
+    const int ib = (int)floorf(__fmul_rn(__fsub_rn(B[a], g.lo[0][a]), g.s[0][a]));
+    const int lo = min(ia, ib), hi = max(ia, ib);
+    if (hi - lo > 2) return 2;                // longer than the mask's window: evaluate
+    if (hi < 0 || lo > R) return 0;          // every point outside the box on this axis
+    interior = interior && lo >= 0 && hi <= R - 2;
+    c[a] = min(max(lo, 0), R - 1);
+  }
+  const uint32_t q = (uint32_t)c[0] + (uint32_t)R * ((uint32_t)c[1] + (uint32_t)R * (uint32_t)c[2]);
+  if (!((__ldg(mask3 + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
+  return interior ? 1 : 2;
 }
 
 // P(k) for a point known to lie inside the (single) level box by a margin far
@@ -325,7 +357,8 @@ __device__ __forceinline__ void lattice_ends(const MarchConst &p, float near_r, 
 template <bool kCone, bool kSkip, bool kL1, typename Emit>
 __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchConst &p,
                                                 const uint32_t *__restrict__ bits,
-                                                const uint32_t *__restrict__ mask2, int M, const RaySetup &s,
+                                                const uint32_t *__restrict__ mask2, int M,
+                                                const uint32_t *__restrict__ mask3, const RaySetup &s,
                                                 const ConeHeader *__restrict__ hdr, const float *__restrict__ tab,
                                                 int *seglist, int &kb_out, int &ke_out, Emit emit) {
   const int lane = threadIdx.x & 31;
@@ -359,7 +392,7 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
         const float ma = lattice_mid<kCone>(p, s, tab, ks), mb = lattice_mid<kCone>(p, s, tab, kl);
         const float A[3] = {__fmaf_rn(ma, s.dx, s.ox), __fmaf_rn(ma, s.dy, s.oy), __fmaf_rn(ma, s.dz, s.oz)};
         const float B[3] = {__fmaf_rn(mb, s.dx, s.ox), __fmaf_rn(mb, s.dy, s.oy), __fmaf_rn(mb, s.dz, s.oz)};
-        code = segment_test<kL1>(g, mask2, M, A, B);
+        code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, mask3, A, B) : segment_test<kL1>(g, mask2, M, A, B);
         flag = code != 0;
 #if NACC_MARCH_PREFETCH
         if (code == 1) {  // interior segment: warm L1 with the bit words its points will read
@@ -461,7 +494,7 @@ struct FusedTile {  // per-lane metadata of a tile in flight (lane j: ray j)
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
-    const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
+    const uint32_t *__restrict__ mask3, const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
     const float *__restrict__ t_max, int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr,
     const float *__restrict__ tab, LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info,
     int64_t *__restrict__ total, int64_t capacity, int32_t *__restrict__ status_out, float *__restrict__ t0,
@@ -504,7 +537,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
         const int start = pos;
         int kb0 = 0, ke0 = 0;
         const int32_t c =
-            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[warp], kb0, ke0,
                                              [&](unsigned b, bool pred, int k, int32_t cnt) {
                                                const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
                                                const int off = k - kb0;
@@ -604,7 +637,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
           } else {  // k-list overflowed: traverse again, writing directly
             const RaySetup s = s_setup[warp][pb][j];
             int kb0, ke0;
-            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[warp], kb0, ke0,
+            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[warp], kb0, ke0,
                                             [&](unsigned b, bool pred, int k, int32_t cnt) {
                                               if (pred) {
                                                 const int64_t q = run + cnt + __popc(b & ((1u << lane) - 1u));
@@ -632,6 +665,7 @@ __global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(256) march_fill_kernel(GridConst g, MarchConst p, const uint32_t *__restrict__ bits,
                                                          const uint32_t *__restrict__ mask2, int M,
+                                                         const uint32_t *__restrict__ mask3,
                                                          const float *__restrict__ obox,
                                                          const float *__restrict__ rays_o,
                                                          const float *__restrict__ rays_d,
@@ -649,7 +683,7 @@ __global__ void __launch_bounds__(256) march_fill_kernel(GridConst g, MarchConst
   const int64_t out = packed_info[2 * r];
   const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r);
   int kb0, ke0;
-  traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[threadIdx.x >> 5], kb0, ke0,
+  traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[threadIdx.x >> 5], kb0, ke0,
                                   [&](unsigned b, bool pred, int k, int32_t cnt) {
                                     if (pred) {
                                       const int64_t q = out + cnt + __popc(b & ((1u << lane) - 1u));
@@ -668,7 +702,7 @@ __global__ void __launch_bounds__(256) march_fill_kernel(GridConst g, MarchConst
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(128) march_bounds_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
-    const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d,
+    const uint32_t *__restrict__ mask3, const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d,
     const float *__restrict__ t_min, const float *__restrict__ t_max, int64_t n_rays,
     const ConeHeader *__restrict__ hdr, const float *__restrict__ tab, float *__restrict__ t_near,
     float *__restrict__ t_far, unsigned long long *__restrict__ n_alive) {
@@ -678,7 +712,7 @@ __global__ void __launch_bounds__(128) march_bounds_kernel(
   if (r >= n_rays) return;
   const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r);
   int kfirst = -1, klast = -1, kb0, ke0;
-  traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, s, hdr, tab, seglist[threadIdx.x >> 5], kb0, ke0,
+  traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[threadIdx.x >> 5], kb0, ke0,
                                   [&](unsigned b, bool pred, int k, int32_t cnt) {
                                     if (b) {
                                       const int kf = __shfl_sync(kFull, k, __ffs(b) - 1);
@@ -837,6 +871,9 @@ static nacc_status launch_march(int mode, const nacc_grid *grid, const uint32_t 
   const int M = grid->res / kMacro;
   // built by nacc_grid_prepare / nacc_occgrid_update (gridaux.cu)
   const uint32_t *mask2 = bits + grid_mask2_offset_words(*grid);
+  // fine dilated mask (single level; build option NACC_MARCH_FINEMASK, 0 = macro test only)
+  const uint32_t *mask3 =
+      (NACC_MARCH_FINEMASK && grid_fine_mask_enabled(*grid)) ? bits + grid_mask3_offset_words(*grid) : nullptr;
   const float *obox = reinterpret_cast<const float *>(bits + grid_aux_offset_words(*grid) + kAuxBoxWord);
   if (cone) {  // shared cone lattice table (reading #5)
     NACC_CUDA(cudaMemsetAsync(w.hdr, 0, sizeof(ConeHeader), stream));
@@ -847,16 +884,16 @@ static nacc_status launch_march(int mode, const nacc_grid *grid, const uint32_t 
   }
   if (mode == kModeBounds) {  // t0 / t1 carry t_near / t_far
     if (n_alive) NACC_CUDA(cudaMemsetAsync(n_alive, 0, sizeof(unsigned long long), stream));
-    NACC_DISPATCH3(march_bounds_kernel, (unsigned)grid_for(n_rays * 32, 128), 128, stream, g, p, bits, mask2, M,
+    NACC_DISPATCH3(march_bounds_kernel, (unsigned)grid_for(n_rays * 32, 128), 128, stream, g, p, bits, mask2, M, mask3,
                    obox, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, t0, t1, n_alive);
   } else if (mode == kModeFused) {
     const int64_t n_tiles = fused_tiles(n_rays, cone, l1);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
-    NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, obox, rays_o,
+    NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, mask3, obox, rays_o,
                    rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,
                    status_out, t0, t1, ray_id);
   } else {
-    NACC_DISPATCH3(march_fill_kernel, (unsigned)grid_for(n_rays * 32, 256), 256, stream, g, p, bits, mask2, M,
+    NACC_DISPATCH3(march_fill_kernel, (unsigned)grid_for(n_rays * 32, 256), 256, stream, g, p, bits, mask2, M, mask3,
                    obox, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, packed_info, t0, t1, ray_id);
   }
   count_launch(1);
