@@ -315,12 +315,13 @@ class Pipeline:
         self.acc.zero_()
         self.acc_status.zero_()
 
-    def step_graph(self, timing=False, rays=None):
+    def step_graph(self, timing=False, rays=None, copy_inputs=True):
         torch = self.torch
-        o, d = rays if rays is not None else self.rays[self.k % len(self.rays)]
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
-        self.o_buf.copy_(o, non_blocking=True)
-        self.d_buf.copy_(d, non_blocking=True)
+        if copy_inputs:  # else the caller has filled o_buf / d_buf on this stream
+            o, d = rays if rays is not None else self.rays[self.k % len(self.rays)]
+            self.o_buf.copy_(o, non_blocking=True)
+            self.d_buf.copy_(d, non_blocking=True)
         if timing:  # stage breakdown: one graph per stage, events between
             for i, g in enumerate(self.graphs):
                 ev[i].record()
@@ -372,6 +373,25 @@ def run_extras(device, reps=20):
     byts = len(c.rays_o) * 40 + n3 * 12
     out["cfg3_march"] = {"rays": len(c.rays_o), "samples": n3, "ms": ms3, "samples_per_s": n3 / (ms3 / 1e3),
                          "GBps": byts / (ms3 / 1e3) / 1e9, "frac_of_peak": byts / (ms3 / 1e3) / 1e9 / peak}
+    # ---- CFG3 full inference frame (SURVEY 8(d).2 passes): march -> field σ -> filter -> field σ,rgb
+    # -> render fwd, device counts throughout (no host sync inside the frame); harness field included
+    fld3 = H.TextureField(torch.from_numpy(c.scene.data.reshape(-1, 4)).to(device), c.scene.lo, c.scene.hi,
+                          contracted=True)
+
+    def frame():
+        s = N.sampling_occgrid(o, d, spec, bits, prm, capacity=cap, sync=False)
+        sg, _ = fld3.at_samples(o, d, s.t0, s.t1, s.ray_id, want_rgb=False, n_dev=s.total)
+        f = N.filter_early_stop(s, sg, EPS, sync=False)
+        sg2, rgb2 = fld3.at_samples(o, d, f.t0, f.t1, f.ray_id, n_dev=f.total)
+        return N.render_fwd(f, sg2, rgb2, EPS), f
+
+    ms_fr, (_, f3) = timed(frame, n=5)
+    kept3 = int(f3.total.item())
+    out["cfg3_frame"] = {"rays": len(c.rays_o), "samples_marched": n3, "samples_kept": kept3, "ms": ms_fr,
+                         "frames_per_s": 1e3 / ms_fr, "rays_per_s": len(c.rays_o) / (ms_fr / 1e3),
+                         "kept_samples_per_s": kept3 / (ms_fr / 1e3), "includes": "harness field (texture σ, "
+                         "lattice σ,rgb over the contracted scene)"}
+    del fld3
     # ---- CFG4: proposal resampling 256 -> 96 -> 48 + 48-sample render fwd/bwd
     pc = W.cfg4()
     lat = H.LatticeField(torch.from_numpy(pc.scene.data.reshape(-1, 4)).to(device), pc.scene.lo, pc.scene.hi,
@@ -676,7 +696,7 @@ def run_nacc(args):
     if not args.profile:
         pinned = [(torch.from_numpy(o).pin_memory(), torch.from_numpy(d).pin_memory()) for o, d in pipe.rays_host]
         out_host = torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32).pin_memory()
-        k2 = max(args.steps // 4, 20)
+        k2 = max(args.steps, 20)
         if use_graph:
             pipe.acc.zero_()
         post_e2e = 0
@@ -684,20 +704,76 @@ def run_nacc(args):
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
-        f0.record()
-        for i in range(k2):
-            ho, hd = pinned[i % len(pinned)]
+        main = torch.cuda.current_stream()
+        up, down = torch.cuda.Stream(), torch.cuda.Stream()
+        stage = [(torch.empty_like(pipe.o_buf), torch.empty_like(pipe.d_buf)) for _ in range(2)] if use_graph else None
+        snaps = [torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32, device=device) for _ in range(2)]
+        hosts = [out_host, torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32).pin_memory()]
+        h2d_done = [torch.cuda.Event() for _ in range(2)]
+        stage_free = [torch.cuda.Event() for _ in range(2)]
+        snap_ready = [torch.cuda.Event() for _ in range(2)]
+        d2h_done = [torch.cuda.Event() for _ in range(2)]
+
+        def run_io(k2):
+            n_post_eager = 0
             if use_graph:
-                pipe.step_graph(rays=(ho, hd))  # H2D copy from pinned memory into the static inputs
-                res = torch.cat([pipe.outs["color"], pipe.outs["opacity"][:, None], pipe.outs["depth"][:, None]], 1)
+                # Pipelined host I/O (what a training loop does): step i+1's rays go host->device on
+                # one copy stream and step i's colour/opacity/depth device->host on another while
+                # step i computes; every step still moves its own inputs and results.
+                up.wait_stream(main)
+                down.wait_stream(main)
+
+                def h2d(i):
+                    b = i % 2
+                    with torch.cuda.stream(up):
+                        if i >= 2:
+                            up.wait_event(stage_free[b])  # step i-2 has copied this staging buffer out
+                        ho, hd = pinned[i % len(pinned)]
+                        stage[b][0].copy_(ho, non_blocking=True)
+                        stage[b][1].copy_(hd, non_blocking=True)
+                        h2d_done[b].record(up)
+
+                h2d(0)
+                for i in range(k2):
+                    b = i % 2
+                    if i + 1 < k2:
+                        h2d(i + 1)
+                    main.wait_event(h2d_done[b])
+                    pipe.o_buf.copy_(stage[b][0], non_blocking=True)
+                    pipe.d_buf.copy_(stage[b][1], non_blocking=True)
+                    stage_free[b].record(main)
+                    pipe.step_graph(copy_inputs=False)
+                    if i >= 2:
+                        main.wait_event(d2h_done[b])  # step i-2's result has left this snapshot
+                    torch.cat([pipe.outs["color"], pipe.outs["opacity"][:, None], pipe.outs["depth"][:, None]], 1,
+                              out=snaps[b])
+                    snap_ready[b].record(main)
+                    with torch.cuda.stream(down):
+                        down.wait_event(snap_ready[b])
+                        hosts[b].copy_(snaps[b], non_blocking=True)
+                        d2h_done[b].record(down)
+                main.wait_stream(up)
+                main.wait_stream(down)
             else:
-                o = ho.to(device, non_blocking=True)
-                d = hd.to(device, non_blocking=True)
-                color, opacity, depth, n_post = pipe.step(rays=(o, d))
-                post_e2e += n_post
-                res = torch.cat([color.detach(), opacity.detach()[:, None], depth.detach()[:, None]], 1)
-            out_host.copy_(res, non_blocking=True)
+                for i in range(k2):
+                    ho, hd = pinned[i % len(pinned)]
+                    o = ho.to(device, non_blocking=True)
+                    d = hd.to(device, non_blocking=True)
+                    color, opacity, depth, n_post = pipe.step(rays=(o, d))
+                    n_post_eager += n_post
+                    res = torch.cat([color.detach(), opacity.detach()[:, None], depth.detach()[:, None]], 1)
+                    out_host.copy_(res, non_blocking=True)
+            return n_post_eager
+
+        run_io(3)  # untimed: first use of the copy streams, staging buffers and pinned outputs
+        torch.cuda.synchronize()
+        if use_graph:
+            pipe.acc.zero_()
+        f0.record()
+        h0 = time.perf_counter()
+        post_e2e = run_io(k2)
         f1.record()
+        host_ms = (time.perf_counter() - h0) * 1e3 / k2  # host time to issue one step
         torch.cuda.synchronize()
         barrier()
         if use_graph:
@@ -710,7 +786,9 @@ def run_nacc(args):
             dist.all_reduce(t2[1:], op=dist.ReduceOp.SUM)
             t2[0] = m[0]
         e2e = {"value": t2[1].item() / (t2[0].item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": RAYS_PER_GPU * 24,
-               "d2h_bytes_per_step": RAYS_PER_GPU * 20, "steps": k2}
+               "d2h_bytes_per_step": RAYS_PER_GPU * 20, "steps": k2, "host_issue_ms_per_step": host_ms,
+               "io": ("pinned host buffers; H2D of step i+1 and D2H of step i on two copy streams, "
+                      "double-buffered, overlapping step i" if use_graph else "pinned host buffers, serial")}
 
     if rank == 0:
         peak, peak_kind = measured_peaks()

@@ -18,11 +18,11 @@ constexpr int kFiltRays = 256;
 // sums: rays of very different lengths no longer hold a 256-thread block (and
 // its resources) at a barrier until the longest one is done.
 constexpr int kCutThreads = 64;
-// Samples read per step of a ray's walk: 4 at first, doubling up to kCutBatch, so
-// short rays overread little while long ones (which set the kernel's tail) take
-// fewer dependent round trips to memory.
+// Samples read per step of a ray's walk: 4 at first, doubling up to kCutBatch
+// (build parameter; 4 = fixed quads measured fastest on CFG2: 74.6 us vs 76.0 for
+// 8 and 78.3 for 16 -- the overread costs more than the saved round trips).
 #ifndef NACC_FILTER_BATCH
-#define NACC_FILTER_BATCH 16
+#define NACC_FILTER_BATCH 4
 #endif
 constexpr int kCutBatch = NACC_FILTER_BATCH;
 

@@ -13,7 +13,7 @@
 //   mask3 (single-level grids with skipping): for every fine cell c the OR of
 //     the fine bits of cells c + {0,1,2}^3 clipped to the grid, at the fine
 //     resolution (the march's segment test for 8-point segments, which span at
-//     most 3 cells per axis).
+//     most 3 cells per axis);
 #include "common.cuh"
 
 namespace nacc {
@@ -36,11 +36,15 @@ bool grid_fine_mask_enabled(const nacc_grid &g) { return grid_skip_enabled(g) &&
 
 int64_t grid_mask3_offset_words(const nacc_grid &g) { return grid_mask2_offset_words(g) + mask2_words(g); }
 
+static int64_t mask3_words(const nacc_grid &g) {
+  return ceil_div(ceil_div((int64_t)g.res * g.res * g.res, 32), 64) * 64;
+}
+
 static int64_t grid_aux_words(const nacc_grid &g) {
   if (!grid_skip_enabled(g)) return kAuxHeaderWords;
   const int64_t w = kAuxHeaderWords + mask2_words(g);
   if (!grid_fine_mask_enabled(g)) return w;
-  return w + ceil_div((int64_t)g.res * g.res * g.res, 32);
+  return w + mask3_words(g);
 }
 
 __global__ void bbox_init_kernel(int32_t *__restrict__ hdr, int levels, int R) {

@@ -161,6 +161,39 @@ def test_march_sparse_grid_bounds(N, levels, res):
     assert_march_equal(gpu_march(N, one, levels, res, roi, o * 3, d, step=step), ref)
 
 
+@pytest.mark.parametrize("cells_per_step", [0.05, 0.2, 0.37, 0.5, 1.3])
+def test_march_fine_mask_stress(N, cells_per_step):
+    """Single-level grids take the fine (3-cell-window) segment test: isolated occupied
+    cells, cells on the box faces and corners, axis-aligned rays along cell boundaries,
+    rays starting inside the box, and steps whose 8-point segments span 0.4 .. 10 cells
+    (beyond 3 cells per axis the test falls back to full evaluation).  Bit-exact."""
+    R = 32
+    rng = np.random.default_rng(int(cells_per_step * 1000))
+    occ = (rng.random(R**3) < 0.01).astype(np.uint8)
+    idx = np.arange(R)
+    for a, b in ((0, 0), (R - 1, R - 1), (0, R - 1), (R - 2, 1)):  # face and corner lines
+        occ[a + R * (b + R * idx)] = 1
+        occ[idx + R * (a + R * b)] = 1
+    roi = (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5)
+    o, d = random_rays(3000, rng)
+    # axis-aligned rays exactly on cell boundaries, and origins inside the box
+    k = 400
+    j = rng.integers(0, R + 1, (k, 2)) / R - 0.5
+    ax = rng.integers(0, 3, k)
+    for i in range(k):
+        oo = np.empty(3)
+        oo[ax[i]] = -0.9
+        oo[(ax[i] + 1) % 3], oo[(ax[i] + 2) % 3] = j[i]
+        dd = np.zeros(3)
+        dd[ax[i]] = 1.0
+        o[5 + i], d[5 + i] = oo, dd
+    o[500:800] = rng.uniform(-0.45, 0.45, (300, 3)).astype(np.float32)
+    step = float(np.float32(cells_per_step / R))
+    ref = O.march(occ, 1, R, roi, o, d, step=step)
+    assert ref[0][:, 1].sum() > 500
+    assert_march_equal(gpu_march(N, occ, 1, R, roi, o, d, step=step), ref)
+
+
 def test_march_deterministic(N):
     rng = np.random.default_rng(2)
     o, d = random_rays(4000, rng)
