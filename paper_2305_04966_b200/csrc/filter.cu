@@ -25,6 +25,9 @@ constexpr int kCutThreads = 64;
 #define NACC_FILTER_BATCH 4
 #endif
 constexpr int kCutBatch = NACC_FILTER_BATCH;
+#ifndef NACC_FILTER_SECTOR
+#define NACC_FILTER_SECTOR 1  // build parameter: sector-aligned walk when the arrays are 32-byte aligned
+#endif
 
 __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
                                                                  const float *__restrict__ t0,
@@ -55,6 +58,51 @@ __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *
         if (!done && j < nb && i + j < cnt) {
           if (S > L) {
             cut = i + j;
+            done = true;
+          } else {
+            S = __dadd_rn(S, __dmul_rn((double)c[j], __dsub_rn((double)b[j], (double)a[j])));
+          }
+        }
+      }
+      if (done) break;
+    }
+    cut_out[r] = (int32_t)cut;
+  }
+  const int64_t tot = warp_sum_i64(cut);
+  const int64_t r_warp = r - (threadIdx.x & 31);
+  if ((threadIdx.x & 31) == 0 && tot)
+    atomicAdd(reinterpret_cast<unsigned long long *>(block_sums + r_warp / kFiltRays), (unsigned long long)tot);
+}
+
+// Pass 1, sector-aligned variant: the walk reads whole 32-byte sectors (8 floats, two
+// float4 loads per array) starting at the sector that holds the ray's first sample, so
+// every DRAM sector fetched is used in full (the unaligned quads above straddle two).
+// Needs 32-byte-aligned t0 / t1 / sigma; reads stay inside the last sector of the ray.
+__global__ void __launch_bounds__(kCutThreads) filter_cut_sector_kernel(
+    const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
+    const float *__restrict__ t1, const float *__restrict__ sigma, double L, int32_t *__restrict__ cut_out,
+    int64_t *__restrict__ block_sums) {
+  const int64_t r = (int64_t)blockIdx.x * kCutThreads + threadIdx.x;
+  int64_t cut = 0;
+  if (r < n_rays) {
+    const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
+    const int64_t st = pi.x, e = pi.x + pi.y;
+    double S = 0.0;
+    cut = pi.y;
+    for (int64_t q = st & ~(int64_t)7; q < e; q += 8) {
+      const float4 *pa = reinterpret_cast<const float4 *>(t0 + q), *pb = reinterpret_cast<const float4 *>(t1 + q),
+                   *pc = reinterpret_cast<const float4 *>(sigma + q);
+      const float4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1), c0 = __ldg(pc),
+                   c1 = __ldg(pc + 1);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      bool done = false;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!done && q + j >= st && q + j < e) {
+          if (S > L) {
+            cut = q + j - st;
             done = true;
           } else {
             S = __dadd_rn(S, __dmul_rn((double)c[j], __dsub_rn((double)b[j], (double)a[j])));
@@ -215,8 +263,12 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   filter_ws_layout(n_rays, &cuts, &bsums, ws);
   const int64_t nb = ceil_div(n_rays, kFiltRays);
   NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)nb, stream));
-  filter_cut_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-      packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts, bsums);
+  if (NACC_FILTER_SECTOR && aligned(t0, 32) && aligned(t1, 32) && aligned(sigma, 32))
+    filter_cut_sector_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
+        packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts, bsums);
+  else
+    filter_cut_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
+        packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts, bsums);
   block_sums_scan_kernel<<<1, 1024, 0, stream>>>(bsums, nb, total);
   filter_copy_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, cuts, bsums, total, capacity,
                                                              packed_info_out, capacity > 0 ? t0_out : nullptr, t1_out,

@@ -25,6 +25,9 @@
 #ifndef NACC_MARCH_FINEMASK
 #define NACC_MARCH_FINEMASK 1  // build parameter: single-level segment test on the fine 3-cell dilated mask
 #endif
+#ifndef NACC_MARCH_SHAREDENDS
+#define NACC_MARCH_SHAREDENDS 1  // build parameter: segment ends from the next lane's start (fine mask)
+#endif
 #ifndef NACC_MARCH_PREFETCH
 #define NACC_MARCH_PREFETCH 0  // build parameter: L1 prefetch of interior segments' bit words
 #endif
@@ -160,16 +163,20 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
 // fine bits) being 0 proves no point is emitted.  A segment whose floors lie in
 // [0, R-2] on every axis is inside the box (u >= 0 <=> x >= lo exactly; u < R-1
 // keeps x below hi by a cell), so its points skip the box test and the clamp.
-__device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ mask3,
-                                                 const float A[3], const float B[3]) {
+__device__ __forceinline__ void cell_floors(const GridConst &g, const float X[3], int f[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) f[a] = (int)floorf(__fmul_rn(__fsub_rn(X[a], g.lo[0][a]), g.s[0][a]));
+}
+
+// the fine test from the endpoints' cell floors (ia: first point, ib: last point or any later one)
+__device__ __forceinline__ int segment_test_floors(const GridConst &g, const uint32_t *__restrict__ mask3,
+                                                   const int ia[3], const int ib[3]) {
   const int R = g.res;
   int c[3];
   bool interior = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const int ia = (int)floorf(__fmul_rn(__fsub_rn(A[a], g.lo[0][a]), g.s[0][a]));
-    const int ib = (int)floorf(__fmul_rn(__fsub_rn(B[a], g.lo[0][a]), g.s[0][a]));
-    const int lo = min(ia, ib), hi = max(ia, ib);
+    const int lo = min(ia[a], ib[a]), hi = max(ia[a], ib[a]);
     if (hi - lo > 2) return 2;                // longer than the mask's window: evaluate
     if (hi < 0 || lo > R) return 0;          // every point outside the box on this axis
     interior = interior && lo >= 0 && hi <= R - 2;
@@ -178,6 +185,14 @@ __device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint3
   const uint32_t q = (uint32_t)c[0] + (uint32_t)R * ((uint32_t)c[1] + (uint32_t)R * (uint32_t)c[2]);
   if (!((__ldg(mask3 + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
   return interior ? 1 : 2;
+}
+
+__device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ mask3,
+                                                 const float A[3], const float B[3]) {
+  int ia[3], ib[3];
+  cell_floors(g, A, ia);
+  cell_floors(g, B, ib);
+  return segment_test_floors(g, mask3, ia, ib);
 }
 
 // P(k) for a point known to lie inside the (single) level box by a margin far
@@ -381,9 +396,30 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
   kb_out = kb;
   ke_out = ke;
   constexpr int kSpan = kSkip ? 32 * kSeg : 32;
-  for (int k0 = kb; k0 < ke; k0 += kSpan) {
+  // shared endpoints (uniform single-level lattice, fine mask): every lane computes the cell
+  // floors of its segment's first point only; a segment's range is closed by the next lane's
+  // first point (a later point: still a superset by monotonicity), so a window holds 31
+  // segments and lane 31 only supplies the last end
+  const bool shared = NACC_MARCH_SHAREDENDS && kSkip && kL1 && !kCone && mask3 != nullptr;
+  const int span = shared ? 31 * kSeg : kSpan;
+  for (int k0 = kb; k0 < ke; k0 += span) {
     int nseg = 1;
-    if (kSkip) {
+    if (kSkip && shared) {
+      const int ks = k0 + lane * kSeg;
+      const float m = lattice_mid<false>(p, s, tab, ks);
+      const float X[3] = {__fmaf_rn(m, s.dx, s.ox), __fmaf_rn(m, s.dy, s.oy), __fmaf_rn(m, s.dz, s.oz)};
+      int fa[3], fb[3];
+      cell_floors(g, X, fa);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) fb[a] = __shfl_down_sync(kFull, fa[a], 1);
+      int code = 0;
+      if (lane < 31 && ks < ke) code = segment_test_floors(g, mask3, fa, fb);
+      const bool flag = code != 0;
+      const unsigned F = __ballot_sync(kFull, flag);
+      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : 0);
+      __syncwarp();
+      nseg = __popc(F);
+    } else if (kSkip) {
       const int ks = k0 + lane * kSeg;
       bool flag = false;
       int code = 0;
