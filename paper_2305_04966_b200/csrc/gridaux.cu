@@ -44,7 +44,7 @@ static int64_t grid_aux_words(const nacc_grid &g) {
   if (!grid_skip_enabled(g)) return kAuxHeaderWords;
   const int64_t w = kAuxHeaderWords + mask2_words(g);
   if (!grid_fine_mask_enabled(g)) return w;
-  return w + mask3_words(g);
+  return w + 2 * mask3_words(g);  // OR window mask, then AND window mask
 }
 
 __global__ void bbox_init_kernel(int32_t *__restrict__ hdr, int levels, int R) {
@@ -159,7 +159,10 @@ __global__ void mask2_kernel(uint32_t *__restrict__ bits, int levels, int R, int
   if ((threadIdx.x & 31) == 0 && q < n) bits[aux_off + (q >> 5)] = b;
 }
 
-// thread per fine cell: OR of the bits of cells c + {0,1,2}^3 clipped to the grid (one level)
+// thread per fine cell (one level): the OR (kAnd = false) or the AND (kAnd = true) of the
+// bits of cells c + {0,1,2}^3; cells outside the grid count as empty (an AND window that
+// leaves the grid is 0)
+template <bool kAnd>
 __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits, int R, int64_t off) {
   const int64_t n = (int64_t)R * R * R;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -168,14 +171,26 @@ __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits,
     const int x = (int)(q % R), y = (int)((q / R) % R), z = (int)(q / ((int64_t)R * R));
     const int nx = min(3, R - x);
     const uint32_t xmask = (1u << nx) - 1u;
-    for (int zz = z; zz < min(z + 3, R) && !on; ++zz)
-      for (int yy = y; yy < min(y + 3, R) && !on; ++yy) {
-        const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
-        const int o = (int)(s & 31);
-        uint32_t v = __ldg(bits + (s >> 5)) >> o;
-        if (o + nx > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
-        on = (v & xmask) != 0u;
-      }
+    if (kAnd) {
+      on = x + 3 <= R && y + 3 <= R && z + 3 <= R;
+      for (int zz = z; zz < z + 3 && on; ++zz)
+        for (int yy = y; yy < y + 3 && on; ++yy) {
+          const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
+          const int o = (int)(s & 31);
+          uint32_t v = __ldg(bits + (s >> 5)) >> o;
+          if (o + 3 > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
+          on = (v & 7u) == 7u;
+        }
+    } else {
+      for (int zz = z; zz < min(z + 3, R) && !on; ++zz)
+        for (int yy = y; yy < min(y + 3, R) && !on; ++yy) {
+          const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
+          const int o = (int)(s & 31);
+          uint32_t v = __ldg(bits + (s >> 5)) >> o;
+          if (o + nx > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
+          on = (v & xmask) != 0u;
+        }
+    }
   }
   const unsigned b = __ballot_sync(kFull, on);
   if ((threadIdx.x & 31) == 0 && q < n) bits[off + (q >> 5)] = b;
@@ -205,8 +220,9 @@ cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream
   }
   if (grid_fine_mask_enabled(g)) {
     const int64_t n = (int64_t)g.res * g.res * g.res;
-    mask3_kernel<<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
-    count_launch(1);
+    mask3_kernel<false><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
+    mask3_kernel<true><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g) + mask3_words(g));
+    count_launch(2);
   }
   return cudaGetLastError();
 }

@@ -28,6 +28,9 @@
 #ifndef NACC_MARCH_SHAREDENDS
 #define NACC_MARCH_SHAREDENDS 1  // build parameter: segment ends from the next lane's start (fine mask)
 #endif
+#ifndef NACC_MARCH_SOLID
+#define NACC_MARCH_SOLID 1  // build parameter: segments in an all-occupied 3^3 window skip P(k)
+#endif
 #ifndef NACC_MARCH_PREFETCH
 #define NACC_MARCH_PREFETCH 0  // build parameter: L1 prefetch of interior segments' bit words
 #endif
@@ -184,7 +187,12 @@ __device__ __forceinline__ int segment_test_floors(const GridConst &g, const uin
   }
   const uint32_t q = (uint32_t)c[0] + (uint32_t)R * ((uint32_t)c[1] + (uint32_t)R * (uint32_t)c[2]);
   if (!((__ldg(mask3 + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
-  return interior ? 1 : 2;
+  if (!interior) return 2;
+  // solid window (mask3and, R^3 bits after mask3): every cell the points can fall in is
+  // occupied, so every point is a member (subject only to k < ke and m < far)
+  const uint32_t *mask3and = mask3 + ((((int64_t)R * R * R + 31) / 32 + 63) / 64) * 64;
+  if (NACC_MARCH_SOLID && ((__ldg(mask3and + (q >> 5)) >> (q & 31u)) & 1u)) return 3;
+  return 1;
 }
 
 __device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ mask3,
@@ -416,7 +424,7 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
       if (lane < 31 && ks < ke) code = segment_test_floors(g, mask3, fa, fb);
       const bool flag = code != 0;
       const unsigned F = __ballot_sync(kFull, flag);
-      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : 0);
+      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : (code == 3 ? 0x300 : 0));
       __syncwarp();
       nseg = __popc(F);
     } else if (kSkip) {
@@ -449,17 +457,18 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 #endif
       }
       const unsigned F = __ballot_sync(kFull, flag);
-      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : 0);
+      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : (code == 3 ? 0x300 : 0));
       __syncwarp();
       nseg = __popc(F);
     }
     // lane (lane % kSeg) of segment list entry idx: its point k and P(k)
     auto eval = [&](int idx, int &k) -> bool {
-      bool interior = false;
+      bool interior = false, solid = false;
       if (kSkip) {
         const int e = idx < nseg ? seglist[idx] : 0;
         k = idx < nseg ? k0 + (e & 0xff) * kSeg + (lane % kSeg) : ke;
         interior = kL1 && (e & 0x100);
+        solid = kL1 && (e & 0x200);
       } else {
         k = k0 + lane;
       }
@@ -467,8 +476,9 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
       if (k < ke) {
         const float m = lattice_mid<kCone>(p, s, tab, k);
         if (m < s.far_r)
-          pred = interior ? occupied_interior(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz)
-                          : occupied<kL1>(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz);
+          pred = solid ? true
+                       : (interior ? occupied_interior(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz)
+                                   : occupied<kL1>(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz));
       }
       return pred;
     };
