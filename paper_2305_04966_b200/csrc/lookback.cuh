@@ -6,6 +6,9 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef NACC_LB_STATS
+#define NACC_LB_STATS 0  // debug build: count look-back polls (nacc_debug_lb_stats)
+#endif
 #ifndef NACC_LB_NS0
 #define NACC_LB_NS0 256  // first back-off of a look-back wait (ns); doubles up to NACC_LB_NSMAX (swept)
 #endif
@@ -14,6 +17,11 @@
 #endif
 
 namespace nacc {
+
+#if NACC_LB_STATS
+// debug build only: [0] resolves, [1] poll iterations, [2] iterations that slept, [3] tiles walked
+__device__ unsigned long long g_lb_stats[4];
+#endif
 
 struct LookbackWs {
   unsigned int tile_counter;
@@ -58,6 +66,13 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long *st, in
     const unsigned m0 = __ballot_sync(kFull, (w & 3ull) == 0ull);
     const int last = m2 ? __ffs(m2) - 1 : 31;  // nearest predecessor with an inclusive prefix
     const unsigned need = last == 31 ? kFull : ((2u << last) - 1u);
+#if NACC_LB_STATS
+    if (lane == 0) {
+      atomicAdd(&g_lb_stats[1], 1ull);
+      if (m0 & need) atomicAdd(&g_lb_stats[2], 1ull);
+      else atomicAdd(&g_lb_stats[3], (unsigned long long)(last + 1));
+    }
+#endif
     if (m0 & need) {  // a tile we need has not published yet: back off and re-read the window
       __nanosleep(ns);
       ns = ns < NACC_LB_NSMAX ? 2 * ns : ns;
@@ -71,6 +86,9 @@ __device__ __forceinline__ long long lookback_resolve(unsigned long long *st, in
     j -= 32;
   }
   if (lane == 0) st_relaxed(st + tile, ((unsigned long long)(excl + agg) << 2) | 2ull);
+#if NACC_LB_STATS
+  if (lane == 0) atomicAdd(&g_lb_stats[0], 1ull);
+#endif
   return excl;
 }
 

@@ -1010,4 +1010,14 @@ nacc_status nacc_occgrid_ray_bounds(const nacc_grid *grid, const uint32_t *bits,
                       nullptr, 0, nullptr, nullptr, ws, stream, reinterpret_cast<unsigned long long *>(n_alive));
 }
 
+#if NACC_LB_STATS
+// debug build only: read and reset the look-back counters (resolves, polls, sleeping polls, tiles walked)
+void nacc_debug_lb_stats(unsigned long long *out4) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out4, g_lb_stats, 4 * sizeof(unsigned long long));
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_lb_stats, z, sizeof(z));
+}
+#endif
+
 }  // extern "C"
