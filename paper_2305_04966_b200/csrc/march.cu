@@ -31,6 +31,9 @@
 #ifndef NACC_MARCH_SOLID
 #define NACC_MARCH_SOLID 1  // build parameter: segments in an all-occupied 3^3 window skip P(k)
 #endif
+#ifndef NACC_MARCH_MINB
+#define NACC_MARCH_MINB 7  // build parameter: min resident blocks per SM in the fused march's launch bounds
+#endif
 #ifndef NACC_MARCH_PREFETCH
 #define NACC_MARCH_PREFETCH 0  // build parameter: L1 prefetch of interior segments' bit words
 #endif
@@ -538,7 +541,7 @@ struct FusedTile {  // per-lane metadata of a tile in flight (lane j: ray j)
 };
 
 template <bool kCone, bool kSkip, bool kL1>
-__global__ void __launch_bounds__(kFWarps * 32, 10) march_fused_kernel(
+__global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
     const uint32_t *__restrict__ mask3, const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
     const float *__restrict__ t_max, int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr,

@@ -233,6 +233,9 @@ struct Items {
 #ifndef NACC_RENDER_TPROD
 #define NACC_RENDER_TPROD 1  // build parameter: T_{j+1} = T_j e^{-s_j} within a thread's items
 #endif
+#ifndef NACC_RENDER_RAYCACHE
+#define NACC_RENDER_RAYCACHE 1  // build parameter: backward loads per-ray constants once per run of the ray
+#endif
 #ifndef NACC_RENDER_F32A
 #define NACC_RENDER_F32A 0  // build parameter: alpha = -expm1f(-s) in fp32 (experiment)
 #endif
@@ -557,6 +560,10 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
         float col[12];
         load_rgb4(col, it, rgb, kVec);
         double Tn = exp(-S[0]);  // T_{j+1} = T_j e^{-s_j}, as in the forward
+        // per-ray constants, loaded once per run of the ray within the thread's items
+        int32_t cr = -1;
+        float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
+        double2 gon = make_double2(0.0, 0.0);
   #pragma unroll
         for (int j = 0; j < 4; ++j) {
           w[j] = 0.0;
@@ -567,8 +574,11 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
           Tn = T * ea;
           if (it.valid[j] && !(S[j] > L)) {
             live |= 1u << j;
-            const float4 gc = __ldg(gcv + it.rid[j]);
-            const double2 gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
+            if (!NACC_RENDER_RAYCACHE || it.rid[j] != cr) {
+              gc = __ldg(gcv + it.rid[j]);
+              gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
+              cr = it.rid[j];
+            }
             w[j] = T * (1.0 - ea);
             const double gw = (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2] +
                               gon.x + gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
@@ -584,14 +594,20 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
       }
       Seg<1> run = warp_seg_excl<1>(agg, carryP);
       float gs[4], gr[12];
+      int32_t cr = -1;
+      float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
+      double R = 0.0;
   #pragma unroll
       for (int j = 0; j < 4; ++j) {
         run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + s[j];
         gs[j] = 0.f;
         gr[3 * j] = gr[3 * j + 1] = gr[3 * j + 2] = 0.f;
         if (live & (1u << j)) {
-          const float4 gc = __ldg(gcv + it.rid[j]);
-          const double R = __ldg(gq + 2 * (int64_t)it.rid[j] + 1).x;
+          if (!NACC_RENDER_RAYCACHE || it.rid[j] != cr) {
+            gc = __ldg(gcv + it.rid[j]);
+            R = __ldg(gq + 2 * (int64_t)it.rid[j] + 1).x;
+            cr = it.rid[j];
+          }
           const double Q = R - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
           gs[j] = (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q));
           gr[3 * j] = (float)(w[j] * gc.x);
