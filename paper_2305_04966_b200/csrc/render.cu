@@ -228,7 +228,7 @@ struct Items {
 #define NACC_RENDER_TILE 256
 #endif
 #ifndef NACC_RENDER_BPS
-#define NACC_RENDER_BPS 3
+#define NACC_RENDER_BPS 4  // blocks per SM of the tile kernels (A/B: 2 / 3 / 4 -> bwd 88.4 / 81.7 / 79.7 us)
 #endif
 #ifndef NACC_RENDER_TPROD
 #define NACC_RENDER_TPROD 1  // build parameter: T_{j+1} = T_j e^{-s_j} within a thread's items
