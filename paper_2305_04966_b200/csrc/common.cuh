@@ -114,6 +114,10 @@ inline int grid_for(int64_t work_items, int per_block, int64_t cap = (1ll << 31)
 
 // occupancy bitfield auxiliary skip mask (gridaux.cu)
 constexpr int kMacroCells = 4;  // fine cells per macro cell and axis
+#ifndef NACC_MARCH_WIN
+#define NACC_MARCH_WIN 5  // fine-mask window (cells per axis): 3 for 8-point segments, 5 for 16
+#endif
+constexpr int kFineWin = NACC_MARCH_WIN;
 bool grid_skip_enabled(const nacc_grid &g);
 int64_t grid_aux_offset_words(const nacc_grid &g);   // start of the private region (gridaux.cu)
 int64_t grid_mask2_offset_words(const nacc_grid &g);  // the macro skip mask

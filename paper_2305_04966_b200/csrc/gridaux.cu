@@ -169,21 +169,21 @@ __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits,
   bool on = false;
   if (q < n) {
     const int x = (int)(q % R), y = (int)((q / R) % R), z = (int)(q / ((int64_t)R * R));
-    const int nx = min(3, R - x);
+    const int nx = min(kFineWin, R - x);
     const uint32_t xmask = (1u << nx) - 1u;
     if (kAnd) {
-      on = x + 3 <= R && y + 3 <= R && z + 3 <= R;
-      for (int zz = z; zz < z + 3 && on; ++zz)
-        for (int yy = y; yy < y + 3 && on; ++yy) {
+      on = x + kFineWin <= R && y + kFineWin <= R && z + kFineWin <= R;
+      for (int zz = z; zz < z + kFineWin && on; ++zz)
+        for (int yy = y; yy < y + kFineWin && on; ++yy) {
           const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
           const int o = (int)(s & 31);
           uint32_t v = __ldg(bits + (s >> 5)) >> o;
-          if (o + 3 > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
-          on = (v & 7u) == 7u;
+          if (o + kFineWin > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
+          on = (v & xmask) == xmask;
         }
     } else {
-      for (int zz = z; zz < min(z + 3, R) && !on; ++zz)
-        for (int yy = y; yy < min(y + 3, R) && !on; ++yy) {
+      for (int zz = z; zz < min(z + kFineWin, R) && !on; ++zz)
+        for (int yy = y; yy < min(y + kFineWin, R) && !on; ++yy) {
           const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
           const int o = (int)(s & 31);
           uint32_t v = __ldg(bits + (s >> 5)) >> o;
@@ -194,6 +194,34 @@ __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits,
   }
   const unsigned b = __ballot_sync(kFull, on);
   if ((threadIdx.x & 31) == 0 && q < n) bits[off + (q >> 5)] = b;
+}
+
+// Row-wise variant (R % 32 == 0): thread per output word, i.e. 32 cells of one x-row; the
+// x-window is W shifted copies of the row's word and its successor, then OR (AND) over the
+// W x W rows of the window.  Same bits as mask3_kernel, 32x fewer loads.
+template <bool kAnd>
+__global__ void __launch_bounds__(256) mask3_rows_kernel(uint32_t *__restrict__ bits, int R, int64_t off) {
+  const int64_t nw = (int64_t)R * R * R / 32;
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nw) return;
+  const int64_t c0 = q * 32;
+  const int x0 = (int)(c0 % R), y = (int)((c0 / R) % R), z = (int)(c0 / ((int64_t)R * R));
+  const bool last_word = x0 + 32 >= R;
+  uint32_t acc = kAnd ? 0xffffffffu : 0u;
+  if (kAnd && (y + kFineWin > R || z + kFineWin > R)) acc = 0u;
+  for (int zz = z; zz < min(z + kFineWin, R) && (!kAnd || acc); ++zz)
+    for (int yy = y; yy < min(y + kFineWin, R); ++yy) {
+      const int64_t wi = (x0 + (int64_t)R * (yy + (int64_t)R * zz)) >> 5;
+      const uint32_t w = __ldg(bits + wi), wn = last_word ? 0u : __ldg(bits + wi + 1);
+      uint32_t d = w;
+#pragma unroll
+      for (int k = 1; k < kFineWin; ++k) {
+        const uint32_t sh = (w >> k) | (wn << (32 - k));
+        d = kAnd ? (d & sh) : (d | sh);
+      }
+      acc = kAnd ? (acc & d) : (acc | d);
+    }
+  bits[off + q] = acc;
 }
 
 cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream) {
@@ -220,8 +248,14 @@ cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream
   }
   if (grid_fine_mask_enabled(g)) {
     const int64_t n = (int64_t)g.res * g.res * g.res;
-    mask3_kernel<false><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
-    mask3_kernel<true><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g) + mask3_words(g));
+    if (g.res % 32 == 0) {
+      mask3_rows_kernel<false><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
+      mask3_rows_kernel<true><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.res,
+                                                                         grid_mask3_offset_words(g) + mask3_words(g));
+    } else {
+      mask3_kernel<false><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
+      mask3_kernel<true><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g) + mask3_words(g));
+    }
     count_launch(2);
   }
   return cudaGetLastError();

@@ -114,11 +114,16 @@ __device__ __forceinline__ bool occupied(const GridConst &g, const uint32_t *__r
 // the segment AB (monotone lattice), so they share its bounding box; positions
 // use the same fp32 ops as P(k) and a 1e-3 macro-cell margin covers rounding.
 #ifndef NACC_MARCH_SEG
-#define NACC_MARCH_SEG 8
+#define NACC_MARCH_SEG 16
 #endif
-constexpr int kSeg = NACC_MARCH_SEG;  // lattice points per segment (8 or 16; build parameter)
-constexpr int kSegPerPass = 32 / kSeg;  // segments evaluated per 32-lane pass
-static_assert(kSeg == 8 || kSeg == 16, "segment length");
+#ifndef NACC_MARCH_SEG_CASCADE
+#define NACC_MARCH_SEG_CASCADE 8
+#endif
+// lattice points per segment (8 or 16; build parameters): single-level grids (fine mask, whose
+// window NACC_MARCH_WIN must hold a segment's cell range) and cascades (macro test)
+constexpr int seg_len(bool l1) { return l1 ? NACC_MARCH_SEG : NACC_MARCH_SEG_CASCADE; }
+static_assert(NACC_MARCH_SEG == 8 || NACC_MARCH_SEG == 16, "segment length");
+static_assert(NACC_MARCH_SEG_CASCADE == 8 || NACC_MARCH_SEG_CASCADE == 16, "segment length");
 constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
 constexpr float kSegEps = 1e-3f;
 
@@ -183,7 +188,7 @@ __device__ __forceinline__ int segment_test_floors(const GridConst &g, const uin
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const int lo = min(ia[a], ib[a]), hi = max(ia[a], ib[a]);
-    if (hi - lo > 2) return 2;                // longer than the mask's window: evaluate
+    if (hi - lo > kFineWin - 1) return 2;     // longer than the mask's window: evaluate
     if (hi < 0 || lo > R) return 0;          // every point outside the box on this axis
     interior = interior && lo >= 0 && hi <= R - 2;
     c[a] = min(max(lo, 0), R - 1);
@@ -406,6 +411,8 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
   }
   kb_out = kb;
   ke_out = ke;
+  constexpr int kSeg = seg_len(kL1);
+  constexpr int kSegPerPass = 32 / kSeg;  // segments evaluated per 32-lane pass
   constexpr int kSpan = kSkip ? 32 * kSeg : 32;
   // shared endpoints (uniform single-level lattice, fine mask): every lane computes the cell
   // floors of its segment's first point only; a segment's range is closed by the next lane's
