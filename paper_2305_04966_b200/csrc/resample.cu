@@ -46,14 +46,17 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
   if (sigma) {
     const float *sr = sigma + r * (int64_t)n_in;
     double carry = 0.0;
+    // t of every edge once: lane l holds t(e[base + l]); t(e[j + 1]) comes from the next lane,
+    // and for lane 31 from lane 0 of the next window (computed one window ahead)
+    double ta = lane <= n_in ? phi(map, (double)e[lane], tn, inv_tn, inv_tf, tf) : 0.0;
     for (int base = 0; base < n_in; base += 32) {
       const int j = base + lane;
+      const double tnext = j + 32 <= n_in ? phi(map, (double)e[j + 32], tn, inv_tn, inv_tf, tf) : 0.0;
+      const double dn = __shfl_down_sync(kFull, ta, 1), wn = __shfl_sync(kFull, tnext, 0);
+      const double tb = lane < 31 ? dn : wn;
       double s = 0.0;
-      if (j < n_in) {
-        const double ta = phi(map, (double)e[j], tn, inv_tn, inv_tf, tf);
-        const double tb = phi(map, (double)e[j + 1], tn, inv_tn, inv_tf, tf);
-        s = (double)__ldg(sr + j) * (tb - ta);
-      }
+      if (j < n_in) s = (double)__ldg(sr + j) * (tb - ta);
+      ta = tnext;
       const double incl = warp_incl_scan(s);
       if (j < n_in) F[j + 1] = -expm1f(-(float)(carry + incl));
       carry += __shfl_sync(kFull, incl, 31);
@@ -61,9 +64,11 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     if (lane == 0) F[0] = 0.f;
     uniform = !(-expm1(-carry) > 1e-12);
     __syncwarp();
-    if (!uniform) {
-      const float Fm = F[n_in];
-      for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(F[j], Fm);
+    if (!uniform) {  // F / F_m by one reciprocal (within an ulp of the quotient); F_m / F_m = 1 exactly
+      const float Fm = F[n_in], rFm = __frcp_rn(Fm);
+      for (int j = lane; j < n_in; j += 32) F[j] = fminf(__fmul_rn(F[j], rFm), 1.0f);  // monotone, <= 1
+      __syncwarp();
+      if (lane == 0) F[n_in] = 1.0f;
     }
   } else {
     const float *cr = cdf + r * (int64_t)(n_in + 1);
