@@ -574,6 +574,27 @@ def test_resample_cdf_input_stratified_and_degenerate(N):
     check_resample(sg.cpu().numpy(), sr, F, e, 17, stratified=True)
 
 
+def test_resample_unbounded_lindisp(N):
+    """Φ = lindisp with t_f = inf (S:73, S:78: 1/t = (1 - s)/t_n): t grows without bound as s -> 1;
+    the kernel's reciprocals must follow the oracle out to t ~ 1e6."""
+    rng = np.random.default_rng(21)
+    n, m = 500, 64
+    e = np.sort(rng.uniform(0, 0.999999, (n, m + 1)), axis=1).astype(np.float32)
+    e[:, 0] = 0
+    sig = rng.uniform(0, 3, (n, m)).astype(np.float32)
+    sg, tg = N.importance_sample(cuda(e), 24, sigma=cuda(sig), map_kind=N.MAP_LINDISP, t_near=0.5,
+                                 t_far=math.inf)
+    sr, tr = O.importance_sample(e, 24, sigma=sig, map_kind=1, t_near=0.5, t_far=math.inf)
+    F = O.importance_cdf(e, sigma=sig, map_kind=1, t_near=0.5, t_far=math.inf)
+    check_resample(sg.cpu().numpy(), sr, F, e, 24)
+    tg = tg.cpu().numpy().astype(np.float64)
+    s32 = sg.cpu().numpy()
+    t_of_s = 1.0 / ((1.0 - s32.astype(np.float64)) / 0.5)  # Φ of the kernel's own (rounded) s
+    # the kernel maps its unrounded s: allow dΦ/ds = t^2 / t_n times one fp32 ulp of s
+    ulp = np.spacing(np.abs(s32)).astype(np.float64)
+    assert np.all(np.abs(tg - t_of_s) <= 1e-6 * t_of_s + t_of_s**2 / 0.5 * ulp)
+
+
 # ============================================================================ combined estimator
 def gpu_bounds(N, occ, levels, res, roi, o, d, **kw):
     import torch
