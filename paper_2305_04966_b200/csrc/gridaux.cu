@@ -10,7 +10,7 @@
 //   mask2 (when skipping is enabled): for every macro cell m (4^3 fine cells)
 //     of every level, the OR of the fine bits of macro cells m + {0,1}^3,
 //     i.e. of the fine cells [4m, 4m + 8)^3 clipped to the level;
-//   mask3 (single-level grids with skipping): for every fine cell c the OR of
+//   mask3 (every grid with skipping; per level): for every fine cell c the OR of
 //     the fine bits of cells c + {0,1,2}^3 clipped to the grid, at the fine
 //     resolution (the march's segment test for 8-point segments, which span at
 //     most 3 cells per axis);
@@ -32,12 +32,12 @@ static int64_t mask2_words(const nacc_grid &g) {
   return ceil_div(ceil_div((int64_t)g.levels * M * M * M, 32), 64) * 64;
 }
 
-bool grid_fine_mask_enabled(const nacc_grid &g) { return grid_skip_enabled(g) && g.levels == 1; }
+bool grid_fine_mask_enabled(const nacc_grid &g) { return grid_skip_enabled(g); }
 
 int64_t grid_mask3_offset_words(const nacc_grid &g) { return grid_mask2_offset_words(g) + mask2_words(g); }
 
-static int64_t mask3_words(const nacc_grid &g) {
-  return ceil_div(ceil_div((int64_t)g.res * g.res * g.res, 32), 64) * 64;
+static int64_t mask3_words(const nacc_grid &g) {  // one mask, every level (level-major, R^3 bits each)
+  return ceil_div(ceil_div((int64_t)g.levels * g.res * g.res * g.res, 32), 64) * 64;
 }
 
 static int64_t grid_aux_words(const nacc_grid &g) {
@@ -163,19 +163,20 @@ __global__ void mask2_kernel(uint32_t *__restrict__ bits, int levels, int R, int
 // bits of cells c + {0,1,2}^3; cells outside the grid count as empty (an AND window that
 // leaves the grid is 0)
 template <bool kAnd>
-__global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits, int R, int64_t off) {
-  const int64_t n = (int64_t)R * R * R;
+__global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits, int levels, int R, int64_t off) {
+  const int64_t R3 = (int64_t)R * R * R, n = levels * R3;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool on = false;
   if (q < n) {
-    const int x = (int)(q % R), y = (int)((q / R) % R), z = (int)(q / ((int64_t)R * R));
+    const int64_t lbase = (q / R3) * R3, ql = q - lbase;  // the cell's level: windows stay inside it
+    const int x = (int)(ql % R), y = (int)((ql / R) % R), z = (int)(ql / ((int64_t)R * R));
     const int nx = min(kFineWin, R - x);
     const uint32_t xmask = (1u << nx) - 1u;
     if (kAnd) {
       on = x + kFineWin <= R && y + kFineWin <= R && z + kFineWin <= R;
       for (int zz = z; zz < z + kFineWin && on; ++zz)
         for (int yy = y; yy < y + kFineWin && on; ++yy) {
-          const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
+          const int64_t s = lbase + x + (int64_t)R * (yy + (int64_t)R * zz);
           const int o = (int)(s & 31);
           uint32_t v = __ldg(bits + (s >> 5)) >> o;
           if (o + kFineWin > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits,
     } else {
       for (int zz = z; zz < min(z + kFineWin, R) && !on; ++zz)
         for (int yy = y; yy < min(y + kFineWin, R) && !on; ++yy) {
-          const int64_t s = x + (int64_t)R * (yy + (int64_t)R * zz);
+          const int64_t s = lbase + x + (int64_t)R * (yy + (int64_t)R * zz);
           const int o = (int)(s & 31);
           uint32_t v = __ldg(bits + (s >> 5)) >> o;
           if (o + nx > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
@@ -200,18 +201,18 @@ __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits,
 // x-window is W shifted copies of the row's word and its successor, then OR (AND) over the
 // W x W rows of the window.  Same bits as mask3_kernel, 32x fewer loads.
 template <bool kAnd>
-__global__ void __launch_bounds__(256) mask3_rows_kernel(uint32_t *__restrict__ bits, int R, int64_t off) {
-  const int64_t nw = (int64_t)R * R * R / 32;
+__global__ void __launch_bounds__(256) mask3_rows_kernel(uint32_t *__restrict__ bits, int levels, int R, int64_t off) {
+  const int64_t R3 = (int64_t)R * R * R, nw = levels * R3 / 32;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nw) return;
-  const int64_t c0 = q * 32;
+  const int64_t lbase = (q * 32 / R3) * R3, c0 = q * 32 - lbase;
   const int x0 = (int)(c0 % R), y = (int)((c0 / R) % R), z = (int)(c0 / ((int64_t)R * R));
   const bool last_word = x0 + 32 >= R;
   uint32_t acc = kAnd ? 0xffffffffu : 0u;
   if (kAnd && (y + kFineWin > R || z + kFineWin > R)) acc = 0u;
   for (int zz = z; zz < min(z + kFineWin, R) && (!kAnd || acc); ++zz)
     for (int yy = y; yy < min(y + kFineWin, R); ++yy) {
-      const int64_t wi = (x0 + (int64_t)R * (yy + (int64_t)R * zz)) >> 5;
+      const int64_t wi = (lbase + x0 + (int64_t)R * (yy + (int64_t)R * zz)) >> 5;
       const uint32_t w = __ldg(bits + wi), wn = last_word ? 0u : __ldg(bits + wi + 1);
       uint32_t d = w;
 #pragma unroll
@@ -247,14 +248,14 @@ cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream
     count_launch(1);
   }
   if (grid_fine_mask_enabled(g)) {
-    const int64_t n = (int64_t)g.res * g.res * g.res;
+    const int64_t n = (int64_t)g.levels * g.res * g.res * g.res;
+    const int64_t o3 = grid_mask3_offset_words(g), o3and = o3 + mask3_words(g);
     if (g.res % 32 == 0) {
-      mask3_rows_kernel<false><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
-      mask3_rows_kernel<true><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.res,
-                                                                         grid_mask3_offset_words(g) + mask3_words(g));
+      mask3_rows_kernel<false><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3);
+      mask3_rows_kernel<true><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3and);
     } else {
-      mask3_kernel<false><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g));
-      mask3_kernel<true><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.res, grid_mask3_offset_words(g) + mask3_words(g));
+      mask3_kernel<false><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3);
+      mask3_kernel<true><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3and);
     }
     count_launch(2);
   }

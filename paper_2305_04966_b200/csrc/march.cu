@@ -117,7 +117,7 @@ __device__ __forceinline__ bool occupied(const GridConst &g, const uint32_t *__r
 #define NACC_MARCH_SEG 16
 #endif
 #ifndef NACC_MARCH_SEG_CASCADE
-#define NACC_MARCH_SEG_CASCADE 8
+#define NACC_MARCH_SEG_CASCADE 16
 #endif
 // lattice points per segment (8 or 16; build parameters): single-level grids (fine mask, whose
 // window NACC_MARCH_WIN must hold a segment's cell range) and cascades (macro test)
@@ -127,12 +127,59 @@ static_assert(NACC_MARCH_SEG_CASCADE == 8 || NACC_MARCH_SEG_CASCADE == 16, "segm
 constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
 constexpr float kSegEps = 1e-3f;
 
+// Single-level grids: the same decision at the fine resolution.  The points of
+// a segment have positions x and cell coordinates u = (x - lo) * s computed by
+// the normative fp32 ops of P(k), each of which is monotone in m (RN rounding
+// is monotone), so every point's floor(u) lies between the endpoints' floors,
+// exactly, per axis.  With at most 3 cells per axis that range lies in
+// c + {0,1,2}^3, c = the clamped low corner, and mask3[c] (the OR of those 27
+// fine bits) being 0 proves no point is emitted.  A segment whose floors lie in
+// [0, R-2] on every axis is inside the box (u >= 0 <=> x >= lo exactly; u < R-1
+// keeps x below hi by a cell), so its points skip the box test and the clamp.
+__device__ __forceinline__ void cell_floors(const GridConst &g, const float X[3], int f[3], int l = 0) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) f[a] = (int)floorf(__fmul_rn(__fsub_rn(X[a], g.lo[l][a]), g.s[l][a]));
+}
+
+// the fine test from the endpoints' cell floors (ia: first point, ib: last point or any later one)
+__device__ __forceinline__ int segment_test_floors(const GridConst &g, const uint32_t *__restrict__ mask3,
+                                                   const int ia[3], const int ib[3], int l = 0) {
+  const int R = g.res;
+  const int64_t R3w = (int64_t)R * R * R / 32;  // words per level (R % 4 == 0)
+  int c[3];
+  bool interior = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int lo = min(ia[a], ib[a]), hi = max(ia[a], ib[a]);
+    if (hi - lo > kFineWin - 1) return 2;     // longer than the mask's window: evaluate
+    if (hi < 0 || lo > R) return 0;          // every point outside the box on this axis
+    interior = interior && lo >= 0 && hi <= R - 2;
+    c[a] = min(max(lo, 0), R - 1);
+  }
+  const uint32_t q = (uint32_t)c[0] + (uint32_t)R * ((uint32_t)c[1] + (uint32_t)R * (uint32_t)c[2]);
+  if (!((__ldg(mask3 + l * R3w + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
+  if (!interior) return 2;
+  // solid window (mask3and, after every level's mask3): every cell the points can fall in is
+  // occupied, so every point is a member (subject only to k < ke and m < far)
+  const uint32_t *mask3and = mask3 + ((g.levels * R3w + 63) / 64) * 64;
+  if (NACC_MARCH_SOLID && ((__ldg(mask3and + l * R3w + (q >> 5)) >> (q & 31u)) & 1u)) return 3;
+  return 1;
+}
+
+__device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ mask3,
+                                                 const float A[3], const float B[3]) {
+  int ia[3], ib[3];
+  cell_floors(g, A, ia);
+  cell_floors(g, B, ib);
+  return segment_test_floors(g, mask3, ia, ib);
+}
+
 // Returns 0 (skip the segment), 1 (evaluate; the segment lies inside the
 // single level's box with margin, so P(k) can skip the box test) or 2
 // (evaluate with the full predicate).
 template <bool kL1>
 __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *__restrict__ mask2, int M,
-                                            const float A[3], const float B[3]) {
+                                            const uint32_t *__restrict__ mask3, const float A[3], const float B[3]) {
   int la = 0;
   if (!kL1) {
     la = level_of<false>(g, A[0], A[1], A[2]);
@@ -146,6 +193,12 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
         meets = meets && hi >= g.lo[la - 1][a] - pad && lo <= g.hi[la - 1][a] + pad;
       }
       if (meets) return 2;
+    }
+    if (mask3 != nullptr) {  // every point lies in level la (convex box, finer box clear): its fine window
+      int ia[3], ib[3];
+      cell_floors(g, A, ia, la);
+      cell_floors(g, B, ib, la);
+      return segment_test_floors(g, mask3, ia, ib, la) | (la << 4);
     }
   }
   int i0[3];
@@ -165,73 +218,29 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
   return kL1 ? 1 : 2;
 }
 
-// Single-level grids: the same decision at the fine resolution.  The points of
-// a segment have positions x and cell coordinates u = (x - lo) * s computed by
-// the normative fp32 ops of P(k), each of which is monotone in m (RN rounding
-// is monotone), so every point's floor(u) lies between the endpoints' floors,
-// exactly, per axis.  With at most 3 cells per axis that range lies in
-// c + {0,1,2}^3, c = the clamped low corner, and mask3[c] (the OR of those 27
-// fine bits) being 0 proves no point is emitted.  A segment whose floors lie in
-// [0, R-2] on every axis is inside the box (u >= 0 <=> x >= lo exactly; u < R-1
-// keeps x below hi by a cell), so its points skip the box test and the clamp.
-__device__ __forceinline__ void cell_floors(const GridConst &g, const float X[3], int f[3]) {
-#pragma unroll
-  for (int a = 0; a < 3; ++a) f[a] = (int)floorf(__fmul_rn(__fsub_rn(X[a], g.lo[0][a]), g.s[0][a]));
-}
-
-// the fine test from the endpoints' cell floors (ia: first point, ib: last point or any later one)
-__device__ __forceinline__ int segment_test_floors(const GridConst &g, const uint32_t *__restrict__ mask3,
-                                                   const int ia[3], const int ib[3]) {
-  const int R = g.res;
-  int c[3];
-  bool interior = true;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const int lo = min(ia[a], ib[a]), hi = max(ia[a], ib[a]);
-    if (hi - lo > kFineWin - 1) return 2;     // longer than the mask's window: evaluate
-    if (hi < 0 || lo > R) return 0;          // every point outside the box on this axis
-    interior = interior && lo >= 0 && hi <= R - 2;
-    c[a] = min(max(lo, 0), R - 1);
-  }
-  const uint32_t q = (uint32_t)c[0] + (uint32_t)R * ((uint32_t)c[1] + (uint32_t)R * (uint32_t)c[2]);
-  if (!((__ldg(mask3 + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
-  if (!interior) return 2;
-  // solid window (mask3and, R^3 bits after mask3): every cell the points can fall in is
-  // occupied, so every point is a member (subject only to k < ke and m < far)
-  const uint32_t *mask3and = mask3 + ((((int64_t)R * R * R + 31) / 32 + 63) / 64) * 64;
-  if (NACC_MARCH_SOLID && ((__ldg(mask3and + (q >> 5)) >> (q & 31u)) & 1u)) return 3;
-  return 1;
-}
-
-__device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ mask3,
-                                                 const float A[3], const float B[3]) {
-  int ia[3], ib[3];
-  cell_floors(g, A, ia);
-  cell_floors(g, B, ib);
-  return segment_test_floors(g, mask3, ia, ib);
-}
-
 // P(k) for a point known to lie inside the (single) level box by a margin far
 // above the fp32 error: the box test is skipped, the rest is the normative
 // sequence of occupied()
 __device__ __forceinline__ bool occupied_interior(const GridConst &g, const uint32_t *__restrict__ bits, float m,
-                                                  float ox, float oy, float oz, float dx, float dy, float dz) {
+                                                  float ox, float oy, float oz, float dx, float dy, float dz,
+                                                  int l = 0) {
   const float x = __fmaf_rn(m, dx, ox), y = __fmaf_rn(m, dy, oy), z = __fmaf_rn(m, dz, oz);
   const int R = g.res;
-  // inside the box by >= 4e-3 cells (segment_test's margin, far above the fp32
-  // error of u), so floor(u) is already in [0, R-1]: the clamp is the identity
+  // the segment test proved every point in level l's box with floor(u) in [0, R-2] (and
+  // outside the finer box), so l* = l and the clamp is the identity
 #if NACC_MARCH_MAGICFLOOR
   // floor of u in [0, 2^23) without the conversion unit: u + 2^23 rounded toward zero holds
   // floor(u) in its mantissa (bit-identical to floorf there)
-  const int ix = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(x, g.lo[0][0]), g.s[0][0]), 8388608.0f)) - 0x4B000000;
-  const int iy = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(y, g.lo[0][1]), g.s[0][1]), 8388608.0f)) - 0x4B000000;
-  const int iz = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(z, g.lo[0][2]), g.s[0][2]), 8388608.0f)) - 0x4B000000;
+  const int ix = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(x, g.lo[l][0]), g.s[l][0]), 8388608.0f)) - 0x4B000000;
+  const int iy = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(y, g.lo[l][1]), g.s[l][1]), 8388608.0f)) - 0x4B000000;
+  const int iz = __float_as_int(__fadd_rz(__fmul_rn(__fsub_rn(z, g.lo[l][2]), g.s[l][2]), 8388608.0f)) - 0x4B000000;
 #else
-  const int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[0][0]), g.s[0][0]));
-  const int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[0][1]), g.s[0][1]));
-  const int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[0][2]), g.s[0][2]));
+  const int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[l][0]), g.s[l][0]));
+  const int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[l][1]), g.s[l][1]));
+  const int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[l][2]), g.s[l][2]));
 #endif
-  const uint32_t q = (uint32_t)ix + (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
+  const uint32_t q = (uint32_t)l * (uint32_t)(R * R * R) + (uint32_t)ix +
+                     (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
   return (__ldg(bits + (q >> 5)) >> (q & 31u)) & 1u;
 }
 
@@ -440,13 +449,16 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
     } else if (kSkip) {
       const int ks = k0 + lane * kSeg;
       bool flag = false;
-      int code = 0;
+      int code = 0, lvl = 0;
       if (ks < ke) {
         const int kl = min(ks + kSeg - 1, ke - 1);
         const float ma = lattice_mid<kCone>(p, s, tab, ks), mb = lattice_mid<kCone>(p, s, tab, kl);
         const float A[3] = {__fmaf_rn(ma, s.dx, s.ox), __fmaf_rn(ma, s.dy, s.oy), __fmaf_rn(ma, s.dz, s.oz)};
         const float B[3] = {__fmaf_rn(mb, s.dx, s.ox), __fmaf_rn(mb, s.dy, s.oy), __fmaf_rn(mb, s.dz, s.oz)};
-        code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, mask3, A, B) : segment_test<kL1>(g, mask2, M, A, B);
+        code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, mask3, A, B)
+                                          : segment_test<kL1>(g, mask2, M, mask3, A, B);
+        lvl = code >> 4;  // cascades: the level every point of the segment lies in
+        code &= 15;
         flag = code != 0;
 #if NACC_MARCH_PREFETCH
         if (code == 1) {  // interior segment: warm L1 with the bit words its points will read
@@ -467,18 +479,21 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 #endif
       }
       const unsigned F = __ballot_sync(kFull, flag);
-      if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : (code == 3 ? 0x300 : 0));
+      if (flag)
+        seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : (code == 3 ? 0x300 : 0)) | (lvl << 12);
       __syncwarp();
       nseg = __popc(F);
     }
     // lane (lane % kSeg) of segment list entry idx: its point k and P(k)
     auto eval = [&](int idx, int &k) -> bool {
       bool interior = false, solid = false;
+      int lv = 0;
       if (kSkip) {
         const int e = idx < nseg ? seglist[idx] : 0;
         k = idx < nseg ? k0 + (e & 0xff) * kSeg + (lane % kSeg) : ke;
-        interior = kL1 && (e & 0x100);
-        solid = kL1 && (e & 0x200);
+        interior = (e & 0x100) != 0;
+        solid = (e & 0x200) != 0;
+        lv = kL1 ? 0 : (e >> 12) & 7;
       } else {
         k = k0 + lane;
       }
@@ -487,7 +502,7 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
         const float m = lattice_mid<kCone>(p, s, tab, k);
         if (m < s.far_r)
           pred = solid ? true
-                       : (interior ? occupied_interior(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz)
+                       : (interior ? occupied_interior(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz, lv)
                                    : occupied<kL1>(g, bits, m, s.ox, s.oy, s.oz, s.dx, s.dy, s.dz));
       }
       return pred;
