@@ -225,7 +225,7 @@ struct Items {
 // fp64 warp-level segmented scans (no shared memory, no block barriers) carry
 // the open ray across chunks.  Extra warps zero the outputs of empty rays.
 #ifndef NACC_RENDER_TILE
-#define NACC_RENDER_TILE 256
+#define NACC_RENDER_TILE 512  // samples per warp tile (A/B on 3.8 M samples: 128 / 256 / 512 / 768 / 1024 -> fwd+bwd 177 / 151 / 141 / 157 / 140 us)
 #endif
 #ifndef NACC_RENDER_BPS
 #define NACC_RENDER_BPS 4  // blocks per SM of the tile kernels (A/B: 2 / 3 / 4 -> bwd 88.4 / 81.7 / 79.7 us)
