@@ -348,16 +348,21 @@ def run_extras(device, reps=20):
     import paper_2305_04966_b200 as N
     from paper_2305_04966_b200 import harness as H
 
-    def timed(fn, n=reps):
+    def timed(fn, n=reps, batches=5):
+        """median over batches of the mean per-call device time (one slow batch does not move it)"""
         fn()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(n):
-            out = fn()
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / n, out
+        per = max(n // batches, 2)
+        res = []
+        for _ in range(batches):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(per):
+                out = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            res.append(e0.elapsed_time(e1) / per)
+        return float(np.median(res)), out
 
     out = {}
     peak, _ = measured_peaks()
