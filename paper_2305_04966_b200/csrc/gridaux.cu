@@ -11,9 +11,9 @@
 //     of every level, the OR of the fine bits of macro cells m + {0,1}^3,
 //     i.e. of the fine cells [4m, 4m + 8)^3 clipped to the level;
 //   mask3 (every grid with skipping; per level): for every fine cell c the OR of
-//     the fine bits of cells c + {0,1,2}^3 clipped to the grid, at the fine
-//     resolution (the march's segment test for 8-point segments, which span at
-//     most 3 cells per axis);
+//     the fine bits of cells c + {0..W-1}^3 (W = kFineWin) clipped to the level,
+//     at the fine resolution (the march's segment test: a 16-point segment spans
+//     at most 5 cells per axis on the CFG lattices);
 #include "common.cuh"
 
 namespace nacc {
@@ -160,7 +160,7 @@ __global__ void mask2_kernel(uint32_t *__restrict__ bits, int levels, int R, int
 }
 
 // thread per fine cell (one level): the OR (kAnd = false) or the AND (kAnd = true) of the
-// bits of cells c + {0,1,2}^3; cells outside the grid count as empty (an AND window that
+// bits of cells c + {0..W-1}^3; cells outside the grid count as empty (an AND window that
 // leaves the grid is 0)
 template <bool kAnd>
 __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits, int levels, int R, int64_t off) {

@@ -23,7 +23,7 @@
 #define NACC_MARCH_FLATW 0  // build parameter: write a tile's samples as one run (vs ray by ray)
 #endif
 #ifndef NACC_MARCH_FINEMASK
-#define NACC_MARCH_FINEMASK 1  // build parameter: single-level segment test on the fine 3-cell dilated mask
+#define NACC_MARCH_FINEMASK 1  // build parameter: segment test on the fine window masks (0: macro test only)
 #endif
 #ifndef NACC_MARCH_SHAREDENDS
 #define NACC_MARCH_SHAREDENDS 1  // build parameter: segment ends from the next lane's start (fine mask)
@@ -127,15 +127,17 @@ static_assert(NACC_MARCH_SEG_CASCADE == 8 || NACC_MARCH_SEG_CASCADE == 16, "segm
 constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
 constexpr float kSegEps = 1e-3f;
 
-// Single-level grids: the same decision at the fine resolution.  The points of
-// a segment have positions x and cell coordinates u = (x - lo) * s computed by
+// The same decision at the fine resolution (reading #22).  The points of a
+// segment have positions x and cell coordinates u = (x - lo) * s computed by
 // the normative fp32 ops of P(k), each of which is monotone in m (RN rounding
 // is monotone), so every point's floor(u) lies between the endpoints' floors,
-// exactly, per axis.  With at most 3 cells per axis that range lies in
-// c + {0,1,2}^3, c = the clamped low corner, and mask3[c] (the OR of those 27
-// fine bits) being 0 proves no point is emitted.  A segment whose floors lie in
-// [0, R-2] on every axis is inside the box (u >= 0 <=> x >= lo exactly; u < R-1
-// keeps x below hi by a cell), so its points skip the box test and the clamp.
+// exactly, per axis.  With at most W = kFineWin cells per axis that range lies
+// in c + {0..W-1}^3, c = the clamped low corner, and mask3[c] (the OR of those
+// W^3 fine bits) being 0 proves no point is emitted.  A segment whose floors lie
+// in [0, R-2] on every axis is inside the box (u >= 0 <=> x >= lo exactly;
+// u < R-1 keeps x below hi by a cell), so its points skip the box test and the
+// clamp.  Cascades run this on level l once both ends are known to lie in l and
+// the segment misses the finer box (segment_test below).
 __device__ __forceinline__ void cell_floors(const GridConst &g, const float X[3], int f[3], int l = 0) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) f[a] = (int)floorf(__fmul_rn(__fsub_rn(X[a], g.lo[l][a]), g.s[l][a]));
