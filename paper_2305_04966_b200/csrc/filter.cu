@@ -11,7 +11,10 @@ namespace nacc {
 // S_i = Σ_{j<i} σ_j δ_j in fp64 exactly as the definition (σ_j δ_j is exact in
 // fp64, so this is the sequential sum), stopping at the first S_i > L; only the
 // kept prefix plus a few samples are read.  Each block also reduces its cuts.
-constexpr int kFiltRays = 256;
+#ifndef NACC_FILTER_RAYS
+#define NACC_FILTER_RAYS 256  // build parameter: rays per copy block / group sum
+#endif
+constexpr int kFiltRays = NACC_FILTER_RAYS;
 
 
 // Small blocks (two warps) and per-warp atomic adds into the 256-ray group

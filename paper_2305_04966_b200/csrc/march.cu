@@ -549,7 +549,10 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 #ifndef NACC_MARCH_RPT
 #define NACC_MARCH_RPT 8  // build parameter: rays per tile of the uniform single-level march
 #endif
-constexpr int kFWarps = 4, kFRaysPerWarp = NACC_MARCH_RPT, kFKCap = NACC_MARCH_KCAP;
+#ifndef NACC_MARCH_WARPS
+#define NACC_MARCH_WARPS 4  // build parameter: warps per block of the fused march
+#endif
+constexpr int kFWarps = NACC_MARCH_WARPS, kFRaysPerWarp = NACC_MARCH_RPT, kFKCap = NACC_MARCH_KCAP;
 // cone lattices and cascades give long rays (hundreds of samples): half the rays per tile
 constexpr int fused_rpt(bool cone, bool l1) { return (cone || !l1) ? kFRaysPerWarp / 2 : kFRaysPerWarp; }
 #ifndef NACC_MARCH_PIPE
