@@ -237,7 +237,7 @@ struct Items {
 #define NACC_RENDER_RAYCACHE 1  // build parameter: backward loads per-ray constants once per run of the ray
 #endif
 #ifndef NACC_RENDER_F32A
-#define NACC_RENDER_F32A 1  // build parameter: alpha = -expm1f(-s) in fp32 (DESIGN reading #23)
+#define NACC_RENDER_F32A 0  // build parameter: alpha = -expm1f(-s) in fp32 (experiment)
 #endif
 // e^{-s} of one interval (1 - alpha)
 __device__ __forceinline__ double interval_ea(double s) {
