@@ -378,7 +378,10 @@ __global__ void tex_samples_kernel(cudaTextureObject_t tex, int R, float lo, flo
 // independent texture fetches in flight)
 constexpr int kTexQuads = 1;  // quads of samples per thread and iteration (2 measured slower)
 
-__global__ void tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, float hi, int contracted,
+#ifndef NACCX_TEX_MINB
+#define NACCX_TEX_MINB 1  // build parameter: min resident 256-thread blocks per SM (register cap)
+#endif
+__global__ void __launch_bounds__(256, NACCX_TEX_MINB) tex_sigma4_kernel(cudaTextureObject_t tex, int R, float lo, float hi, int contracted,
                                   const float *__restrict__ o, const float *__restrict__ d,
                                   const float *__restrict__ t0, const float *__restrict__ t1,
                                   const int32_t *__restrict__ rid, int64_t n, const int64_t *__restrict__ n_dev,
