@@ -103,6 +103,13 @@ def philox4x32_10(ctr, key):
 
 
 # --------------------------------------------------------------------------- geometry
+def lattice_point(near, step, k, half):
+    f = lib().or_lattice_point
+    f.restype = C.c_float
+    f.argtypes = [C.c_float, C.c_float, C.c_int64, C.c_int32]
+    return float(f(float(near), float(step), int(k), int(half)))
+
+
 def ray_aabb(o, d, lo, hi, near=0.0, far=np.inf):
     """O1 slab test; returns (t_enter, t_exit) or None."""
     arr = lambda v: (C.c_double * 3)(*[float(x) for x in v])
@@ -258,7 +265,8 @@ def accumulate(packed_info, weights, values=None, C_=1):
     pi = _i64(packed_info).reshape(-1, 2)
     n = pi.shape[0]
     if values is not None:
-        values = _f64(values).reshape(len(weights), -1)
+        values = _f64(values)
+        values = values.reshape(len(weights), -1) if values.ndim != 2 else values
         C_ = values.shape[1]
     out = np.zeros((n, C_))
     lib().or_accumulate(_p(pi), C.c_int64(n), _p(_f64(weights)), _p(values), C.c_int32(C_), _p(out))

@@ -184,6 +184,32 @@ static float ray_near(const or_march *p, const float *t_min, int64_t r) {
   return nr;
 }
 
+/* fp32 rounding (to nearest, ties to even) of the exact real a + b, where a and
+ * b are doubles (reading #3: lattice values are the fp32 of the exact value).
+ * The fp64 sum s may itself be rounded; a double rounding differs from the
+ * single one only when s lands exactly on a tie between two fp32 neighbours
+ * while the exact sum does not, so the tie is broken by the sign of the exact
+ * error e = (a + b) - s (Knuth's TwoSum). */
+static float f32_exact_sum(double a, double b) {
+  double s = a + b;
+  double a1 = s - b, b1 = s - a1;
+  double e = (a - a1) + (b - b1);
+  float r = (float)s;
+  if (e != 0.0) {
+    float lo = (float)s, hi = (float)s;
+    if ((double)r > s) lo = nextafterf(r, -INFINITY);
+    else if ((double)r < s) hi = nextafterf(r, INFINITY);
+    if (lo != hi && s - (double)lo == (double)hi - s) r = e > 0.0 ? hi : lo;
+  }
+  return r;
+}
+
+/* Uniform lattice value near_r + (k + half/2)·Δt rounded once to fp32 (reading
+ * #1, #3): t_k for half = 0, the midpoint m_k for half = 1. */
+float or_lattice_point(float near_r, float step, int64_t k, int32_t half) {
+  return f32_exact_sum((double)near_r, ((double)k + 0.5 * (double)half) * (double)step);
+}
+
 /* One ray.  Returns the number of emitted intervals; writes them when t0 != NULL. */
 static int64_t march_ray(const gctx *c, const uint8_t *occ, const or_march *p, const float o[3],
                          const float d[3], float near_r, float far_r, int brute, int32_t rid,
@@ -214,15 +240,17 @@ static int64_t march_ray(const gctx *c, const uint8_t *occ, const or_march *p, c
       k_begin = kb > 0.0 ? (int64_t)kb : 0;
       if (ke < (double)k_end) k_end = ke > 0.0 ? (int64_t)ke : 0;
     }
+    /* lattice indices k < 2^24 (header of nacc.h); (k + 1/2)·Δt and k·Δt are exact
+     * fp64 products (25 x 24 bits), the sums with near_r are rounded once to fp32 */
     for (int64_t k = k_begin; k < k_end; ++k) {
-      double tk = nr + (double)k * dt; /* exact in fp64 (asserted by a test) */
+      double tk = nr + (double)k * dt;
       if (brute && tk > T_stop) break;
-      float m = (float)(nr + ((double)k + 0.5) * dt);
+      float m = or_lattice_point(near_r, p->step, k, 1);
       if (!(m < far_r)) break;
       if (member(c, occ, m, o, d)) {
         if (t0) {
-          t0[n] = (float)tk;
-          t1[n] = (float)(nr + (double)(k + 1) * dt);
+          t0[n] = or_lattice_point(near_r, p->step, k, 0);
+          t1[n] = or_lattice_point(near_r, p->step, k + 1, 0);
           ray_id[n] = rid;
         }
         ++n;

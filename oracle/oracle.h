@@ -76,6 +76,11 @@ typedef struct {
   uint64_t seed;
 } or_march;
 
+/* Uniform lattice value fp32(near_r + (k + half/2)·Δt), the exact real rounded
+ * once (reading #3): t_k (half = 0) or the midpoint m_k (half = 1).  Pinned
+ * against exact rationals, including fp64 double-rounding ties. */
+float or_lattice_point(float near_r, float step, int64_t k, int32_t half);
+
 /* O2-O4: every lattice interval whose midpoint lies in an occupied cell, in
  * ray/t order ("sample as interval", "packed tensor"; P:240 skipping).
  * occ: uint8 per cell, level-major, x-fastest (reading #27).

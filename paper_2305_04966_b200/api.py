@@ -169,6 +169,11 @@ def sampling_occgrid(rays_o: torch.Tensor, rays_d: torch.Tensor, grid: GridSpec,
             raise ValueError("sync=False needs a capacity")
         return PackedSamples(packed, t0, t1, rid, total, status)
     N = int(total.item())
+    st = int(status.item())
+    if st not in (L.NACC_OK, L.NACC_ERR_INSUFFICIENT_CAPACITY):
+        # e.g. the shared cone lattice overflowed its 2^20-entry table: the samples would be truncated
+        raise L.NaccError(st, "nacc_sampling_occgrid: device status (the shared cone lattice is longer than "
+                              "2^20 intervals: raise step or cone_angle, or lower far_plane)")
     if N > cap:
         t0 = torch.empty(max(N, 1), dtype=torch.float32, device=dev)
         t1 = torch.empty(max(N, 1), dtype=torch.float32, device=dev)

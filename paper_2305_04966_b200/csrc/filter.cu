@@ -35,14 +35,16 @@ constexpr int kCutBatch = NACC_FILTER_BATCH;
 __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
                                                                  const float *__restrict__ t0,
                                                                  const float *__restrict__ t1,
-                                                                 const float *__restrict__ sigma, double L,
-                                                                 int32_t *__restrict__ cut_out,
+                                                                 const float *__restrict__ sigma, int64_t n_samples,
+                                                                 double L, int32_t *__restrict__ cut_out,
                                                                  int64_t *__restrict__ block_sums) {
   const int64_t r = (int64_t)blockIdx.x * kCutThreads + threadIdx.x;
   int64_t cut = 0;
   if (r < n_rays) {
     const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
-    const int64_t st = pi.x, cnt = pi.y;
+    // a packed_info written past the input's capacity (device-count mode after an overflowed
+    // march) is clamped to the n_samples readable samples; the result is invalid but in bounds
+    const int64_t st = min((int64_t)pi.x, n_samples), cnt = min((int64_t)(pi.x + pi.y), n_samples) - st;
     double S = 0.0;
     cut = cnt;
     int nb = 4;
@@ -83,23 +85,34 @@ __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *
 // Needs 32-byte-aligned t0 / t1 / sigma; reads stay inside the last sector of the ray.
 __global__ void __launch_bounds__(kCutThreads) filter_cut_sector_kernel(
     const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
-    const float *__restrict__ t1, const float *__restrict__ sigma, double L, int32_t *__restrict__ cut_out,
-    int64_t *__restrict__ block_sums) {
+    const float *__restrict__ t1, const float *__restrict__ sigma, int64_t n_samples, double L,
+    int32_t *__restrict__ cut_out, int64_t *__restrict__ block_sums) {
   const int64_t r = (int64_t)blockIdx.x * kCutThreads + threadIdx.x;
   int64_t cut = 0;
   if (r < n_rays) {
     const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
-    const int64_t st = pi.x, e = pi.x + pi.y;
+    const int64_t st = min((int64_t)pi.x, n_samples), e = min((int64_t)(pi.x + pi.y), n_samples);  // clamped as above
     double S = 0.0;
-    cut = pi.y;
+    cut = e - st;
     for (int64_t q = st & ~(int64_t)7; q < e; q += 8) {
-      const float4 *pa = reinterpret_cast<const float4 *>(t0 + q), *pb = reinterpret_cast<const float4 *>(t1 + q),
-                   *pc = reinterpret_cast<const float4 *>(sigma + q);
-      const float4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1), c0 = __ldg(pc),
-                   c1 = __ldg(pc + 1);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-      const float c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      float a[8], b[8], c[8];
+      if (q + 8 <= n_samples) {  // whole sector inside the arrays
+        const float4 *pa = reinterpret_cast<const float4 *>(t0 + q), *pb = reinterpret_cast<const float4 *>(t1 + q),
+                     *pc = reinterpret_cast<const float4 *>(sigma + q);
+        const float4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1), c0 = __ldg(pc),
+                     c1 = __ldg(pc + 1);
+        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+        b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+        c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w; c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
+      } else {  // the arrays' last, partial sector: element loads (no padding is required)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool in = q + j < n_samples;
+          a[j] = in ? __ldg(t0 + q + j) : 0.f;
+          b[j] = in ? __ldg(t1 + q + j) : 0.f;
+          c[j] = in ? __ldg(sigma + q + j) : 0.f;
+        }
+      }
       bool done = false;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -173,7 +186,7 @@ __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
   if (t < nr) {
     reinterpret_cast<longlong2 *>(packed_out)[r0 + t] = make_longlong2(out, c);
     s_out[t] = out;
-    s_in[t] = __ldg(packed_info + 2 * (r0 + t));
+    s_in[t] = __ldg(packed_info + 2 * (r0 + t));  // cut <= the clamped count: sources stay < n_samples
     if (t == nr - 1) s_out[nr] = out + c;
   }
   __syncthreads();
@@ -268,10 +281,10 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)nb, stream));
   if (NACC_FILTER_SECTOR && aligned(t0, 32) && aligned(t1, 32) && aligned(sigma, 32))
     filter_cut_sector_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-        packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts, bsums);
+        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
   else
     filter_cut_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-        packed_info, n_rays, t0, t1, sigma, neg_log_eps, cuts, bsums);
+        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
   block_sums_scan_kernel<<<1, 1024, 0, stream>>>(bsums, nb, total);
   filter_copy_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, cuts, bsums, total, capacity,
                                                              packed_info_out, capacity > 0 ? t0_out : nullptr, t1_out,

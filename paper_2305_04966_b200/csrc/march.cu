@@ -298,10 +298,13 @@ __device__ __forceinline__ RaySetup ray_setup(const GridConst &g, const MarchCon
   return s;
 }
 
-// k range of the uniform lattice that can hold emitted intervals (±2 slack)
+// k range of the uniform lattice that can hold emitted intervals: ±2 steps of
+// slack plus 2^-20 of the index itself, which covers the relative error of the
+// fp32 slab and of this division (a few ulps) up to the 2^24 index cap
 __device__ __forceinline__ void uniform_k_range(const RaySetup &s, const MarchConst &p, int64_t &kb, int64_t &ke) {
-  const float fb = floorf((s.t_lo - s.near_r) * p.inv_step - 0.5f) - 2.0f;
-  const float fe = ceilf((s.t_hi - s.near_r) * p.inv_step) + 3.0f;
+  const float xb = (s.t_lo - s.near_r) * p.inv_step, xe = (s.t_hi - s.near_r) * p.inv_step;
+  const float fb = floorf(xb - 0.5f - fabsf(xb) * 0x1p-20f) - 2.0f;
+  const float fe = ceilf(xe + fabsf(xe) * 0x1p-20f) + 3.0f;
   const float cap = (float)(1 << 24);
   kb = fb > 0.0f ? (int64_t)fminf(fb, cap) : 0;
   ke = fe > 0.0f ? (int64_t)fminf(fe, cap) : 0;
@@ -367,6 +370,30 @@ __global__ void cone_table_kernel(MarchConst p, ConeHeader *hdr, float *__restri
   hdr->overflow = overflow;
 }
 
+// Uniform lattice midpoint m_k = fp32(near_r + (k + 1/2)Δt), the exact value
+// rounded once (reading #3).  For k < 2^23, k + 1/2 is an fp32 and one fmaf is
+// that rounding.  Above (lattice indices go up to 2^24), (k + 1/2)Δt is an
+// exact fp64 product (25 x 24 bits) and the fp64 sum with near_r is rounded
+// to fp32 with the tie fixed by the sign of its TwoSum error (a double rounding
+// differs from the single one only on an exact fp32 tie).
+__device__ __noinline__ float lattice_mid_wide(int k, float step, float near_r) {
+  const double a = (double)near_r, b = __dmul_rn((double)k + 0.5, (double)step);
+  const double s = __dadd_rn(a, b);
+  const double a1 = __dsub_rn(s, b), b1 = __dsub_rn(s, a1);
+  const double e = __dadd_rn(__dsub_rn(a, a1), __dsub_rn(b, b1));
+  float r = __double2float_rn(s);
+  if (e != 0.0) {
+    const float lo = __double2float_rd(s), hi = __double2float_ru(s);
+    if (lo != hi && __dsub_rn(s, (double)lo) == __dsub_rn((double)hi, s)) r = e > 0.0 ? hi : lo;
+  }
+  return r;
+}
+
+__device__ __forceinline__ float lattice_mid_uniform(int k, float step, float near_r) {
+  if (k < (1 << 23)) return __fmaf_rn((float)k + 0.5f, step, near_r);
+  return lattice_mid_wide(k, step, near_r);
+}
+
 // midpoint of lattice interval k (uniform or cone table)
 template <bool kCone>
 __device__ __forceinline__ float lattice_mid(const MarchConst &p, const RaySetup &s, const float *__restrict__ tab,
@@ -376,7 +403,7 @@ __device__ __forceinline__ float lattice_mid(const MarchConst &p, const RaySetup
     const float dt = fminf(fmaxf(__fmul_rn(ta, p.cone), p.step), p.max_step);
     return __fadd_rn(ta, __fmul_rn(0.5f, dt));
   }
-  return __fmaf_rn((float)k + 0.5f, p.step, s.near_r);
+  return lattice_mid_uniform(k, p.step, s.near_r);
 }
 
 template <bool kCone>

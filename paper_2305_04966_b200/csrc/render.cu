@@ -415,7 +415,7 @@ __device__ __forceinline__ void render_fwd_out(const SegM &v, int64_t r, float *
 
 template <bool kVec>
 __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
-    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
     float *__restrict__ depth, double *__restrict__ ctx) {
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
   }
   // persistent warps stride over the tiles in use (N from packed_info: the launch is sized by
   // the resident capacity, not by the arrays' capacity)
-  const int64_t N = packed_end(packed_info, n_rays);
+  const int64_t N = min(packed_end(packed_info, n_rays), n_samples);  // in bounds after an overflowed march
   for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
     const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
     const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
@@ -534,13 +534,13 @@ __global__ void __launch_bounds__(256) ray_grad_kernel(int64_t n_rays, const dou
 
 template <bool kVec>
 __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
-    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_wtiles,
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, const float4 *__restrict__ gcv, const double2 *__restrict__ gq,
     float *__restrict__ g_sigma, float *__restrict__ g_rgb) {
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t N = packed_end(packed_info, n_rays);
+  const int64_t N = min(packed_end(packed_info, n_rays), n_samples);  // in bounds after an overflowed march
   for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
     const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
     const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
@@ -896,10 +896,10 @@ nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, i
                      aligned(ray_id, 16);
     const unsigned blocks = resident_blocks(ceil_div(warps * 32, 256));
     if (vec)
-      render_fwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+      render_fwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
                                                                rgb, neg_log_eps, color, opacity, depth, ctx);
     else
-      render_fwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+      render_fwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
                                                                 rgb, neg_log_eps, color, opacity, depth, ctx);
   } else {
     render_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, rgb,
@@ -931,10 +931,10 @@ nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, i
                      aligned(ray_id, 16) && aligned(g_sigma, 16) && (!g_rgb || aligned(g_rgb, 16));
     const unsigned blocks = resident_blocks(ceil_div(n_wtiles * 32, 256));
     if (vec)
-      render_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+      render_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
                                                                rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb);
     else
-      render_bwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_wtiles, t0, t1, sigma,
+      render_bwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
                                                                 rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb);
     count_launch(1);
   } else {

@@ -96,3 +96,25 @@ def test_early_stop_constant():
     t0 = np.arange(20, dtype=np.float32)
     counts, _ = O.filter_counts(pk, t0, t0 + 1, np.ones(20, np.float32), ex["neg_log_eps"])
     assert counts.tolist() == [math.ceil(ex["neg_log_eps"])]
+
+
+@pytest.mark.parametrize("ex", _G["accumulate"], ids=lambda e: e["cite"][:6])
+def test_accumulate(ex):
+    """accumulate_along_rays (Alg. 1 outputs) on the S:410-418 worked examples."""
+    n = len(ex["weights"])
+    pk = np.array([[0, n]], np.int64)
+    w = np.array(ex["weights"], np.float64)
+    v = np.array(ex["values"], np.float64).reshape(n, 3)
+    out = O.accumulate(pk, w, v)
+    assert np.allclose(out[0], ex["out"], rtol=1e-15, atol=0)
+    op = O.accumulate(pk, w, None)
+    assert op[0, 0] == pytest.approx(ex["opacity"], rel=1e-15, abs=0)
+
+
+@pytest.mark.parametrize("ex", _G["accumulate_bwd"], ids=lambda e: e["cite"][:6])
+def test_accumulate_bwd(ex):
+    n = len(ex["weights"])
+    pk = np.array([[0, n]], np.int64)
+    gw, gv = O.accumulate_bwd(pk, ex["weights"], np.array(ex["values"], np.float64), np.array([ex["g_out"]], np.float64))
+    assert np.allclose(gw, ex["g_weights"], rtol=1e-15, atol=0)
+    assert np.allclose(gv, ex["g_values"], rtol=1e-15, atol=0)

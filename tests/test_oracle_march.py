@@ -165,6 +165,67 @@ def test_lattice_values_exact_in_fp64():
                 assert Fraction(fp) == exact
 
 
+def _f32_round_exact(q: Fraction) -> float:
+    """Round an exact rational to the nearest fp32, ties to even -- by exact comparison with the
+    two fp32 neighbours, no floating-point arithmetic (IEEE 754 roundTiesToEven)."""
+    lo = float(np.float32(float(q)))  # a neighbour within one ulp
+    a = np.float32(lo)
+    while Fraction(float(a)) > q:
+        a = np.nextafter(a, np.float32(-np.inf))
+    while Fraction(float(np.nextafter(a, np.float32(np.inf)))) <= q:
+        a = np.nextafter(a, np.float32(np.inf))
+    b = np.nextafter(a, np.float32(np.inf))
+    da, db = q - Fraction(float(a)), Fraction(float(b)) - q
+    if da < db or (da == db and (int(a.view(np.uint32)) & 1) == 0):
+        return float(a)
+    return float(b)
+
+
+def test_lattice_point_is_the_exact_value_rounded_once():
+    """Reading #3: t_k and m_k are fp32(near + (k + h/2)·Δt) of the exact real, for every index the
+    ABI admits (k < 2^24).  Includes k in [2^22, 2^24), where k + 1/2 is not an fp32, and anchors
+    that make the fp64 sum land on an fp32 tie (a double rounding would go to even)."""
+    rng = np.random.default_rng(41)
+    cases = [(np.float32(2.0**-60), np.float32(2.0**-10), (1 << 23) + 2, 1),  # tie: exact rounds up
+             (np.float32(-(2.0**-60)), np.float32(2.0**-10), (1 << 23) + 3, 1),  # tie: exact rounds down
+             (np.float32(0.0), np.float32(2.0**-10), (1 << 23) + 2, 1)]  # a real tie: to even
+    for step in (np.float32(1e-2), np.float32(math.sqrt(3) / 1024), np.float32(2.0**-10)):
+        for near in (np.float32(0.0), np.float32(0.2), np.float32(1e-30), np.float32(-3.5), np.float32(2.0**-70)):
+            for k in list(rng.integers(1 << 22, 1 << 24, 60)) + list(rng.integers(0, 1 << 20, 20)) + [(1 << 24) - 1]:
+                cases += [(near, step, int(k), 0), (near, step, int(k), 1)]
+    n_ties = 0
+    for near, step, k, h in cases:
+        exact = Fraction(float(near)) + (k + Fraction(h, 2)) * Fraction(float(step))
+        want = _f32_round_exact(exact)
+        got = O.lattice_point(near, step, k, h)
+        assert got == want, (near, step, k, h, got, want)
+        naive = float(np.float32(float(near) + (k + h / 2) * float(step)))
+        n_ties += naive != want
+    assert n_ties >= 2  # the tie cases above do defeat plain fp64 rounding
+
+
+def test_far_origin_march_equals_brute_force():
+    """Rays whose box crossing sits at lattice indices in [2^22, 2^24) (t ≈ 4e3-1.6e4 at Δt = 2^-10):
+    the fast oracle equals the brute force over every k, with the exact midpoints above."""
+    rng = np.random.default_rng(42)
+    res, roi = 8, (-0.5, -0.5, -0.5, 0.5, 0.5, 0.5)
+    occ = (rng.random(res**3) < 0.4).astype(np.uint8)
+    n = 24
+    dist = rng.uniform(5000.0, 15000.0, n)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    tgt = rng.uniform(-0.4, 0.4, (n, 3))
+    o = (tgt - dist[:, None] * d).astype(np.float32)
+    d = d.astype(np.float32)
+    for near in (0.0, float(np.float32(2.0**-60))):
+        kw = dict(step=float(np.float32(2.0**-10)), near=near)
+        a = O.march(occ, 1, res, roi, o, d, **kw)
+        b = O.march(occ, 1, res, roi, o, d, brute=True, **kw)
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+        assert a[0][:, 1].sum() > 200
+
+
 @pytest.mark.parametrize("levels,res,cone,strat", [(1, 4, 0, 0), (1, 8, 0, 1), (1, 16, 0, 0), (2, 8, 0, 0),
                                                    (3, 6, 0, 1), (1, 8, 1, 0), (3, 8, 1, 0), (2, 16, 1, 0)])
 def test_fast_march_equals_brute_force(levels, res, cone, strat):

@@ -263,3 +263,52 @@ def test_oracle_render_deterministic_across_threads():
     for k in a:
         assert np.array_equal(a[k], b[k])
     assert np.array_equal(ga[0], gb[0]) and np.array_equal(ga[1], gb[1])
+
+
+def test_accumulate_equals_render_fwd_outputs():
+    """Pin or_accumulate to the independently pinned O6 renderer (Eq. 2 closed forms, S:416-418
+    goldens): accumulating O6's own weights with rgb, ones and interval midpoints must give O6's
+    colour, opacity and depth·opacity on ragged fuzz inputs."""
+    pk, t0, t1, rid, sig, rgb = W.ragged_samples(400, seed=21)
+    for eps in (math.inf, L_EPS):
+        ref = O.render_fwd(pk, t0, t1, sig, rgb, neg_log_eps=eps)
+        w = ref["weights"]
+        col = O.accumulate(pk, w, rgb)
+        assert np.allclose(col, ref["color"], rtol=1e-12, atol=1e-15)
+        op = O.accumulate(pk, w, None)[:, 0]
+        assert np.allclose(op, ref["opacity"], rtol=1e-12, atol=1e-15)
+        mid = (t0.astype(np.float64) + t1.astype(np.float64)) / 2.0
+        nd = O.accumulate(pk, w, mid[:, None])[:, 0]
+        assert np.allclose(nd, ref["depth"] * np.maximum(ref["opacity"], 1e-10), rtol=1e-10, atol=1e-15)
+
+
+def test_accumulate_bwd_finite_differences():
+    """or_accumulate_bwd against central finite differences of or_accumulate (a linear map, so the
+    difference quotient is exact up to rounding)."""
+    pk, t0, t1, rid, sig, rgb = W.ragged_samples(60, seed=22)
+    rng = np.random.default_rng(23)
+    n = len(t0)
+    w = rng.uniform(0, 0.2, n)
+    g = rng.normal(size=(60, 3))
+    gw, gv = O.accumulate_bwd(pk, w, rgb, g)
+
+    def f(wv, vv):
+        return float((O.accumulate(pk, wv, vv) * g).sum())
+
+    h = 1e-3
+    for q in rng.choice(n, 40, replace=False):
+        wp, wm = w.copy(), w.copy()
+        wp[q] += h
+        wm[q] -= h
+        fd = (f(wp, rgb) - f(wm, rgb)) / (2 * h)
+        assert abs(fd - gw[q]) <= 1e-9 * max(1.0, abs(fd))
+        ch = int(rng.integers(3))
+        vp, vm = rgb.astype(np.float64).copy(), rgb.astype(np.float64).copy()
+        vp[q, ch] += h
+        vm[q, ch] -= h
+        fd = (f(w, vp) - f(w, vm)) / (2 * h)
+        assert abs(fd - gv[q, ch]) <= 1e-9 * max(1.0, abs(fd))
+    # ones (opacity): g_w is the ray's upstream gradient
+    gw1, _ = O.accumulate_bwd(pk, w, None, g[:, :1])
+    ray = np.repeat(np.arange(60), pk[:, 1])
+    assert np.array_equal(gw1, g[ray, 0])

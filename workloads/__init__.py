@@ -323,6 +323,28 @@ def cfg2_rays(n_rays, seed=1002, n_cams=100, width=800, height=800, focal=1111.1
     return o, d
 
 
+def cfg5_rays(rank, world, n_global=1 << 24, seed=1005, n_cams=100, width=800, height=800, focal=1111.1111,
+              radius=1.35):
+    """CFG5 (configs[4]): rank `rank`'s contiguous slice [rank*n/world, (rank+1)*n/world) of a global
+    batch of n_global rays drawn like CFG2's (camera, pixel) pairs.  The draws are i.i.d., so the
+    batch is already shuffled (no image-tile imbalance across ranks).  Vectorised over rays."""
+    assert n_global % world == 0
+    rng = np.random.default_rng(seed)
+    cam = rng.integers(0, n_cams, n_global, dtype=np.int32)
+    px = rng.integers(0, width, n_global, dtype=np.int32)
+    py = rng.integers(0, height, n_global, dtype=np.int32)
+    lo, hi = rank * (n_global // world), (rank + 1) * (n_global // world)
+    cam, px, py = cam[lo:hi], px[lo:hi].astype(np.float64), py[lo:hi].astype(np.float64)
+    centre = np.array([0.5, 0.5, 0.5])
+    cams = hemisphere_cameras(n_cams, radius, centre)
+    c2w = np.stack([look_at(c, centre) for c in cams])  # [n_cams, 3, 3]
+    dirs_cam = np.stack([(px + 0.5 - width / 2.0) / focal, -(py + 0.5 - height / 2.0) / focal,
+                         -np.ones_like(px)], -1)
+    d = np.einsum("nij,nj->ni", c2w[cam], dirs_cam)
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    return cams[cam].astype(np.float32), d.astype(np.float32)
+
+
 def cfg2_lattice(seed=1002):
     prims = random_primitives(seed)
     return bake_lattice(prims, 128, 0.0, 1.0)
