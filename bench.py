@@ -1,17 +1,27 @@
 """bench.py — throughput of the NerfAcc packed-sample hot path on B200.
 
-One step = one CFG2 training step (BASELINE.json configs[1], the config the
-metric is quoted on): march the occupancy grid (nacc_sampling_occgrid) ->
-caller's no-grad σ query (harness lattice field) -> no-gradient early-stop
-filter (nacc_filter_early_stop) -> caller's σ, rgb query -> render fwd
-(nacc_render_fwd) -> MSE gradient -> render bwd (nacc_render_bwd), plus the
+One step = one training step of the workload's global ray batch: for every
+chunk of rays, march the occupancy grid (nacc_sampling_occgrid) -> caller's
+no-grad σ query (harness lattice field) -> no-gradient early-stop filter
+(nacc_filter_early_stop) -> caller's σ, rgb query -> render fwd
+(nacc_render_fwd) -> MSE gradient -> render bwd (nacc_render_bwd); plus the
 occupancy-grid update with its MAX all-reduce every 16 steps (points ->
-field -> all_reduce -> nacc_occgrid_update).  Rays are sharded across ranks
-(2^18 per GPU, weak scaling); the grid is replicated.
+field -> all_reduce -> nacc_occgrid_update).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Workloads (--workload):
+  cfg5       (default) BASELINE.json configs[4]: 2^24 rays per step split
+             across the N ranks (strong scaling), each rank running chunks of
+             2^21 rays; at N = 1 this is S(1) = 8 sequential 2^21-ray chunks
+             (SURVEY §8(e)).
+  cfg5-weak  2^21 rays per GPU per step (weak scaling).
+  cfg2       configs[1]: 2^18 rays per GPU per step (weak scaling).
 
-Prints ONE JSON line (rank 0).  See DESIGN.md §7 for every field.
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5]
+                    [--impl reference]
+
+With --gpus N > 1 and no torchrun environment, the script re-launches itself
+under torch.distributed.run (one rank per GPU, NCCL).  Prints ONE JSON line
+(rank 0).  See DESIGN.md §7 for every field.
 """
 from __future__ import annotations
 
@@ -20,6 +30,8 @@ import glob
 import json
 import math
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -31,25 +43,59 @@ sys.path.insert(0, ROOT)
 
 METRIC = "samples/sec (march+render fwd+bwd) and HBM GB/s vs 8 TB/s at 1/2/4/8 B200"
 UNIT = "samples/s"
-RAYS_PER_GPU = 1 << 18
 UPDATE_EVERY = 16
 EPS = 1e-4
-WORKLOAD = ("cfg2: NeRF-Synthetic-shaped training batch, 2^18 rays per GPU, 128^3 occupancy grid over the unit box, "
-            "step sqrt(3)/1024, early stop T<1e-4, dense-lattice trilinear sigma/rgb field, fwd+bwd, "
-            "grid EMA update + MAX all-reduce every 16 steps")
+GRID_DESC = ("128^3 occupancy grid over the unit box (EMA gamma 0.95, tau 0.01 on sigma*dt, 16 warm-up updates), "
+             "step sqrt(3)/1024, early stop T<1e-4, dense-lattice trilinear sigma/rgb field (CFG2 scene), fwd+bwd, "
+             "grid EMA update + MAX all-reduce every 16 steps")
+WORKLOADS = {
+    "cfg5": dict(global_rays=1 << 24, chunk=1 << 21, scaling="strong",
+                 desc="cfg5: 8xB200 ray-sharded training step, 2^24 rays per step split across the GPUs "
+                      "(chunks of 2^21 rays per rank), " + GRID_DESC),
+    "cfg5-weak": dict(rays_per_gpu=1 << 21, chunk=1 << 21, scaling="weak",
+                      desc="cfg5-weak: 2^21 rays per GPU per step, " + GRID_DESC),
+    "cfg2": dict(rays_per_gpu=1 << 18, chunk=1 << 18, scaling="weak", batches=4,
+                 desc="cfg2: NeRF-Synthetic-shaped training batch, 2^18 rays per GPU per step, " + GRID_DESC),
+}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="cfg5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="nacc", choices=["nacc", "reference"])
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: test runs that put several ranks on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no extras (for ncu)")
     ap.add_argument("--eager", action="store_true", help="time the eager (non-graph) step")
-    ap.add_argument("--no-extras", action="store_true", help="skip the CFG3/CFG4 secondary measurements")
+    ap.add_argument("--no-extras", action="store_true", help="skip the CFG2/CFG3/CFG4 secondary measurements")
     return ap.parse_args()
+
+
+def rays_per_rank(workload, world):
+    w = WORKLOADS[workload]
+    if "global_rays" in w:
+        if w["global_rays"] % world:
+            raise SystemExit(f"bench: {workload} needs a GPU count dividing 2^24, got {world}")
+        return w["global_rays"] // world
+    return w["rays_per_gpu"]
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args):
+    """--gpus N without a torchrun environment: re-run this script under torch.distributed.run
+    (one process per GPU on this node, rendezvous on 127.0.0.1) and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def dist_env():
@@ -151,23 +197,28 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workload
-def make_inputs(rank, n_batches=4):
+def make_inputs(workload, rank, world):
+    """Per-rank ray batches (resident in HBM during the timed region) and the MSE targets."""
     import workloads as W
 
-    rays = []
-    for b in range(n_batches):
-        o, d = W.cfg2_rays(RAYS_PER_GPU, seed=1002 + 1000 * rank + 17 * b)
-        rays.append((o, d))
-    lat = W.cfg2_lattice()
+    n = rays_per_rank(workload, world)
+    if workload == "cfg2":
+        rays = [W.cfg2_rays(n, seed=1002 + 1000 * rank + 17 * b) for b in range(WORKLOADS["cfg2"]["batches"])]
+    elif workload == "cfg5":
+        rays = [W.cfg5_rays(rank, world)]
+    else:  # cfg5-weak: rank r's 2^21 rays are slice r of an 8 x 2^21 global draw (then a reseeded one)
+        rays = [W.cfg5_rays(rank % 8, 8, seed=1005 + 1000 * (rank // 8))]
     rng = np.random.default_rng(7 + rank)
-    gt = rng.uniform(0, 1, (RAYS_PER_GPU, 3)).astype(np.float32)
-    return rays, lat, gt
+    gt = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    return rays, W.cfg2_lattice(), gt
 
 
 class Pipeline:
-    """One CFG2 training step through the public API (paper_2305_04966_b200)."""
+    """One training step of the workload through the public API (paper_2305_04966_b200): the
+    rank's rays in chunks, each chunk march -> σ -> filter -> σ,rgb -> render fwd -> MSE grad ->
+    render bwd."""
 
-    def __init__(self, rank, world, device):
+    def __init__(self, workload, rank, world, device):
         import torch
 
         import workloads as W
@@ -175,11 +226,15 @@ class Pipeline:
         from paper_2305_04966_b200 import harness as H
 
         self.N, self.H, self.torch = N, H, torch
-        self.rank, self.world, self.device = rank, world, device
-        rays, lat, gt = make_inputs(rank)
+        self.workload, self.rank, self.world, self.device = workload, rank, world, device
+        self.n_rank = rays_per_rank(workload, world)
+        ch = min(WORKLOADS[workload]["chunk"], self.n_rank)
+        self.chunks = [(c, min(c + ch, self.n_rank)) for c in range(0, self.n_rank, ch)]
+        rays, lat, gt = make_inputs(workload, rank, world)
         self.rays_host = rays
         self.rays = [(torch.from_numpy(o).to(device), torch.from_numpy(d).to(device)) for o, d in rays]
         self.gt = torch.from_numpy(gt).to(device)
+        self.lattice = lat
         self.field = H.TextureField(torch.from_numpy(lat.data.reshape(-1, 4)).to(device), lat.lo, lat.hi)
         self.spec = N.GridSpec(roi=(0, 0, 0, 1, 1, 1), res=128, levels=1)
         self.step_size = float(np.float32(W.SQRT3 / 1024.0))
@@ -193,10 +248,9 @@ class Pipeline:
         self.stats = {"pre": 0, "post": 0, "rays": 0}
         self.events = []
 
-    def step(self, rays=None, timing=False):
+    def step_chunk(self, o, d, gt, timing=False):
         N, H, torch = self.N, self.H, self.torch
-        o, d = rays if rays is not None else self.rays[self.k % len(self.rays)]
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)] if timing else None
         rec = (lambda i: ev[i].record()) if timing else (lambda i: None)
         rec(0)
         s = N.sampling_occgrid(o, d, self.spec, self.grid.bits, self.params, capacity=self.capacity)
@@ -212,13 +266,10 @@ class Pipeline:
         rec(4)
         color, opacity, depth = N.rendering(f, sig2, rgb, eps=EPS)
         rec(5)
-        g = H.mse_grad(color.detach(), self.gt)
+        g = H.mse_grad(color.detach(), gt)
         rec(6)
         color.backward(g)
         rec(7)
-        self.grid.update_every_n_steps(self.k, self.occ_fn, n=UPDATE_EVERY)
-        rec(8)
-        self.k += 1
         self.stats["pre"] += s.n_samples
         self.stats["post"] += f.n_samples
         self.stats["rays"] += s.n_rays
@@ -226,114 +277,148 @@ class Pipeline:
             self.events.append(ev)
         return color, opacity, depth, f.n_samples
 
+    def step(self, rays=None, timing=False):
+        """eager step (warm-up, capacity estimate, --eager)"""
+        o, d = rays if rays is not None else self.rays[self.k % len(self.rays)]
+        outs, post = [], 0
+        for c0, c1 in self.chunks:
+            color, opacity, depth, n_post = self.step_chunk(o[c0:c1], d[c0:c1], self.gt[c0:c1], timing)
+            outs.append((color, opacity, depth))
+            post += n_post
+        self.grid.update_every_n_steps(self.k, self.occ_fn, n=UPDATE_EVERY)
+        self.k += 1
+        cat = self.torch.cat
+        return (cat([x[0] for x in outs]), cat([x[1] for x in outs]), cat([x[2] for x in outs]), post)
+
     def stage_ms(self):
-        names = ["march", "field_sigma", "filter", "field_sigma_rgb", "render_fwd", "mse_grad", "render_bwd",
-                 "grid_update"]
+        """mean per-chunk stage times x chunks per step"""
+        names = ["march", "field_sigma", "filter", "field_sigma_rgb", "render_fwd", "mse_grad", "render_bwd"]
         acc = {n: 0.0 for n in names}
         for ev in self.events:
             for i, n in enumerate(names):
-                if i + 1 < len(ev):
-                    acc[n] += ev[i].elapsed_time(ev[i + 1])
+                acc[n] += ev[i].elapsed_time(ev[i + 1])
         k = max(len(self.events), 1)
-        return {n: v / k for n, v in acc.items()}
+        return {n: v / k * len(self.chunks) for n, v in acc.items()}
 
     # ------------------------------------------------------------------ CUDA-graph step
     def capture(self):
-        """Capture each stage of the step as a CUDA graph over static buffers,
-        using the device-count API (no host syncs): march -> field σ -> filter
-        -> field σ,rgb -> render fwd -> MSE grad -> render bwd (+ counters).
-        The capacity is the max total seen in warm-up x 1.25; an overflow is
-        recorded in a device status checked after the timed region."""
+        """Capture the step as ONE CUDA graph over static buffers (every chunk: march -> field σ
+        -> filter -> field σ,rgb -> render fwd -> MSE grad -> render bwd, + counters and the
+        result snapshot), using the device-count API (no host syncs); plus per-stage graphs of
+        chunk 0 for the stage breakdown.  The capacity is the max total seen over the chunks x
+        1.25; an overflow is recorded in a device status checked after the timed region."""
         N, H, torch = self.N, self.H, self.torch
         torch.cuda.synchronize()
         caps = []
         for o, d in self.rays:
-            s = N.sampling_occgrid(o, d, self.spec, self.grid.bits, self.params)
-            caps.append(s.n_samples)
+            for c0, c1 in self.chunks:
+                caps.append(N.sampling_occgrid(o[c0:c1], d[c0:c1], self.spec, self.grid.bits, self.params).n_samples)
         cap1 = int(max(caps) * 1.25) + 4096
-        self.o_buf = self.rays[0][0].clone()
-        self.d_buf = self.rays[0][1].clone()
+        if len(self.rays) == 1:  # one resident batch: the graph reads it in place
+            self.o_buf, self.d_buf = self.rays[0]
+        else:  # rotating batches are copied into the static input each step
+            self.o_buf = self.rays[0][0].clone()
+            self.d_buf = self.rays[0][1].clone()
         self.acc = torch.zeros(2, dtype=torch.int64, device=self.device)  # pre, post
         self.acc_status = torch.zeros(1, dtype=torch.int32, device=self.device)
-        pool = torch.cuda.graph_pool_handle()
+        self.result = torch.zeros((self.n_rank, 5), dtype=torch.float32, device=self.device)  # colour, opacity, depth
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
-        outs = {}
         l0 = N.launch_count() + H.launch_count()
 
-        def st_march():
-            outs["s"] = N.sampling_occgrid(self.o_buf, self.d_buf, self.spec, self.grid.bits, self.params,
-                                           capacity=cap1, sync=False)
+        def stages_of(c0, c1, outs):
+            o, d, gt = self.o_buf[c0:c1], self.d_buf[c0:c1], self.gt[c0:c1]
 
-        def st_f1():
-            s = outs["s"]
-            outs["sigma"], _ = self.field.at_samples(self.o_buf, self.d_buf, s.t0, s.t1, s.ray_id, want_rgb=False,
-                                                     n_dev=s.total)
+            def st_march():
+                outs["s"] = N.sampling_occgrid(o, d, self.spec, self.grid.bits, self.params, capacity=cap1, sync=False)
 
-        def st_filter():
-            outs["f"] = N.filter_early_stop(outs["s"], outs["sigma"], EPS, sync=False)
+            def st_f1():
+                s = outs["s"]
+                outs["sigma"], _ = self.field.at_samples(o, d, s.t0, s.t1, s.ray_id, want_rgb=False, n_dev=s.total)
 
-        def st_f2():
-            f = outs["f"]
-            outs["sig2"], outs["rgb"] = self.field.at_samples(self.o_buf, self.d_buf, f.t0, f.t1, f.ray_id,
-                                                              n_dev=f.total)
+            def st_filter():
+                outs["f"] = N.filter_early_stop(outs["s"], outs["sigma"], EPS, sync=False)
 
-        def st_rfwd():
-            outs["color"], outs["opacity"], outs["depth"], outs["ctx"] = N.render_fwd(outs["f"], outs["sig2"],
-                                                                                      outs["rgb"], EPS)
+            def st_f2():
+                f = outs["f"]
+                outs["sig2"], outs["rgb"] = self.field.at_samples(o, d, f.t0, f.t1, f.ray_id, n_dev=f.total)
 
-        def st_mse():
-            outs["gcol"] = H.mse_grad(outs["color"], self.gt)
+            def st_rfwd():
+                outs["color"], outs["opacity"], outs["depth"], outs["ctx"] = N.render_fwd(
+                    outs["f"], outs["sig2"], outs["rgb"], EPS)
 
-        def st_rbwd():
-            outs["gs"], outs["grgb"] = N.render_bwd(outs["f"], outs["sig2"], outs["rgb"], outs["ctx"], outs["gcol"],
-                                                    None, None, EPS)
-            self.acc[0].add_(outs["s"].total[0])
-            self.acc[1].add_(outs["f"].total[0])
-            torch.maximum(self.acc_status, outs["s"].status, out=self.acc_status)
+            def st_mse():
+                outs["gcol"] = H.mse_grad(outs["color"], gt)
+
+            def st_rbwd():
+                outs["gs"], outs["grgb"] = N.render_bwd(outs["f"], outs["sig2"], outs["rgb"], outs["ctx"],
+                                                        outs["gcol"], None, None, EPS)
+                self.acc[0].add_(outs["s"].total[0])
+                self.acc[1].add_(outs["f"].total[0])
+                torch.maximum(self.acc_status, outs["s"].status, out=self.acc_status)
+                torch.cat([outs["color"], outs["opacity"][:, None], outs["depth"][:, None]], 1,
+                          out=self.result[c0:c1])
+
+            return (st_march, st_f1, st_filter, st_f2, st_rfwd, st_mse, st_rbwd)
 
         self.graphs = []
-        stages = (st_march, st_f1, st_filter, st_f2, st_rfwd, st_mse, st_rbwd)
+        self.outs0 = {}
         with torch.cuda.stream(side):
-            for fn in stages:
+            pool = torch.cuda.graph_pool_handle()
+            for fn in stages_of(*self.chunks[0], self.outs0):
                 fn()  # eager warm-up of the stage on the side stream
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, pool=pool, stream=side):
                     fn()
                 self.graphs.append(g)
-            # the whole step as one graph (the timed path); per-stage graphs serve the stage breakdown
+            # the whole step as one graph (the timed path): chunks in sequence, each chunk's
+            # intermediates released before the next chunk allocates (reused within the capture)
             self.full_graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(self.full_graph, pool=torch.cuda.graph_pool_handle(), stream=side):
-                for fn in stages:
-                    fn()
+                for c0, c1 in self.chunks:
+                    outs = {}
+                    for fn in stages_of(c0, c1, outs):
+                        fn()
+                    del outs
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
-        self.launches_per_graph_step = N.launch_count() + H.launch_count() - l0  # (eager + 2 captures) / 3
-        self.launches_per_graph_step //= 3
-        self.outs = outs
+        # launches per graph step: the counter saw chunk 0's stages 2x (eager + capture) and every
+        # chunk once (full capture)
+        per_chunk = (N.launch_count() + H.launch_count() - l0) // (2 + len(self.chunks))
+        self.launches_per_graph_step = per_chunk * len(self.chunks)
         self.capacity = cap1
         self.acc.zero_()
         self.acc_status.zero_()
 
     def step_graph(self, timing=False, rays=None, copy_inputs=True):
         torch = self.torch
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(9)] if timing else None
-        if copy_inputs:  # else the caller has filled o_buf / d_buf on this stream
+        if copy_inputs and len(self.rays) > 1:  # else the inputs are resident in place / filled by the caller
             o, d = rays if rays is not None else self.rays[self.k % len(self.rays)]
             self.o_buf.copy_(o, non_blocking=True)
             self.d_buf.copy_(d, non_blocking=True)
-        if timing:  # stage breakdown: one graph per stage, events between
+        if timing:  # stage breakdown: one graph per stage of chunk 0, events between
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
             for i, g in enumerate(self.graphs):
                 ev[i].record()
                 g.replay()
             ev[7].record()
+            self.events.append(ev)
         else:
             self.full_graph.replay()
-        self.grid.update_every_n_steps(self.k, self.occ_fn, n=UPDATE_EVERY)
-        if timing:
-            ev[8].record()
-            self.events.append(ev)
-        self.k += 1
+            self.grid.update_every_n_steps(self.k, self.occ_fn, n=UPDATE_EVERY)
+            self.k += 1
+
+    def time_grid_update(self, reps=8):
+        """device time of one grid update (points -> field -> MAX all-reduce -> EMA update), the
+        step that runs every 16 steps"""
+        torch = self.torch
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            self.grid.update_every_n_steps(0, self.occ_fn, n=UPDATE_EVERY)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
 
 
 def run_extras(device, reps=20):
@@ -441,14 +526,15 @@ def run_extras(device, reps=20):
                             "rays_per_s": n4 / ((ms_a + ms_b + ms_f + ms_r) / 1e3)}
     # ---- P:86 no-gradient filtering on CFG2: render fwd+bwd over every marched sample versus
     # filter + render over the kept ones (library time; the harness field's share reported apart)
-    c2 = W.cfg2(n_rays=RAYS_PER_GPU)
+    N2 = 1 << 18  # CFG2 ray batch
+    c2 = W.cfg2(n_rays=N2)
     spec2 = N.GridSpec(roi=c2.roi, res=c2.res, levels=c2.levels)
     bits2 = N.prepare_bits(spec2, torch.from_numpy(W.pack_bits(c2.occ).view(np.int32)).to(device))
     o2, d2 = torch.from_numpy(c2.rays_o).to(device), torch.from_numpy(c2.rays_d).to(device)
     fld = H.TextureField(torch.from_numpy(c2.scene.data.reshape(-1, 4)).to(device), c2.scene.lo, c2.scene.hi)
     s_all = N.sampling_occgrid(o2, d2, spec2, bits2, N.MarchParams(step=c2.step))
     sg_all, rgb_all = fld.at_samples(o2, d2, s_all.t0, s_all.t1, s_all.ray_id)
-    g_all = torch.randn((RAYS_PER_GPU, 3), device=device)
+    g_all = torch.randn((N2, 3), device=device)
 
     def unfiltered():
         col, _, _, cx = N.render_fwd(s_all, sg_all, rgb_all, EPS)
@@ -475,7 +561,7 @@ def run_extras(device, reps=20):
         "speedup_with_harness_field": (ms_u + ms_fu) / (ms_k + ms_fs + ms_fk)}
     # ---- P:120-122 combined estimator on CFG2 rays: grid spans (culling), then one proposal
     # round 64 -> 32 edges inside each span (identity map), then a 32-sample render fwd+bwd
-    n2, m2 = RAYS_PER_GPU, 64
+    n2, m2 = N2, 64
     prm2 = N.MarchParams(step=c2.step)
     ms_b, (tn2, tf2, alive2) = timed(lambda: N.occgrid_ray_bounds(o2, d2, spec2, bits2, prm2))
     e64 = torch.linspace(0, 1, m2 + 1, device=device).repeat(n2, 1).contiguous()
@@ -547,50 +633,95 @@ def algorithmic_bytes(stage, pre, post, rays):
 
 
 # ----------------------------------------------------------------------------- oracle (CPU baseline)
-def oracle_sample(n_rays, seed_offset=0):
-    """A bounded sample of the CFG2 workload for the CPU oracle: n_rays rays,
-    with the caller's σ/rgb precomputed (numpy field, untimed)."""
+def oracle_stages(inp):
+    """march -> filter -> render fwd -> render bwd on the CPU oracle; per-stage seconds and the
+    number of post-filter samples."""
+    import oracle as O
+
+    t = [time.perf_counter()]
+    pk, t0, t1, rid = O.march(inp["occ"], 1, 128, (0, 0, 0, 1, 1, 1), inp["o"], inp["d"], step=inp["step"])
+    t.append(time.perf_counter())
+    pk2, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, inp["sig"], inp["L"])
+    t.append(time.perf_counter())
+    out = O.render_fwd(pk2, a0, a1, inp["s2"], inp["rgb"], neg_log_eps=inp["L"])
+    t.append(time.perf_counter())
+    g = 2.0 * (out["color"] - inp["gt"]) / (3 * len(pk2))
+    O.render_bwd(pk2, a0, a1, inp["s2"], inp["rgb"], g, None, None, neg_log_eps=inp["L"])
+    t.append(time.perf_counter())
+    names = ("march", "filter", "render_fwd", "render_bwd")
+    return {n: t[i + 1] - t[i] for i, n in enumerate(names)}, len(a0)
+
+
+def oracle_inputs_from_gpu(pipe, n_rays):
+    """The GPU arm's identical inputs for the oracle: the first n_rays rays of the rank's batch, the
+    same (EMA-trained) occupancy grid, and the σ / rgb the same harness field returned for the
+    same samples (the oracle's march is bit-exact with the GPU's, asserted)."""
+    import torch
+
+    N = pipe.N
+    o, d = pipe.rays[0][0][:n_rays].contiguous(), pipe.rays[0][1][:n_rays].contiguous()
+    s = N.sampling_occgrid(o, d, pipe.spec, pipe.grid.bits, pipe.params)
+    sig, _ = pipe.field.at_samples(o, d, s.t0, s.t1, s.ray_id, want_rgb=False)
+    f = N.filter_early_stop(s, sig, EPS)
+    s2, rgb = pipe.field.at_samples(o, d, f.t0, f.t1, f.ray_id, want_rgb=True)
+    bits = pipe.grid.bits[: (pipe.spec.n_cells + 31) // 32].cpu().numpy().view(np.uint8)
+    occ = np.unpackbits(bits, bitorder="little")[: pipe.spec.n_cells].astype(np.uint8)
+    torch.cuda.synchronize()
+    return dict(o=o.cpu().numpy(), d=d.cpu().numpy(), occ=occ, step=pipe.step_size, sig=sig.cpu().numpy(),
+                s2=s2.detach().cpu().numpy(), rgb=rgb.detach().cpu().numpy(), L=-math.log(float(np.float32(EPS))),
+                gt=pipe.gt[:n_rays].cpu().numpy().astype(np.float64), n_pre=s.n_samples, n_post=f.n_samples)
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(pipe, n_rays=1 << 15, reps=3):
+    """The oracle as it stands on this host (bounded): the GPU arm's identical inputs
+    (rays, EMA grid, field values), timed per stage on all host cores (median of `reps`) and on one
+    thread (one rep)."""
+    import oracle as O
+
+    inp = oracle_inputs_from_gpu(pipe, n_rays)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    O.set_num_threads(cores)
+    st, post = oracle_stages(inp)  # warm (also the parity check below)
+    if post != inp["n_post"]:
+        raise RuntimeError("oracle and GPU disagree on the CPU-baseline sample")
+    runs = [oracle_stages(inp)[0] for _ in range(reps)]
+    per = {k: float(np.median([r[k] for r in runs])) for k in runs[0]}
+    O.set_num_threads(1)
+    one = oracle_stages(inp)[0]
+    O.set_num_threads(cores)
+    tot, tot1 = sum(per.values()), sum(one.values())
+    return {"value": post / tot, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {n_rays} rays of the rank-0 batch, same EMA grid and harness field values as the GPU "
+                      f"arm ({inp['n_pre']} marched / {post} kept samples); march+filter+render fwd+bwd",
+            "stage_s_all_cores": per, "one_thread": {"value": post / tot1, "stage_s": one},
+            "cpu_model": cpu_model()}
+
+
+def ema_grid_cpu():
+    """The GPU arm's estimator built on the CPU (reference arm): 16 EMA updates of the CFG2 field at
+    the oracle's jittered cell points (same seed, decay, threshold and v = σ·Δt)."""
     import oracle as O
     import workloads as W
 
     lat = W.cfg2_lattice()
-    o, d = W.cfg2_rays(n_rays, seed=1002 + seed_offset)
-    occ = W.occupancy_from_lattice(lat, 1, 128, (0, 0, 0, 1, 1, 1))
     step = float(np.float32(W.SQRT3 / 1024.0))
-    pk, t0, t1, rid = O.march(occ, 1, 128, (0, 0, 0, 1, 1, 1), o, d, step=step)
-    sig, _ = W.field_at_intervals(lat.sigma_rgb, o, d, t0, t1, rid)
-    L = -math.log(float(np.float32(EPS)))
-    pk2, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, sig, L)
-    s2, rgb = W.field_at_intervals(lat.sigma_rgb, o, d, a0, a1, r2)
-    gt = np.random.default_rng(0).uniform(0, 1, (n_rays, 3))
-    return dict(o=o, d=d, occ=occ, step=step, sig=sig, s2=s2, rgb=rgb, L=L, gt=gt)
-
-
-def oracle_step(inp):
-    """march -> filter -> render fwd -> render bwd on the CPU oracle (timed part)."""
-    import oracle as O
-
-    pk, t0, t1, rid = O.march(inp["occ"], 1, 128, (0, 0, 0, 1, 1, 1), inp["o"], inp["d"], step=inp["step"])
-    pk2, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, inp["sig"], inp["L"])
-    out = O.render_fwd(pk2, a0, a1, inp["s2"], inp["rgb"], neg_log_eps=inp["L"])
-    g = 2.0 * (out["color"] - inp["gt"]) / (3 * len(pk2))
-    O.render_bwd(pk2, a0, a1, inp["s2"], inp["rgb"], g, None, None, neg_log_eps=inp["L"])
-    return len(a0)
-
-
-def cpu_baseline(n_rays=1 << 15, reps=3):
-    import oracle as O
-
-    inp = oracle_sample(n_rays)
-    oracle_step(inp)
-    t = time.perf_counter()
-    post = 0
-    for _ in range(reps):
-        post += oracle_step(inp)
-    dt = time.perf_counter() - t
-    return {"value": post / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
-            "sample": f"{n_rays} CFG2 rays x {reps} reps (march+filter+render fwd+bwd; field precomputed)",
-            "seconds": dt}
+    dens = np.zeros(128 ** 3, np.float32)
+    occ = None
+    for k in range(16):
+        x = O.occgrid_points(1, 128, (0, 0, 0, 1, 1, 1), 1234, k * UPDATE_EVERY, 1)
+        v = (lat.sigma_rgb(x.astype(np.float64))[0] * step).astype(np.float32)
+        dens, occ, _ = O.occgrid_update(1, 128, (0, 0, 0, 1, 1, 1), dens, v, decay=0.95, threshold=0.01)
+    return lat, occ, step
 
 
 def run_reference(args):
@@ -598,30 +729,47 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle as O
+    import workloads as W
+
+    lat, occ, step = ema_grid_cpu()
+    L = -math.log(float(np.float32(EPS)))
+
+    def sample(n):
+        o, d = W.cfg5_rays(0, 8) if args.workload != "cfg2" else W.cfg2_rays(1 << 18)
+        o, d = o[:n], d[:n]
+        pk, t0, t1, rid = O.march(occ, 1, 128, (0, 0, 0, 1, 1, 1), o, d, step=step)
+        sig, _ = W.field_at_intervals(lat.sigma_rgb, o, d, t0, t1, rid)
+        _, a0, a1, r2, _ = O.filter_early_stop(pk, t0, t1, sig, L)
+        s2, rgb = W.field_at_intervals(lat.sigma_rgb, o, d, a0, a1, r2)
+        gt = np.random.default_rng(7).uniform(0, 1, (n, 3))
+        return dict(o=o, d=d, occ=occ, step=step, sig=sig, s2=s2, rgb=rgb, L=L, gt=gt)
 
     # size each step so the whole --steps K --warmup W run stays within ~2 minutes
-    probe = oracle_sample(4096, seed_offset=5)
-    t = time.perf_counter()
-    oracle_step(probe)
-    per_ray = (time.perf_counter() - t) / 4096
+    probe = sample(4096)
+    st, _ = oracle_stages(probe)
+    per_ray = sum(st.values()) / 4096
     budget = 90.0 / max(args.steps + args.warmup, 1)
     n = int(min(1 << 16, max(256, budget / max(per_ray, 1e-9))))
     n = 1 << int(math.floor(math.log2(n)))
-    inp = oracle_sample(n)
+    inp = sample(n)
     for _ in range(args.warmup):
-        oracle_step(inp)
+        oracle_stages(inp)
     t = time.perf_counter()
     post = 0
     for _ in range(args.steps):
-        post += oracle_step(inp)
+        post += oracle_stages(inp)[1]
     dt = time.perf_counter() - t
     value = post / dt
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    w = WORKLOADS[args.workload]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "rays_per_step": n, "parallelism": "oracle on host cores (rank 0)"},
+            "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w["desc"], "rays_per_step": n,
+                       "parallelism": "oracle on host cores (rank 0 only)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
-                             "sample": f"{n} CFG2 rays per step (field precomputed, untimed)"},
+                             "sample": f"{n} rays of the workload per step (EMA grid built on the CPU; "
+                                       f"numpy field values precomputed, untimed)", "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -632,14 +780,22 @@ def run_nacc(args):
     import torch.distributed as dist
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+    n_dev = torch.cuda.device_count()
+    if args.backend == "nccl" and local >= n_dev:
+        raise SystemExit(f"bench: rank {rank} needs GPU {local}, only {n_dev} visible")
+    torch.cuda.set_device(local % n_dev)
+    device = torch.device("cuda", local % n_dev)
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://", device_id=device)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", init_method="env://", device_id=device)
+        else:
+            dist.init_process_group("gloo", init_method="env://")
     import paper_2305_04966_b200 as N
     from paper_2305_04966_b200 import harness as H
 
-    pipe = Pipeline(rank, world, device)
+    pipe = Pipeline(args.workload, rank, world, device)
     for _ in range(max(args.warmup, 3)):
         pipe.step()
     torch.cuda.synchronize()
@@ -660,33 +816,37 @@ def run_nacc(args):
     # ---- device-timed region: inputs resident in HBM
     pipe.stats = {"pre": 0, "post": 0, "rays": 0}
     pipe.events = []
+    k_start = pipe.k
     l0 = N.launch_count() + H.launch_count()
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local % n_dev) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            step(timing=args.eager and not args.profile)
+            step()
         e1.record()
         torch.cuda.synchronize()
     barrier()
     launches = N.launch_count() + H.launch_count() - l0
+    n_updates = sum(1 for k in range(k_start, k_start + args.steps) if k % UPDATE_EVERY == 0)
     if use_graph:
         launches += pipe.launches_per_graph_step * args.steps
         pre_s, post_s = pipe.acc.tolist()
         if int(pipe.acc_status.item()) != 0:
             raise RuntimeError("march capacity overflow inside the captured step; increase the capacity margin")
-        stats = {"pre": pre_s, "post": post_s, "rays": RAYS_PER_GPU * args.steps}
+        stats = {"pre": pre_s, "post": post_s, "rays": pipe.n_rank * args.steps}
     else:
         stats = dict(pipe.stats)
     ms = e0.elapsed_time(e1)
     if use_graph:  # stage breakdown (not the headline): per-stage graphs with events between them
-        for _ in range(min(args.steps, 50)):
+        for _ in range(min(args.steps, 50) if len(pipe.chunks) == 1 else 10):
             pipe.step_graph(timing=True)
         torch.cuda.synchronize()
     stages = pipe.stage_ms() if not args.profile else {}
+    if stages:
+        stages["grid_update_every_16"] = pipe.time_grid_update()
     t = torch.tensor([ms, stats["post"], stats["pre"], stats["rays"]], dtype=torch.float64, device=device)
     if world > 1:
         tmax = t.clone()
@@ -700,11 +860,10 @@ def run_nacc(args):
     e2e = None
     if not args.profile:
         pinned = [(torch.from_numpy(o).pin_memory(), torch.from_numpy(d).pin_memory()) for o, d in pipe.rays_host]
-        out_host = torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32).pin_memory()
-        k2 = max(args.steps, 20)
+        nr = pipe.n_rank
+        k2 = max(args.steps, 20) if len(pipe.chunks) == 1 else max(args.steps, 8)
         if use_graph:
             pipe.acc.zero_()
-        post_e2e = 0
         barrier()
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
@@ -712,8 +871,8 @@ def run_nacc(args):
         main = torch.cuda.current_stream()
         up, down = torch.cuda.Stream(), torch.cuda.Stream()
         stage = [(torch.empty_like(pipe.o_buf), torch.empty_like(pipe.d_buf)) for _ in range(2)] if use_graph else None
-        snaps = [torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32, device=device) for _ in range(2)]
-        hosts = [out_host, torch.empty((RAYS_PER_GPU, 5), dtype=torch.float32).pin_memory()]
+        snaps = [torch.empty((nr, 5), dtype=torch.float32, device=device) for _ in range(2)]
+        hosts = [torch.empty((nr, 5), dtype=torch.float32).pin_memory() for _ in range(2)]
         h2d_done = [torch.cuda.Event() for _ in range(2)]
         stage_free = [torch.cuda.Event() for _ in range(2)]
         snap_ready = [torch.cuda.Event() for _ in range(2)]
@@ -750,8 +909,7 @@ def run_nacc(args):
                     pipe.step_graph(copy_inputs=False)
                     if i >= 2:
                         main.wait_event(d2h_done[b])  # step i-2's result has left this snapshot
-                    torch.cat([pipe.outs["color"], pipe.outs["opacity"][:, None], pipe.outs["depth"][:, None]], 1,
-                              out=snaps[b])
+                    snaps[b].copy_(pipe.result, non_blocking=True)
                     snap_ready[b].record(main)
                     with torch.cuda.stream(down):
                         down.wait_event(snap_ready[b])
@@ -767,13 +925,14 @@ def run_nacc(args):
                     color, opacity, depth, n_post = pipe.step(rays=(o, d))
                     n_post_eager += n_post
                     res = torch.cat([color.detach(), opacity.detach()[:, None], depth.detach()[:, None]], 1)
-                    out_host.copy_(res, non_blocking=True)
+                    hosts[0].copy_(res, non_blocking=True)
             return n_post_eager
 
         run_io(3)  # untimed: first use of the copy streams, staging buffers and pinned outputs
         torch.cuda.synchronize()
         if use_graph:
             pipe.acc.zero_()
+        barrier()
         f0.record()
         h0 = time.perf_counter()
         post_e2e = run_io(k2)
@@ -790,69 +949,115 @@ def run_nacc(args):
             dist.all_reduce(m[:1], op=dist.ReduceOp.MAX)
             dist.all_reduce(t2[1:], op=dist.ReduceOp.SUM)
             t2[0] = m[0]
-        e2e = {"value": t2[1].item() / (t2[0].item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": RAYS_PER_GPU * 24,
-               "d2h_bytes_per_step": RAYS_PER_GPU * 20, "steps": k2, "host_issue_ms_per_step": host_ms,
+        e2e = {"value": t2[1].item() / (t2[0].item() / 1e3), "unit": UNIT, "h2d_bytes_per_step": nr * 24,
+               "d2h_bytes_per_step": nr * 20, "steps": k2, "host_issue_ms_per_step": host_ms,
                "io": ("pinned host buffers; H2D of step i+1 and D2H of step i on two copy streams, "
                       "double-buffered, overlapping step i" if use_graph else "pinned host buffers, serial")}
 
     if rank == 0:
         peak, peak_kind = measured_peaks()
         K = args.steps
+        n_chunks = len(pipe.chunks)
         pre_pg, post_pg, rays_pg = stats["pre"] / K, stats["post"] / K, stats["rays"] / K
-        roof = None
+        # per-launch (per-chunk) figures: the library kernels run once per chunk
+        pre_pc, post_pc, rays_pc = pre_pg / n_chunks, post_pg / n_chunks, rays_pg / n_chunks
+        roof, lib_ms, lib_bytes = None, None, None
         if stages:
             lib_stages = {k: v for k, v in stages.items() if algorithmic_bytes(k, 1, 1, 1) is not None}
             dom = max(lib_stages, key=lib_stages.get)
-            byts = algorithmic_bytes(dom, pre_pg, post_pg, rays_pg)
-            achieved = byts / (lib_stages[dom] / 1e3) / 1e9
+            byts = algorithmic_bytes(dom, pre_pc, post_pc, rays_pc)
+            ms_launch = lib_stages[dom] / n_chunks
+            achieved = byts / (ms_launch / 1e3) / 1e9
             tr = ncu_traffic().get(dom)
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": tr, "kernel": dom, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": byts,
-                    "ms_per_launch": lib_stages[dom]}
+                    "ms_per_launch": ms_launch, "traffic_note": "ncu dram bytes per launch of the committed CFG2 "
+                    "capture (profiles/), the same kernel at 2^18 rays" if tr else None}
             # the march is bound by instruction issue, not HBM (DESIGN.md §6/§10): its warp
-            # instructions per launch (committed ncu capture) over the issue peak of 148 SMs x 4
-            # schedulers x 1 warp-instruction per cycle at the sampled SM clock
+            # instructions per launch (committed ncu capture, CFG2 shape) over the issue peak of
+            # 148 SMs x 4 schedulers x 1 warp-instruction per cycle at the sampled SM clock
             winst = ncu_warp_instructions() if dom == "march" else None
-            if winst:
+            if winst and rays_pc == (1 << 18):
                 sm_mhz = clk.summary().get("sm_mhz") or 1965.0
                 n_sm = torch.cuda.get_device_properties(device).multi_processor_count
                 issue_peak = n_sm * 4 * sm_mhz * 1e6
-                got = winst / (lib_stages[dom] / 1e3)
+                got = winst / (ms_launch / 1e3)
                 roof["issue"] = {"warp_instructions_per_launch": winst, "achieved": got / 1e9,
                                  "peak": issue_peak / 1e9, "unit": "G warp-instr/s", "frac": got / issue_peak}
+            # library stages only (march, filter, render fwd/bwd; harness field and grid update excluded),
+            # from the per-stage breakdown (includes inter-graph gaps, so conservative)
+            lib_ms = sum(lib_stages.values())
+            lib_bytes = sum(algorithmic_bytes(k, pre_pg, post_pg, rays_pg) for k in lib_stages)
         cpu = None
         if not args.no_cpu_baseline and not args.profile and world == 1:
-            cpu = cpu_baseline()
+            cpu = cpu_baseline(pipe)
         extras = None
         if not args.profile and not args.no_extras:
             try:
                 extras = run_extras(device)
+                if args.workload != "cfg2":
+                    extras["cfg2_step"] = cfg2_step_line(device)
             except Exception as exc:  # secondary lines never sink the headline
                 extras = {"error": repr(exc)}
         clocks = clk.summary()
-        # library stages only (march, filter, render fwd/bwd; harness field and grid update excluded),
-        # from the per-stage breakdown (includes inter-graph gaps, so conservative)
-        lib_ms = sum(v for k, v in stages.items() if algorithmic_bytes(k, 1, 1, 1) is not None) if stages else None
+        w = WORKLOADS[args.workload]
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": w["scaling"], "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "rays_per_gpu": RAYS_PER_GPU, "global_rays_per_step": rays_all / K,
-                           "grid": "1x128^3", "parallelism": f"dp{world} (ray-sharded, replicated grid)",
-                           "l2": "inputs larger than L2 (march output ~0.25 GB/step/GPU; 4 rotating ray batches)"},
+                "config": {"workload": w["desc"], "rays_per_gpu": pipe.n_rank, "chunks_per_gpu": n_chunks,
+                           "global_rays_per_step": rays_all / K, "grid": "1x128^3",
+                           "parallelism": f"dp{world} (ray-sharded, replicated grid, MAX all-reduce every 16 steps)",
+                           "backend": args.backend if world > 1 else None,
+                           "l2": "inputs larger than L2 (march output ~0.25 GB per 2^18 rays; "
+                                 f"{pipe.n_rank} resident rays per GPU)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
                 "execution": "one CUDA graph per step, device-count API (no host syncs)" if use_graph else "eager",
+                "grid_updates_in_timed_region": n_updates,
                 "samples_pre_filter_per_step_per_gpu": pre_pg, "samples_post_filter_per_step_per_gpu": post_pg,
                 "pre_filter_samples_per_s": pre_all / (ms_max / 1e3), "rays_per_s": rays_all / (ms_max / 1e3),
                 "stage_ms": stages, "extras": extras,
                 "library_ms_per_step": lib_ms,
-                "library_samples_per_s": (post_all / K) / (lib_ms / 1e3) if lib_ms else None}
+                "library_samples_per_s": post_pg / (lib_ms / 1e3) if lib_ms else None,
+                "library_hbm": ({"algorithmic_bytes_per_step": lib_bytes, "GBps": lib_bytes / (lib_ms / 1e3) / 1e9,
+                                 "frac_of_measured_peak": lib_bytes / (lib_ms / 1e3) / 1e9 / peak,
+                                 "frac_of_8TBps": lib_bytes / (lib_ms / 1e3) / 8e12} if lib_ms else None)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def cfg2_step_line(device, steps=100):
+    """The CFG2 step (configs[1], 2^18 rays) as a secondary line when the headline is CFG5."""
+    import torch
+
+    p = Pipeline("cfg2", 0, 1, device)
+    for _ in range(3):
+        p.step()
+    p.capture()
+    for _ in range(3):
+        p.step_graph()
+    torch.cuda.synchronize()
+    p.acc.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        p.step_graph()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    pre, post = p.acc.tolist()
+    for _ in range(50):
+        p.step_graph(timing=True)
+    torch.cuda.synchronize()
+    return {"rays": 1 << 18, "ms_per_step": ms, "samples_per_s": post / steps / (ms / 1e3),
+            "samples_pre_filter_per_step": pre / steps, "samples_post_filter_per_step": post / steps,
+            "stage_ms": p.stage_ms()}
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:
