@@ -19,9 +19,6 @@
 #ifndef NACC_MARCH_MAGICFLOOR
 #define NACC_MARCH_MAGICFLOOR 0  // build parameter: floor by FADD.RZ instead of F2I for interior points
 #endif
-#ifndef NACC_MARCH_FLATW
-#define NACC_MARCH_FLATW 0  // build parameter: write a tile's samples as one run (vs ray by ray)
-#endif
 #ifndef NACC_MARCH_FINEMASK
 #define NACC_MARCH_FINEMASK 1  // build parameter: segment test on the fine window masks (0: macro test only)
 #endif
@@ -560,210 +557,324 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 }
 
 // ---------------------------------------------------------------- fused single-pass march
-// Persistent warps; tile = kFRaysPerWarp consecutive rays, handed out by an
-// atomic counter.  Each warp software-pipelines its tiles: phase 1 of tile t
-// traverses the rays once, keeping each ray's emitted lattice indices (16-bit
-// offsets from the ray's first candidate index) in one of the warp's two
-// shared k-list buffers, and publishes the tile's count; then the warp
-// resolves the output offset of its PREVIOUS tile by a warp-wide decoupled
-// look-back (its predecessors have had a whole tile's time to publish, so the
-// warp rarely waits) and writes that tile's packed_info and samples from the
-// other buffer with coalesced stores.  A ray whose k-list overflowed is
-// traversed again when its tile is written.
-#ifndef NACC_MARCH_KCAP
-#define NACC_MARCH_KCAP 1024
+// Persistent warps; a tile = kTRays consecutive rays, handed out by an atomic
+// counter.  Phase 1 of a tile treats the segments of ALL its rays as one flat
+// list, so a warp pass never idles lanes at the end of a ray:
+//   ray j covers slots [base_j, base_j + nseg_j] -- one slot per 16-point
+//   segment q < nseg_j of its k range [kb_j, ke_j), plus one terminal slot that
+//   only supplies the next point; every lane computes the position (and cell
+//   floors) of its slot's first point, and an owner lane (lanes 0..30, not a
+//   terminal) tests its segment against the window masks with the next lane's
+//   point as the segment's far end (a later point: a superset by monotonicity,
+//   reading #22).  A pass advances 31 slots.
+// Flagged segments get entries, in (ray, k) order, in the warp's shared entry
+// buffer: (j << 28) | (q << 16) | mask of the segment's emitted points.  A
+// solid segment (every point provably a member, all < ke and < far) writes its
+// full mask at once; the others are queued and evaluated exactly, two
+// segments per 32-lane pass, filling in their masks.  Per-ray counts
+// accumulate in shared memory; the tile's total is published for the
+// decoupled look-back.  Phase 2 of the PREVIOUS tile (software pipeline:
+// its predecessors have had a tile's time to publish) resolves its output
+// offset, writes packed_info, and streams its entries into contiguous
+// (t0, t1, ray_id) runs, 32 lattice points per pass.  A tile whose entries
+// overflow the buffer (or with a ray longer than 2^16 points) is counted and
+// written by direct traversal instead (traverse_ray).
+#ifndef NACC_MARCH_TRAYS
+#define NACC_MARCH_TRAYS 16  // build parameter: rays per tile
 #endif
-#ifndef NACC_MARCH_RPT
-#define NACC_MARCH_RPT 8  // build parameter: rays per tile of the uniform single-level march
+#ifndef NACC_MARCH_ECAP
+#define NACC_MARCH_ECAP 512  // build parameter: entries (flagged 16-point segments) per tile buffer
 #endif
 #ifndef NACC_MARCH_WARPS
 #define NACC_MARCH_WARPS 4  // build parameter: warps per block of the fused march
 #endif
-constexpr int kFWarps = NACC_MARCH_WARPS, kFRaysPerWarp = NACC_MARCH_RPT, kFKCap = NACC_MARCH_KCAP;
-// cone lattices and cascades give long rays (hundreds of samples): half the rays per tile
-constexpr int fused_rpt(bool cone, bool l1) { return (cone || !l1) ? kFRaysPerWarp / 2 : kFRaysPerWarp; }
-#ifndef NACC_MARCH_PIPE
-#define NACC_MARCH_PIPE 1
-#endif
-// pipeline depth: a tile is resolved and written after the warp has traversed kFPipe more tiles
-constexpr int kFPipe = NACC_MARCH_PIPE;
-constexpr int kFBufs = kFPipe + 1;
+constexpr int kFWarps = NACC_MARCH_WARPS, kTRays = NACC_MARCH_TRAYS, kECap = NACC_MARCH_ECAP;
+// cone lattices and cascades give long rays (up to ~900 points, 57 segments): half the rays per
+// tile, so a tile's entries fit the buffer even when every segment is flagged
+constexpr int tile_rays(bool cone, bool l1) { return (cone || !l1) ? kTRays / 2 : kTRays; }
+constexpr int kTSeg = 16;   // lattice points per segment / entry mask bits
+constexpr int kEvCap = 64;  // queued segments awaiting evaluation
+static_assert(kTRays <= 16, "4-bit ray index in the entries");
+static_assert(kECap <= 1024, "10-bit entry slot in the evaluation queue");
+static_assert(NACC_MARCH_SEG == kTSeg && NACC_MARCH_SEG_CASCADE == kTSeg, "16-point segments");
 
-static_assert(kFRaysPerWarp <= 32, "one lane holds one ray's metadata");
-
-struct FusedTile {  // per-lane metadata of a tile in flight (lane j: ray j)
-  int64_t tile;
-  int32_t c, kb, lpos, buf;
-  long long incl, agg;
+struct TileBuf {                 // one tile in flight (per warp, double-buffered)
+  float4 od[kTRays][2];          // (ox, oy, oz, near_r), (dx, dy, dz, far_r)
+  int2 kr[kTRays];               // (kb, ke)
+  int cnt[kTRays];               // emitted samples per ray
+  uint32_t ent[kECap];           // entries, (ray, k) order
 };
+
+// uniform lattice midpoint / ends with the per-ray anchor (cone: the shared table)
+template <bool kCone>
+__device__ __forceinline__ float tile_mid(const MarchConst &p, float near_r, const float *__restrict__ tab, int k) {
+  if (kCone) {
+    const float ta = __ldg(tab + k);
+    const float dt = fminf(fmaxf(__fmul_rn(ta, p.cone), p.step), p.max_step);
+    return __fadd_rn(ta, __fmul_rn(0.5f, dt));
+  }
+  return lattice_mid_uniform(k, p.step, near_r);
+}
 
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
-    const uint32_t *__restrict__ mask3, const float *__restrict__ obox, const float *__restrict__ rays_o, const float *__restrict__ rays_d, const float *__restrict__ t_min,
-    const float *__restrict__ t_max, int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr,
-    const float *__restrict__ tab, LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info,
-    int64_t *__restrict__ total, int64_t capacity, int32_t *__restrict__ status_out, float *__restrict__ t0,
-    float *__restrict__ t1, int32_t *__restrict__ ray_id) {
-  constexpr int kCap = kFKCap;
-  constexpr int kRpt = fused_rpt(kCone, kL1);  // rays per tile
-  __shared__ uint16_t kbuf[kFWarps][kFBufs][kCap];
-  __shared__ int seglist[kFWarps][32];
-  __shared__ RaySetup s_setup[kFWarps][kFBufs][kFRaysPerWarp];
+    const uint32_t *__restrict__ mask3, const float *__restrict__ obox, const float *__restrict__ rays_o,
+    const float *__restrict__ rays_d, const float *__restrict__ t_min, const float *__restrict__ t_max,
+    int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr, const float *__restrict__ tab,
+    LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info, int64_t *__restrict__ total, int64_t capacity,
+    int32_t *__restrict__ status_out, float *__restrict__ t0, float *__restrict__ t1, int32_t *__restrict__ ray_id) {
+  constexpr int kR = tile_rays(kCone, kL1);  // rays per tile
+  __shared__ TileBuf tb[kFWarps][2];
+  __shared__ uint32_t evq[kFWarps][kEvCap];
+  __shared__ int seglist[kFWarps][32];  // direct traversal (overflowed tiles)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  FusedTile pend[kFPipe > 0 ? kFPipe : 1];  // tiles traversed but not yet written, oldest first
-#pragma unroll
-  for (int i = 0; i < (kFPipe > 0 ? kFPipe : 1); ++i) pend[i].tile = -1;
+  const unsigned lt = (1u << lane) - 1u;
+  const bool fine = kSkip && kL1 && !kCone && mask3 != nullptr;  // single-level fine-mask test on shared floors
+  const int K = kCone ? (int)hdr->K : 0;
+  // the previous tile, pending its phase 2 (lane j < kR: ray j)
+  int64_t prev_tile = -1;
+  int prev_c = 0;
+  long long prev_agg = 0;
+  bool prev_over = false;
   int buf = 0;
-  bool more = true;
-#pragma unroll 1
   for (;;) {
     unsigned int tile32 = 0;
-    if (more && lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
-    const int64_t tile = more ? (int64_t)__shfl_sync(kFull, tile32, 0) : n_tiles;
-    more = tile < n_tiles;
-    FusedTile cur;
-    cur.tile = more ? tile : -1;
-    cur.buf = buf;
-    if (cur.tile >= 0) {
-      // ---- phase 1 of `tile`: lane j < kRpt sets up ray r_base + j, the warp walks the rays in order
-      const int64_t r_base = tile * kRpt;
-      if (lane < kRpt && r_base + lane < n_rays)
-        s_setup[warp][buf][lane] = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r_base + lane);
+    if (lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
+    const int64_t tile = (int64_t)__shfl_sync(kFull, tile32, 0);
+    const bool have = tile < n_tiles;
+    int cur_c = 0;
+    long long cur_agg = 0;
+    bool cur_over = false;
+    if (have) {
+      // ---------------- phase 1 of `tile`
+      TileBuf &T = tb[warp][buf];
+      const int64_t r_base = tile * kR;
+      int kb = 0, ke = 0, nseg = 0;
+      bool longray = false;
+      if (lane < kR) {
+        if (r_base + lane < n_rays) {
+          const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r_base + lane);
+          if (s.hit) {
+            if (kCone) {
+              kb = max((int)lower_bound(tab + 1, K, s.t_lo) - 2, 0);
+              ke = min((int)lower_bound(tab, K + 1, s.t_hi) + 2, K);
+            } else {
+              int64_t b64, e64;
+              uniform_k_range(s, p, b64, e64);
+              kb = (int)b64;
+              ke = (int)e64;
+            }
+            if (ke < kb) ke = kb;
+            nseg = (ke - kb + kTSeg - 1) / kTSeg;
+          }
+          T.od[lane][0] = make_float4(s.ox, s.oy, s.oz, s.near_r);
+          T.od[lane][1] = make_float4(s.dx, s.dy, s.dz, s.far_r);
+        }
+        T.kr[lane] = make_int2(kb, ke);
+        T.cnt[lane] = 0;
+        longray = nseg >= 4096;
+      }
+      // flat slot list: ray j owns slots [base_j, base_j + nseg_j], every ray at least one
+      const int nslot = lane < kR ? nseg + 1 : 0;
+      int sbase = nslot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, sbase, o);
+        if (lane >= o) sbase += v;
+      }
+      const int total_slots = __shfl_sync(kFull, sbase, 31);
+      sbase -= nslot;  // exclusive
+      cur_over = __any_sync(kFull, longray);
       __syncwarp();
-      cur.c = 0;
-      cur.kb = 0;
-      cur.lpos = -1;
-      int pos = 0;  // warp-uniform fill level of the k-list
-      uint16_t *kl = kbuf[warp][buf];
-#pragma unroll 1
-      for (int j = 0; j < kRpt; ++j) {
-        if (r_base + j >= n_rays) break;
-        const RaySetup s = s_setup[warp][buf][j];
-        const int start = pos;
-        int kb0 = 0, ke0 = 0;
-        const int32_t c =
-            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[warp], kb0, ke0,
-                                             [&](unsigned b, bool pred, int k, int32_t cnt) {
-                                               const int q = start + cnt + __popc(b & ((1u << lane) - 1u));
-                                               const int off = k - kb0;
-                                               if (pred && q < kCap) kl[q] = (uint16_t)off;  // an out-of-range ray is discarded below
-                                             });
-        // the list is usable if it fit the buffer and the ray's k range fits 16-bit offsets
-        // (an unusable list leaves its space to the tile's next rays; the ray is traversed again)
-        const bool usable = start + c <= kCap && ke0 - kb0 <= 65536;
-        pos = usable ? start + c : start;
-        if (lane == j) {
-          cur.c = c;
-          cur.kb = kb0;
-          cur.lpos = usable ? start : -1;
+      int n_ent = 0, npend = 0;
+      auto evaluate = [&](int n_eval) {  // the first n_eval queued segments, two per 32-lane pass
+        for (int e0 = 0; e0 < n_eval; e0 += 2) {
+          const int idx = e0 + (lane >> 4);
+          const uint32_t qe = idx < n_eval ? evq[warp][idx] : 0u;
+          const int j = (qe >> 10) & 15, q = (qe >> 14) & 4095, code = (qe >> 26) & 3, lv = (qe >> 28) & 7;
+          const int2 kr = T.kr[j];
+          const int k = kr.x + q * kTSeg + (lane & 15);
+          bool pred = false;
+          if (idx < n_eval && k < kr.y) {
+            const float4 A = T.od[j][0], D = T.od[j][1];
+            const float m = tile_mid<kCone>(p, A.w, tab, k);
+            if (m < D.w)
+              pred = code == 3 ? true
+                               : (code == 1 ? occupied_interior(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z, lv)
+                                            : occupied<kL1>(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z));
+          }
+          const unsigned bal = __ballot_sync(kFull, pred);
+          if ((lane & 15) == 0 && idx < n_eval) {
+            const uint32_t half = (lane ? bal >> 16 : bal) & 0xFFFFu;
+            const int slot = qe & 1023;
+            if (slot < kECap) T.ent[slot] = ((uint32_t)j << 28) | ((uint32_t)q << 16) | half;
+            atomicAdd(&T.cnt[j], __popc(half));
+          }
+        }
+        __syncwarp();
+      };
+      if (!cur_over) {
+        for (int P = 0; P < total_slots; P += 31) {
+          // slot P + lane -> (ray j, segment q)
+          const int sb_in = (lane < kR && sbase > P && sbase < P + 32) ? (1 << (sbase - P)) : 0;
+          const unsigned starts = __reduce_or_sync(kFull, (unsigned)sb_in);
+          const int jP = __popc(__ballot_sync(kFull, lane < kR && sbase <= P)) - 1;
+          const int j = min(jP + __popc(starts & ((2u << lane) - 1u)), kR - 1);
+          const int bj = __shfl_sync(kFull, sbase, j);
+          const int kbj = __shfl_sync(kFull, kb, j), kej = __shfl_sync(kFull, ke, j), nsj = __shfl_sync(kFull, nseg, j);
+          const int q = P + lane - bj;
+          const bool valid = P + lane < total_slots;
+          const bool owner = lane < 31 && valid && q < nsj;
+          const int ks = kbj + q * kTSeg;
+          const float4 A = T.od[j][0], D = T.od[j][1];
+          // first point of the slot (terminal slot: the point after the ray's last segment)
+          const float m = tile_mid<kCone>(p, A.w, tab, kCone ? min(ks, K) : ks);
+          const float X[3] = {__fmaf_rn(m, D.x, A.x), __fmaf_rn(m, D.y, A.y), __fmaf_rn(m, D.z, A.z)};
+          int code = 0, lvl = 0;
+          if (!kSkip) {
+            code = owner ? 2 : 0;
+          } else if (fine) {
+            int fa[3], fb[3];
+            cell_floors(g, X, fa);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) fb[a] = __shfl_down_sync(kFull, fa[a], 1);
+            if (owner) code = segment_test_floors(g, mask3, fa, fb);
+          } else {
+            float Y[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) Y[a] = __shfl_down_sync(kFull, X[a], 1);
+            if (owner) {
+              code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, mask3, X, Y)
+                                                : segment_test<kL1>(g, mask2, M, mask3, X, Y);
+              lvl = code >> 4;
+              code &= 15;
+            }
+          }
+          const bool flag = code != 0;
+          bool direct = false;
+          if (code == 3 && ks + kTSeg <= kej) direct = tile_mid<kCone>(p, A.w, tab, ks + kTSeg - 1) < D.w;
+          const unsigned F = __ballot_sync(kFull, flag), Dm = __ballot_sync(kFull, direct);
+          const int slot = n_ent + __popc(F & lt);
+          if (direct) {
+            if (slot < kECap) T.ent[slot] = ((uint32_t)j << 28) | ((uint32_t)q << 16) | 0xFFFFu;
+            atomicAdd(&T.cnt[j], kTSeg);
+          } else if (flag) {
+            evq[warp][npend + __popc((F & ~Dm) & lt)] = (uint32_t)min(slot, 1023) | ((uint32_t)j << 10) |
+                                                        ((uint32_t)q << 14) | ((uint32_t)code << 26) |
+                                                        ((uint32_t)lvl << 28);
+          }
+          n_ent += __popc(F);
+          npend += __popc(F & ~Dm);
+          __syncwarp();
+          if (npend >= 32) {  // keep the queue short: evaluate all but an odd one
+            const int ne = npend & ~1;
+            evaluate(ne);
+            if (npend & 1) {
+              if (lane == 0) evq[warp][0] = evq[warp][ne];
+              __syncwarp();
+            }
+            npend &= 1;
+          }
+        }
+        evaluate(npend);
+        cur_over = n_ent > kECap;
+      }
+      if (cur_over) {  // count by direct traversal (phase 2 writes the same way)
+        for (int jj = 0; jj < kR; ++jj) {
+          if (r_base + jj >= n_rays) break;
+          const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r_base + jj);
+          int kb0, ke0;
+          const int32_t c = traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[warp],
+                                                            kb0, ke0, [](unsigned, bool, int, int32_t) {});
+          if (lane == 0) T.cnt[jj] = c;
+        }
+        __syncwarp();
+      }
+      __syncwarp();
+      cur_c = lane < kR ? T.cnt[lane] : 0;
+      int agg = cur_c;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(kFull, agg, o);
+      cur_agg = agg;
+      lookback_publish(lb->status, tile, cur_agg);
+      // the entry count travels in lane 31's cur_c slot (lanes >= kR hold no ray)
+      if (lane == 31) cur_c = n_ent;
+    }
+    if (prev_tile >= 0) {
+      // ---------------- phase 2 of the previous tile (buffer buf ^ 1)
+      const TileBuf &T = tb[warp][buf ^ 1];
+      const long long excl = lookback_resolve(lb->status, prev_tile, prev_agg);
+      if (prev_tile == n_tiles - 1 && lane == 0) {
+        *total = excl + prev_agg;
+        if (status_out) {
+          int32_t stt = (excl + prev_agg > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
+          if (hdr && hdr->overflow) stt = NACC_ERR_UNSUPPORTED;
+          *status_out = stt;
         }
       }
-      long long incl = cur.c;  // inclusive scan of the tile's ray counts over lanes
+      const int64_t r_base = prev_tile * kR;
+      const int c = lane < kR ? prev_c : 0;
+      long long incl = c;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const long long v = __shfl_up_sync(kFull, incl, o);
         if (lane >= o) incl += v;
       }
-      cur.incl = incl;
-      cur.agg = __shfl_sync(kFull, incl, 31);
-      lookback_publish(lb->status, tile, cur.agg);
-    }
-    // the tile to write now: the oldest pending one (or the one just traversed)
-    FusedTile prev = kFPipe ? pend[0] : cur;
-    if (kFPipe) {
-#pragma unroll
-      for (int i = 0; i + 1 < kFPipe; ++i) pend[i] = pend[i + 1];
-      pend[kFPipe > 0 ? kFPipe - 1 : 0] = cur;
-    }
-    if (prev.tile >= 0) {
-      // ---- phase 2 of that tile (its own buffer)
-      const int pb = prev.buf;
-      const int64_t ptile = prev.tile;
-      const long long excl = lookback_resolve(lb->status, ptile, prev.agg);
-      if (ptile == n_tiles - 1 && lane == 0) {
-        *total = excl + prev.agg;
-        if (status_out) {
-          int32_t stt = (excl + prev.agg > capacity) ? NACC_ERR_INSUFFICIENT_CAPACITY : NACC_OK;
-          if (hdr && hdr->overflow) stt = NACC_ERR_UNSUPPORTED;
-          *status_out = stt;
-        }
-      }
-      const int64_t r_base = ptile * kRpt;
-      const int64_t my_run = excl + prev.incl - prev.c;
-      if (lane < kRpt && r_base + lane < n_rays)
-        reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(my_run, prev.c);
-      // every list usable: the tile's lists are contiguous in k-list order = output order, so
-      // the warp writes the whole tile as one coalesced run (ray of item i by comparing i with
-      // the rays' inclusive counts)
-      const bool flat = NACC_MARCH_FLATW && __all_sync(kFull, lane >= kRpt || prev.c == 0 || prev.lpos >= 0);
-      if (t0 != nullptr && excl + prev.agg <= capacity && flat) {
-        long long inc[kRpt];
-#pragma unroll
-        for (int jj = 0; jj < kRpt; ++jj) inc[jj] = __shfl_sync(kFull, prev.incl, jj);
-        const uint16_t *kl = kbuf[warp][pb];
-        for (int base = 0; base < (int)prev.agg; base += 32) {  // warp-uniform trip count
-          const int i = base + lane;
-          int j = 0;
-#pragma unroll
-          for (int jj = 0; jj < kRpt; ++jj) j += inc[jj] <= (long long)i;
-          j = min(j, kRpt - 1);
-          const int kb = __shfl_sync(kFull, prev.kb, j);
-          if (i < (int)prev.agg) {
-            const float nr = s_setup[warp][pb][j].near_r;
-            const int k = kb + (int)kl[i];
-            float ta, tb;
-            lattice_ends<kCone>(p, nr, tab, k, ta, tb);
-            t0[excl + i] = ta;
-            t1[excl + i] = tb;
-            ray_id[excl + i] = (int32_t)(r_base + j);
-          }
-        }
-      } else if (t0 != nullptr && excl + prev.agg <= capacity) {
-#pragma unroll 1
-        for (int j = 0; j < kRpt; ++j) {
-          const int64_t r = r_base + j;
-          if (r >= n_rays) break;
-          const int32_t c = __shfl_sync(kFull, prev.c, j);
-          if (c == 0) continue;
-          const int64_t run = __shfl_sync(kFull, my_run, j);
-          const int lpos = __shfl_sync(kFull, prev.lpos, j);
-          if (lpos >= 0) {
-            const int kb = __shfl_sync(kFull, prev.kb, j);
-            const float nr = s_setup[warp][pb][j].near_r;
-            const uint16_t *kl = kbuf[warp][pb] + lpos;
-            for (int i = lane; i < c; i += 32) {
-              const int k = kb + (int)kl[i];
-              float ta, tb;
-              lattice_ends<kCone>(p, nr, tab, k, ta, tb);
-              t0[run + i] = ta;
-              t1[run + i] = tb;
-              ray_id[run + i] = (int32_t)r;
+      const long long run = excl + incl - c;
+      if (lane < kR && r_base + lane < n_rays)
+        reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(run, c);
+      if (t0 != nullptr && excl + prev_agg <= capacity) {
+        if (!prev_over) {
+          const int n_ent = __shfl_sync(kFull, prev_c, 31);
+          const int b = lane & 15;
+          long long carry = excl;
+          for (int e = 0; e < n_ent; e += 2) {
+            const int idx = e + (lane >> 4);
+            const uint32_t ent = idx < n_ent ? T.ent[idx] : 0u;
+            const uint32_t m = ent & 0xFFFFu;
+            const uint32_t mA = __shfl_sync(kFull, m, 0), mB = __shfl_sync(kFull, m, 16);
+            if ((m >> b) & 1u) {
+              const int j = ent >> 28;
+              const long long pos = carry + __popc(m & ((1u << b) - 1u)) + (lane >= 16 ? __popc(mA) : 0);
+              const int k = T.kr[j].x + (int)((ent >> 16) & 4095u) * kTSeg + b;
+              float ta, tb2;
+              lattice_ends<kCone>(p, T.od[j][0].w, tab, k, ta, tb2);
+              t0[pos] = ta;
+              t1[pos] = tb2;
+              ray_id[pos] = (int32_t)(r_base + j);
             }
-          } else {  // k-list overflowed: traverse again, writing directly
-            const RaySetup s = s_setup[warp][pb][j];
+            carry += __popc(mA) + __popc(mB);
+          }
+        } else {  // overflowed tile: traverse again, writing directly
+          for (int jj = 0; jj < kR; ++jj) {
+            const int64_t r = r_base + jj;
+            if (r >= n_rays) break;
+            const long long rj = __shfl_sync(kFull, run, jj);
+            const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r);
             int kb0, ke0;
             traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[warp], kb0, ke0,
-                                            [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                            [&](unsigned bb, bool pred, int k, int32_t cnt) {
                                               if (pred) {
-                                                const int64_t q = run + cnt + __popc(b & ((1u << lane) - 1u));
-                                                float ta, tb;
-                                                lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb);
-                                                t0[q] = ta;
-                                                t1[q] = tb;
-                                                ray_id[q] = (int32_t)r;
+                                                const int64_t qq = rj + cnt + __popc(bb & lt);
+                                                float ta, tb2;
+                                                lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb2);
+                                                t0[qq] = ta;
+                                                t1[qq] = tb2;
+                                                ray_id[qq] = (int32_t)r;
                                               }
                                             });
           }
         }
       }
-      __syncwarp();  // buffer pb is refilled next iteration
+      __syncwarp();  // buffer buf ^ 1 is refilled next iteration
     }
-    bool pending = false;
-#pragma unroll
-    for (int i = 0; i < (kFPipe > 0 ? kFPipe : 1); ++i) pending |= kFPipe > 0 && pend[i].tile >= 0;
-    if (!more && !pending) break;
-    buf = buf + 1 == kFBufs ? 0 : buf + 1;
+    if (!have) break;
+    prev_tile = tile;
+    prev_c = cur_c;
+    prev_agg = cur_agg;
+    prev_over = cur_over;
+    buf ^= 1;
   }
 }
 
@@ -846,7 +957,7 @@ struct MarchWs {
   float *tab;
 };
 
-static int64_t fused_tiles(int64_t n, bool cone, bool l1) { return ceil_div(n, (int64_t)fused_rpt(cone, l1)); }
+static int64_t fused_tiles(int64_t n, bool cone, bool l1) { return ceil_div(n, (int64_t)tile_rays(cone, l1)); }
 
 // persistent grid: every warp resident at once (look-back needs no more; the
 // counter hands out tiles in order of arrival)
