@@ -82,7 +82,35 @@ __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *
 // Pass 1, sector-aligned variant: the walk reads whole 32-byte sectors (8 floats, two
 // float4 loads per array) starting at the sector that holds the ray's first sample, so
 // every DRAM sector fetched is used in full (the unaligned quads above straddle two).
-// Needs 32-byte-aligned t0 / t1 / sigma; reads stay inside the last sector of the ray.
+// Software-pipelined: the next sector's loads are issued before the current one is
+// summed, so a long ray's walk costs one DRAM latency plus its arithmetic, not one
+// latency per sector (the kernel's time was the longest rays' dependent walks).
+// Needs 32-byte-aligned t0 / t1 / sigma; reads stay inside the arrays.
+struct Sector {
+  float a[8], b[8], c[8];
+};
+
+__device__ __forceinline__ void load_sector(Sector &v, const float *__restrict__ t0, const float *__restrict__ t1,
+                                            const float *__restrict__ sigma, int64_t q, int64_t n_samples) {
+  if (q + 8 <= n_samples) {  // whole sector inside the arrays
+    const float4 *pa = reinterpret_cast<const float4 *>(t0 + q), *pb = reinterpret_cast<const float4 *>(t1 + q),
+                 *pc = reinterpret_cast<const float4 *>(sigma + q);
+    const float4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1), c0 = __ldg(pc),
+                 c1 = __ldg(pc + 1);
+    v.a[0] = a0.x; v.a[1] = a0.y; v.a[2] = a0.z; v.a[3] = a0.w; v.a[4] = a1.x; v.a[5] = a1.y; v.a[6] = a1.z; v.a[7] = a1.w;
+    v.b[0] = b0.x; v.b[1] = b0.y; v.b[2] = b0.z; v.b[3] = b0.w; v.b[4] = b1.x; v.b[5] = b1.y; v.b[6] = b1.z; v.b[7] = b1.w;
+    v.c[0] = c0.x; v.c[1] = c0.y; v.c[2] = c0.z; v.c[3] = c0.w; v.c[4] = c1.x; v.c[5] = c1.y; v.c[6] = c1.z; v.c[7] = c1.w;
+  } else {  // the arrays' last, partial sector: element loads (no padding is required)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const bool in = q + j < n_samples;
+      v.a[j] = in ? __ldg(t0 + q + j) : 0.f;
+      v.b[j] = in ? __ldg(t1 + q + j) : 0.f;
+      v.c[j] = in ? __ldg(sigma + q + j) : 0.f;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kCutThreads) filter_cut_sector_kernel(
     const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
     const float *__restrict__ t1, const float *__restrict__ sigma, int64_t n_samples, double L,
@@ -91,28 +119,17 @@ __global__ void __launch_bounds__(kCutThreads) filter_cut_sector_kernel(
   int64_t cut = 0;
   if (r < n_rays) {
     const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
-    const int64_t st = min((int64_t)pi.x, n_samples), e = min((int64_t)(pi.x + pi.y), n_samples);  // clamped as above
+    // a packed_info written past the input's capacity (device-count mode after an overflowed
+    // march) is clamped to the n_samples readable samples; the result is invalid but in bounds
+    const int64_t st = min((int64_t)pi.x, n_samples), e = min((int64_t)(pi.x + pi.y), n_samples);
     double S = 0.0;
     cut = e - st;
-    for (int64_t q = st & ~(int64_t)7; q < e; q += 8) {
-      float a[8], b[8], c[8];
-      if (q + 8 <= n_samples) {  // whole sector inside the arrays
-        const float4 *pa = reinterpret_cast<const float4 *>(t0 + q), *pb = reinterpret_cast<const float4 *>(t1 + q),
-                     *pc = reinterpret_cast<const float4 *>(sigma + q);
-        const float4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1), c0 = __ldg(pc),
-                     c1 = __ldg(pc + 1);
-        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w; a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
-        b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
-        c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w; c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
-      } else {  // the arrays' last, partial sector: element loads (no padding is required)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const bool in = q + j < n_samples;
-          a[j] = in ? __ldg(t0 + q + j) : 0.f;
-          b[j] = in ? __ldg(t1 + q + j) : 0.f;
-          c[j] = in ? __ldg(sigma + q + j) : 0.f;
-        }
-      }
+    int64_t q = st & ~(int64_t)7;
+    Sector cur, nxt;
+    if (q < e) load_sector(cur, t0, t1, sigma, q, n_samples);
+    while (q < e) {
+      const int64_t qn = q + 8;
+      if (qn < e) load_sector(nxt, t0, t1, sigma, qn, n_samples);  // in flight while `cur` is summed
       bool done = false;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -121,11 +138,13 @@ __global__ void __launch_bounds__(kCutThreads) filter_cut_sector_kernel(
             cut = q + j - st;
             done = true;
           } else {
-            S = __dadd_rn(S, __dmul_rn((double)c[j], __dsub_rn((double)b[j], (double)a[j])));
+            S = __dadd_rn(S, __dmul_rn((double)cur.c[j], __dsub_rn((double)cur.b[j], (double)cur.a[j])));
           }
         }
       }
       if (done) break;
+      cur = nxt;
+      q = qn;
     }
     cut_out[r] = (int32_t)cut;
   }

@@ -12,6 +12,7 @@
 // The k range each warp scans is a conservative fp32 slab bound (±2 steps
 // around the padded outermost box); membership alone decides emission.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "lookback.cuh"
@@ -73,14 +74,23 @@ static GridConst make_grid_const(const nacc_grid &g) {
 
 // -------------------------------------------------------------------------- device
 // kL1: single-level grid (the level search reduces to the box-0 test)
+__device__ __forceinline__ bool in_level_box(const GridConst &g, int l, float x, float y, float z) {
+  return g.lo[l][0] <= x && x < g.hi[l][0] && g.lo[l][1] <= y && y < g.hi[l][1] && g.lo[l][2] <= z && z < g.hi[l][2];
+}
+
+// l* = the first level whose half-open box holds x.  The boxes are nested (centre ± half·2^l,
+// each bound rounded once to fp32, monotone in l), so membership is monotone in l and a binary
+// search over the levels returns exactly the linear search's l*.
 template <bool kL1>
 __device__ __forceinline__ int level_of(const GridConst &g, float x, float y, float z) {
-  const int L = kL1 ? 1 : g.levels;
-  for (int l = 0; l < L; ++l)
-    if (g.lo[l][0] <= x && x < g.hi[l][0] && g.lo[l][1] <= y && y < g.hi[l][1] && g.lo[l][2] <= z &&
-        z < g.hi[l][2])
-      return l;
-  return -1;
+  if (kL1) return in_level_box(g, 0, x, y, z) ? 0 : -1;
+  int lo = 0, hi = g.levels;  // l* in [lo, hi]; hi == levels: in no box
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (in_level_box(g, mid, x, y, z)) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo < g.levels ? lo : -1;
 }
 
 // P(k) for the fp32 midpoint m (readings #2, #3): the normative op sequence
@@ -391,6 +401,12 @@ __device__ __forceinline__ float lattice_mid_uniform(int k, float step, float ne
   return lattice_mid_wide(k, step, near_r);
 }
 
+// the same for code paths that know every index they see is < 2^23 (kWide = false)
+template <bool kWide>
+__device__ __forceinline__ float lattice_mid_u(int k, float step, float near_r) {
+  return kWide ? lattice_mid_uniform(k, step, near_r) : __fmaf_rn((float)k + 0.5f, step, near_r);
+}
+
 // midpoint of lattice interval k (uniform or cone table)
 template <bool kCone>
 __device__ __forceinline__ float lattice_mid(const MarchConst &p, const RaySetup &s, const float *__restrict__ tab,
@@ -606,14 +622,14 @@ struct TileBuf {                 // one tile in flight (per warp, double-buffere
 };
 
 // uniform lattice midpoint / ends with the per-ray anchor (cone: the shared table)
-template <bool kCone>
+template <bool kCone, bool kWide>
 __device__ __forceinline__ float tile_mid(const MarchConst &p, float near_r, const float *__restrict__ tab, int k) {
   if (kCone) {
     const float ta = __ldg(tab + k);
     const float dt = fminf(fmaxf(__fmul_rn(ta, p.cone), p.step), p.max_step);
     return __fadd_rn(ta, __fmul_rn(0.5f, dt));
   }
-  return lattice_mid_uniform(k, p.step, near_r);
+  return lattice_mid_u<kWide>(k, p.step, near_r);
 }
 
 template <bool kCone, bool kSkip, bool kL1>
@@ -688,6 +704,10 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
       cur_over = __any_sync(kFull, longray);
       __syncwarp();
       int n_ent = 0, npend = 0;
+      // lattice indices >= 2^23 anywhere in the tile (far origins): the exact wide midpoint
+      const bool wide = !kCone && __any_sync(kFull, lane < kR && ke + kTSeg > (1 << 23));
+      auto phase1 = [&](auto wide_tag) {
+      constexpr bool kW = decltype(wide_tag)::value;
       auto evaluate = [&](int n_eval) {  // the first n_eval queued segments, two per 32-lane pass
         for (int e0 = 0; e0 < n_eval; e0 += 2) {
           const int idx = e0 + (lane >> 4);
@@ -698,7 +718,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           bool pred = false;
           if (idx < n_eval && k < kr.y) {
             const float4 A = T.od[j][0], D = T.od[j][1];
-            const float m = tile_mid<kCone>(p, A.w, tab, k);
+            const float m = tile_mid<kCone, kW>(p, A.w, tab, k);
             if (m < D.w)
               pred = code == 3 ? true
                                : (code == 1 ? occupied_interior(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z, lv)
@@ -714,7 +734,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
         }
         __syncwarp();
       };
-      if (!cur_over) {
+      {
         for (int P = 0; P < total_slots; P += 31) {
           // slot P + lane -> (ray j, segment q)
           const int sb_in = (lane < kR && sbase > P && sbase < P + 32) ? (1 << (sbase - P)) : 0;
@@ -729,7 +749,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           const int ks = kbj + q * kTSeg;
           const float4 A = T.od[j][0], D = T.od[j][1];
           // first point of the slot (terminal slot: the point after the ray's last segment)
-          const float m = tile_mid<kCone>(p, A.w, tab, kCone ? min(ks, K) : ks);
+          const float m = tile_mid<kCone, kW>(p, A.w, tab, kCone ? min(ks, K) : ks);
           const float X[3] = {__fmaf_rn(m, D.x, A.x), __fmaf_rn(m, D.y, A.y), __fmaf_rn(m, D.z, A.z)};
           int code = 0, lvl = 0;
           if (!kSkip) {
@@ -753,7 +773,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           }
           const bool flag = code != 0;
           bool direct = false;
-          if (code == 3 && ks + kTSeg <= kej) direct = tile_mid<kCone>(p, A.w, tab, ks + kTSeg - 1) < D.w;
+          if (code == 3 && ks + kTSeg <= kej) direct = tile_mid<kCone, kW>(p, A.w, tab, ks + kTSeg - 1) < D.w;
           const unsigned F = __ballot_sync(kFull, flag), Dm = __ballot_sync(kFull, direct);
           const int slot = n_ent + __popc(F & lt);
           if (direct) {
@@ -778,6 +798,11 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           }
         }
         evaluate(npend);
+      }
+      };  // phase1
+      if (!cur_over) {
+        if (wide) phase1(std::true_type{});
+        else phase1(std::false_type{});
         cur_over = n_ent > kECap;
       }
       if (cur_over) {  // count by direct traversal (phase 2 writes the same way)
@@ -828,23 +853,26 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
         if (!prev_over) {
           const int n_ent = __shfl_sync(kFull, prev_c, 31);
           const int b = lane & 15;
-          long long carry = excl;
+          float *__restrict__ o0 = t0 + excl;
+          float *__restrict__ o1 = t1 + excl;
+          int32_t *__restrict__ oid = ray_id + excl;
+          int carry = 0;  // samples written so far in the tile
           for (int e = 0; e < n_ent; e += 2) {
             const int idx = e + (lane >> 4);
             const uint32_t ent = idx < n_ent ? T.ent[idx] : 0u;
-            const uint32_t m = ent & 0xFFFFu;
-            const uint32_t mA = __shfl_sync(kFull, m, 0), mB = __shfl_sync(kFull, m, 16);
-            if ((m >> b) & 1u) {
+            const bool set = (ent >> b) & 1u;
+            const unsigned bal = __ballot_sync(kFull, set);  // both entries' masks, in output order
+            if (set) {
               const int j = ent >> 28;
-              const long long pos = carry + __popc(m & ((1u << b) - 1u)) + (lane >= 16 ? __popc(mA) : 0);
-              const int k = T.kr[j].x + (int)((ent >> 16) & 4095u) * kTSeg + b;
+              const int pos = carry + __popc(bal & lt);
+              const int k = T.kr[j].x + (int)((ent >> 12) & 0xFFF0u) + b;  // kb_j + 16 q + b
               float ta, tb2;
               lattice_ends<kCone>(p, T.od[j][0].w, tab, k, ta, tb2);
-              t0[pos] = ta;
-              t1[pos] = tb2;
-              ray_id[pos] = (int32_t)(r_base + j);
+              o0[pos] = ta;
+              o1[pos] = tb2;
+              oid[pos] = (int32_t)(r_base + j);
             }
-            carry += __popc(mA) + __popc(mB);
+            carry += __popc(bal);
           }
         } else {  // overflowed tile: traverse again, writing directly
           for (int jj = 0; jj < kR; ++jj) {
