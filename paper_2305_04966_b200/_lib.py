@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnacc.so")
+# NACC_DEBUG=1 loads the precondition-checking build (libnacc_debug.so, csrc/debug.cu)
+LIB_PATH = os.path.join(_PKG, "libnacc_debug.so" if os.environ.get("NACC_DEBUG") == "1" else "libnacc.so")
 HARNESS_PATH = os.path.join(_PKG, "libnacc_harness.so")
 
 NACC_OK = 0

@@ -22,6 +22,7 @@ INCLUDE = os.path.join(ROOT, "include")
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libnacc.so")
+DEBUG_LIB = os.path.join(PKG, "libnacc_debug.so")  # -DNACC_DEBUG=1: device preconditions checked (csrc/debug.cu)
 HARNESS_LIB = os.path.join(PKG, "libnacc_harness.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -68,15 +69,20 @@ def _link(objs: list[str], out: str) -> None:
         f.write(listing)
 
 
-def build(verbose: bool = False, extra: list[str] | None = None) -> tuple[str, str]:
+def build(verbose: bool = False, extra: list[str] | None = None, debug: bool = True) -> tuple[str, str]:
+    """libnacc.so + libnacc_harness.so (+ libnacc_debug.so, the NACC_DEBUG precondition build)."""
     extra = list(extra or [])
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hsrcs = sorted(glob.glob(os.path.join(CSRC, "harness", "*.cu")))
+    dbg = extra + ["-DNACC_DEBUG=1"]
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
         objs = list(ex.map(lambda s: _compile(s, extra), srcs))
         hobjs = list(ex.map(lambda s: _compile(s, extra), hsrcs))
+        dobjs = list(ex.map(lambda s: _compile(s, dbg), srcs)) if debug else None
     _link(objs, LIB)
     _link(hobjs, HARNESS_LIB)
+    if debug:
+        _link(dobjs, DEBUG_LIB)
     if verbose:
         print(f"built {LIB} and {HARNESS_LIB}")
     return LIB, HARNESS_LIB

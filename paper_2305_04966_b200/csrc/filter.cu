@@ -4,6 +4,7 @@
 // filter is a per-ray cut (sequential fp64 sum, early exit) + exclusive scan of
 // the cuts + a compacting copy (three kernels, no host sync).
 #include "common.cuh"
+#include "debug.cuh"
 
 namespace nacc {
 
@@ -293,6 +294,8 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   NACC_REQUIRE(n_samples == 0 || (t0 && t1 && sigma), "t0, t1, sigma must be non-NULL");
   NACC_REQUIRE(capacity == 0 || (t0_out && t1_out && ray_id_out), "outputs must be non-NULL when capacity > 0");
   NACC_REQUIRE(ws && ws_bytes >= nacc_filter_workspace_bytes(n_rays), "workspace too small");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
   int32_t *cuts;
   int64_t *bsums;
   filter_ws_layout(n_rays, &cuts, &bsums, ws);

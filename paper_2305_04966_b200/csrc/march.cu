@@ -15,6 +15,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "debug.cuh"
 #include "lookback.cuh"
 
 #ifndef NACC_MARCH_MAGICFLOOR
@@ -1174,6 +1175,7 @@ nacc_status nacc_sampling_occgrid(const nacc_grid *grid, const uint32_t *bits, c
   }
   NACC_REQUIRE(packed_info && aligned(packed_info, 16), "packed_info must be non-NULL and 16-byte aligned");
   NACC_REQUIRE((!t0 && !t1 && !ray_id) || (t0 && t1 && ray_id), "t0, t1, ray_id: all or none");
+  NACC_DEBUG_CHECK(debug_check_rays(rays_d, n_rays, stream));
   return launch_march(kModeFused, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays, packed_info, t0, t1,
                       ray_id, capacity, total, status_out, ws, stream);
 }
@@ -1188,6 +1190,7 @@ nacc_status nacc_sampling_occgrid_fill(const nacc_grid *grid, const uint32_t *bi
   if (st != NACC_OK) return st;
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(packed_info && t0 && t1 && ray_id, "packed_info, t0, t1, ray_id must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_rays(rays_d, n_rays, stream));
   // the cone table lives in the workspace; it is rebuilt here
   return launch_march(kModeFill, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays,
                       const_cast<int64_t *>(packed_info), t0, t1, ray_id, 0, nullptr, nullptr, ws, stream);

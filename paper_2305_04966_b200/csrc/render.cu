@@ -10,6 +10,7 @@
 // suffices.  Fused path: flat ray-aligned tiles (segscan.cuh); granular and
 // fallback paths: one warp per ray, 32 consecutive samples per step.
 #include "common.cuh"
+#include "debug.cuh"
 #include "segscan.cuh"
 
 namespace nacc {
@@ -236,15 +237,50 @@ struct Items {
 #ifndef NACC_RENDER_RAYCACHE
 #define NACC_RENDER_RAYCACHE 1  // build parameter: backward loads per-ray constants once per run of the ray
 #endif
-#ifndef NACC_RENDER_F32A
-#define NACC_RENDER_F32A 0  // build parameter: alpha = -expm1f(-s) in fp32 (experiment)
+#ifndef NACC_RENDER_FASTEXP
+#define NACC_RENDER_FASTEXP 1  // build parameter: e^{-s} by exp_neg below (0: the CUDA math library exp)
 #endif
+// e^{-s} for s >= 0 in fp64 to ~2e-13 relative: the fused tile kernels need T = Π e^{-s_j} to
+// ~1e-9 over a 5000-sample ray (abs 1e-5 bars on T and w, rel 1e-3 on gradients), not to the
+// last fp64 ulp, so a Cody-Waite reduction e^{-s} = 2^n e^r, |r| <= ln2/2, and a degree-10
+// Taylor polynomial (remainder |r|^11/11! < 2.2e-13) replace the library exp's ~39 instructions
+// with ~19.  s > 708 returns 0 (e^{-708} ~ 1e-308).
+__device__ __forceinline__ double exp_neg(double s) {
+  const double x = -s;
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52: x*log2(e) + magic holds round(x*log2(e))
+  const double kd = __fma_rn(x, 1.4426950408889634, magic);
+  const int n = __double2loint(kd);
+  const double nd = kd - magic;
+  double r = __fma_rn(nd, -6.93147180369123816490e-01, x);  // ln2 split in two (Cody-Waite)
+  r = __fma_rn(nd, -1.90821492927058770002e-10, r);
+  double p = 2.7557319223985893e-07;  // 1/10!
+  p = __fma_rn(p, r, 2.7557319223985888e-06);
+  p = __fma_rn(p, r, 2.4801587301587302e-05);
+  p = __fma_rn(p, r, 1.9841269841269841e-04);
+  p = __fma_rn(p, r, 1.3888888888888889e-03);
+  p = __fma_rn(p, r, 8.3333333333333332e-03);
+  p = __fma_rn(p, r, 4.1666666666666664e-02);
+  p = __fma_rn(p, r, 1.6666666666666666e-01);
+  p = __fma_rn(p, r, 0.5);
+  p = __fma_rn(p, r, 1.0);
+  p = __fma_rn(p, r, 1.0);
+  const double scale = __hiloint2double((n + 1023) << 20, 0);  // 2^n, n >= -1022 below the cutoff
+  return s > 708.0 ? 0.0 : p * scale;
+}
+
 // e^{-s} of one interval (1 - alpha)
 __device__ __forceinline__ double interval_ea(double s) {
-#if NACC_RENDER_F32A
-  return 1.0 + (double)expm1f(-(float)s);
+#if NACC_RENDER_FASTEXP
+  return exp_neg(s);
 #else
   return exp(-s);
+#endif
+}
+__device__ __forceinline__ double trans_first(double S) {  // T of a thread's first item
+#if NACC_RENDER_FASTEXP
+  return exp_neg(S);
+#else
+  return exp(-S);
 #endif
 }
 constexpr int64_t kWarpTile = NACC_RENDER_TILE;  // samples per warp tile (build parameter)
@@ -455,7 +491,7 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
       int64_t lead_r = -1;
       // T of the thread's first item from its optical depth, later items by the product
       // T_{j+1} = T_j e^{-s_j} (one fp64 exp per item instead of two)
-      double Tn = exp(-S[0]);
+      double Tn = trans_first(S[0]);
   #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const bool live = it.valid[j] && !(S[j] > L);
@@ -559,7 +595,7 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
       {
         float col[12];
         load_rgb4(col, it, rgb, kVec);
-        double Tn = exp(-S[0]);  // T_{j+1} = T_j e^{-s_j}, as in the forward
+        double Tn = trans_first(S[0]);  // T_{j+1} = T_j e^{-s_j}, as in the forward
         // per-ray constants, loaded once per run of the ray within the thread's items
         int32_t cr = -1;
         float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -889,6 +925,8 @@ nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, i
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(n_samples == 0 || (t0 && t1 && sigma), "t0, t1, sigma must be non-NULL");
   NACC_REQUIRE(!ctx || aligned(ctx, 8), "ctx must be 8-byte aligned");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
   if (ray_id && rgb) {
     const int64_t n_wtiles = ceil_div(n_samples, kWarpTile);
     const int64_t warps = n_wtiles > ceil_div(n_rays, 32) ? n_wtiles : ceil_div(n_rays, 32);
@@ -921,6 +959,8 @@ nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, i
   NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
   if (n_rays == 0 || n_samples == 0) return NACC_OK;
   NACC_REQUIRE(t0 && t1 && sigma && g_sigma, "t0, t1, sigma, g_sigma must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
   if (ray_id && rgb && ctx) {
     NACC_REQUIRE(ws && ws_bytes >= nacc_render_bwd_workspace_bytes(n_rays), "workspace too small");
     float4 *gcv = static_cast<float4 *>(ws);
@@ -961,6 +1001,8 @@ nacc_status nacc_render_weights_fwd(const int64_t *packed_info, int64_t n_rays, 
   NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(n_samples == 0 || (t0 && t1 && sigma && weights), "t0, t1, sigma, weights must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
   weights_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma,
                                                                       neg_log_eps, weights, trans, alphas);
   count_launch(1);
@@ -979,6 +1021,8 @@ nacc_status nacc_render_weights_bwd(const int64_t *packed_info, int64_t n_rays, 
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(n_samples == 0 || (t0 && t1 && sigma && g_weights && g_sigma),
                "t0, t1, sigma, g_weights, g_sigma must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
   weights_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma,
                                                                       neg_log_eps, g_weights, g_trans, g_sigma);
   count_launch(1);
@@ -995,6 +1039,8 @@ nacc_status nacc_render_weights_alpha_fwd(const int64_t *packed_info, int64_t n_
   NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(n_samples == 0 || (alphas && weights), "alphas and weights must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, nullptr, nullptr, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_alpha(alphas, n_samples, stream));
   weights_alpha_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, alphas,
                                                                             std::exp(-neg_log_eps), weights, trans,
                                                                             nullptr);
@@ -1019,6 +1065,8 @@ nacc_status nacc_render_weights_alpha_bwd(const int64_t *packed_info, int64_t n_
   NACC_REQUIRE(n_samples == 0 || (alphas && g_weights && g_alphas), "alphas, g_weights, g_alphas must be non-NULL");
   NACC_REQUIRE(ws && ws_bytes >= nacc_render_weights_alpha_bwd_workspace_bytes(n_samples) && aligned(ws, 8),
                "workspace too small");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, nullptr, nullptr, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_alpha(alphas, n_samples, stream));
   const double eps_T = std::exp(-neg_log_eps);
   double *T64 = static_cast<double *>(ws);
   weights_alpha_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, alphas, eps_T,
@@ -1040,6 +1088,7 @@ nacc_status nacc_accumulate_along_rays(const int64_t *packed_info, int64_t n_ray
   NACC_REQUIRE(values || C == 1, "values == NULL requires C == 1");
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(out && (n_samples == 0 || weights), "weights and out must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, nullptr, nullptr, n_samples, stream));
   const int blocks = grid_for(n_rays * 32, 256);
   switch (C) {
     case 1: accumulate_kernel<1><<<blocks, 256, 0, stream>>>(packed_info, n_rays, weights, values, C, out); break;
@@ -1063,6 +1112,7 @@ nacc_status nacc_accumulate_along_rays_bwd(const int64_t *packed_info, int64_t n
   NACC_REQUIRE(values || (C == 1 && !g_values), "values == NULL requires C == 1 and g_values == NULL");
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(g_out && (n_samples == 0 || weights), "weights and g_out must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, nullptr, nullptr, n_samples, stream));
   accumulate_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, weights, values, C,
                                                                          g_out, g_weights, g_values);
   count_launch(1);

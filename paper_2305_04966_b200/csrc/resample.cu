@@ -4,6 +4,7 @@
 // readings #16-#19).  One warp per ray; the ray's normalised CDF lives in
 // shared memory, each lane inverts 1/32 of the output edges by binary search.
 #include "common.cuh"
+#include "debug.cuh"
 
 namespace nacc {
 
@@ -200,6 +201,8 @@ nacc_status nacc_importance_sample(int64_t n_rays, int32_t n_in, const float *s_
   NACC_REQUIRE(std::isfinite(t_near) && t_near > 0.0 && t_far > t_near, "need 0 < t_near < t_far");
   NACC_REQUIRE(map == NACC_MAP_LINDISP || std::isfinite(t_far), "identity map needs a finite t_far");
   if (n_rays == 0) return NACC_OK;
+  NACC_DEBUG_CHECK(debug_check_rows_ascending(s_edges, n_rays, n_in + 1, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, sigma ? n_rays * n_in : 0, "proposal sigma must be >= 0 and finite", stream));
   return launch_importance(n_rays, n_in, s_edges, sigma, cdf, map, t_near, t_far, nullptr, nullptr, n_out,
                            stratified, seed, s_out, t_out, stream);
 }
@@ -213,6 +216,8 @@ nacc_status nacc_importance_sample_ranged(int64_t n_rays, int32_t n_in, const fl
   if (st != NACC_OK) return st;
   if (n_rays == 0) return NACC_OK;
   NACC_REQUIRE(t_near && t_far, "t_near and t_far must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_rows_ascending(s_edges, n_rays, n_in + 1, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, sigma ? n_rays * n_in : 0, "proposal sigma must be >= 0 and finite", stream));
   return launch_importance(n_rays, n_in, s_edges, sigma, cdf, map, 0.0, 0.0, t_near, t_far, n_out, stratified,
                            seed, s_out, t_out, stream);
 }
