@@ -285,6 +285,33 @@ __device__ __forceinline__ double trans_first(double S) {  // T of a thread's fi
 }
 constexpr int64_t kWarpTile = NACC_RENDER_TILE;  // samples per warp tile (build parameter)
 constexpr int kWarpChunk = 128;
+#ifndef NACC_RENDER_L2PF
+#define NACC_RENDER_L2PF 0  // build parameter: TMA bulk L2 prefetch of the warp's next tile (A/B)
+#endif
+
+// One bulk-copy-engine prefetch of [p, p + n floats) into L2 (cp.async.bulk.prefetch.L2,
+// SASS UBLKPF): 16-byte aligned start, size a multiple of 16 B.
+__device__ __forceinline__ void l2_prefetch_floats(const void *p, int64_t n_floats) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uint32_t bytes = (uint32_t)((n_floats * 4 + 15) & ~(int64_t)15);
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+}
+
+// lane 0 prefetches the raw sample range of warp tile wt (plus a chunk of slack past its end,
+// where the ray-aligned tile usually extends) into L2 while the warp works on its current tile
+__device__ __forceinline__ void prefetch_tile(int64_t wt, int64_t N, const float *t0, const float *t1,
+                                              const float *sigma, const int32_t *ray_id, const float *rgb) {
+  if (!NACC_RENDER_L2PF || (threadIdx.x & 31) != 0) return;
+  const int64_t a = wt * kWarpTile;
+  if (a >= N) return;
+  const int64_t b = min(a + kWarpTile + kWarpChunk, N);
+  const int64_t a4 = a & ~(int64_t)3, n = b - a4;
+  l2_prefetch_floats(t0 + a4, n);
+  l2_prefetch_floats(t1 + a4, n);
+  l2_prefetch_floats(sigma + a4, n);
+  l2_prefetch_floats(ray_id + a4, n);
+  if (rgb) l2_prefetch_floats(rgb + 3 * a4, 3 * n);
+}
 
 template <bool kVec>
 __device__ __forceinline__ void load_items_warp(Items &it, int64_t c0, int64_t B, int64_t E,
@@ -470,6 +497,7 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
   // the resident capacity, not by the arrays' capacity)
   const int64_t N = min(packed_end(packed_info, n_rays), n_samples);  // in bounds after an overflowed march
   for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
+    prefetch_tile(wt + nw, N, t0, t1, sigma, ray_id, rgb);
     const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
     const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
     if (B >= E) continue;
@@ -578,6 +606,7 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t N = min(packed_end(packed_info, n_rays), n_samples);  // in bounds after an overflowed march
   for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
+    prefetch_tile(wt + nw, N, t0, t1, sigma, ray_id, rgb);
     const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
     const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
     if (B >= E) continue;
@@ -586,30 +615,6 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
     for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
       Items it;
       load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
-      double s[4], S[4];
-      warp_items_S(it, s, S, carryS);
-      // phase A: per item g_w w (scan input), w and g_w T (1-α); the only state kept
-      double w[4], gwTea[4];
-      unsigned live = 0;
-      Seg<1> agg = seg_identity<1>();
-      {
-        float col[12];
-        load_rgb4(col, it, rgb, kVec);
-        double Tn = trans_first(S[0]);  // T_{j+1} = T_j e^{-s_j}, as in the forward
-        // per-ray constants, loaded once per run of the ray within the thread's items
-        int32_t cr = -1;
-        float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
-        double2 gon = make_double2(0.0, 0.0);
-  #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          w[j] = 0.0;
-          gwTea[j] = 0.0;
-          double v = 0.0;
-          const double ea = interval_ea(s[j]);
-          const double T = NACC_RENDER_TPROD ? ((j > 0 && it.head[j]) ? 1.0 : Tn) : exp(-S[j]);
-          Tn = T * ea;
-          if (it.valid[j] && !(S[j] > L)) {
-            live |= 1u << j;
             if (!NACC_RENDER_RAYCACHE || it.rid[j] != cr) {
               gc = __ldg(gcv + it.rid[j]);
               gon = __ldg(gq + 2 * (int64_t)it.rid[j]);

@@ -131,11 +131,12 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
       }
       s = (double)e[lo + 1];
     } else {
-      // largest j in [0, n_in-1] with F[j] <= u
+      // largest j in [0, n_in-1] with F[j] <= u, i.e. F[j] <= uf, the largest float <= u (exact)
+      const float uf = __double2float_rd(u);
       int lo = 0, hi = n_in - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if ((double)F[mid] <= u) lo = mid;
+        if (F[mid] <= uf) lo = mid;
         else hi = mid - 1;
       }
       const double Fj = (double)F[lo], Fj1 = (double)F[lo + 1];
