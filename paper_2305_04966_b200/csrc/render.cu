@@ -284,9 +284,8 @@ __device__ __forceinline__ double trans_first(double S) {  // T of a thread's fi
 #endif
 }
 constexpr int64_t kWarpTile = NACC_RENDER_TILE;  // samples per warp tile (build parameter)
-constexpr int kWarpChunk = 128;
 #ifndef NACC_RENDER_L2PF
-#define NACC_RENDER_L2PF 0  // build parameter: TMA bulk L2 prefetch of the warp's next tile (A/B)
+#define NACC_RENDER_L2PF 0  // build parameter: TMA bulk L2 prefetch of the warp's next tile (A/B: slower)
 #endif
 
 // One bulk-copy-engine prefetch of [p, p + n floats) into L2 (cp.async.bulk.prefetch.L2,
@@ -296,6 +295,7 @@ __device__ __forceinline__ void l2_prefetch_floats(const void *p, int64_t n_floa
   const uint32_t bytes = (uint32_t)((n_floats * 4 + 15) & ~(int64_t)15);
   if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
 }
+constexpr int kWarpChunk = 128;
 
 // lane 0 prefetches the raw sample range of warp tile wt (plus a chunk of slack past its end,
 // where the ray-aligned tile usually extends) into L2 while the warp works on its current tile
@@ -615,6 +615,30 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
     for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
       Items it;
       load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
+      double s[4], S[4];
+      warp_items_S(it, s, S, carryS);
+      // phase A: per item g_w w (scan input), w and g_w T (1-α); the only state kept
+      double w[4], gwTea[4];
+      unsigned live = 0;
+      Seg<1> agg = seg_identity<1>();
+      {
+        float col[12];
+        load_rgb4(col, it, rgb, kVec);
+        double Tn = trans_first(S[0]);  // T_{j+1} = T_j e^{-s_j}, as in the forward
+        // per-ray constants, loaded once per run of the ray within the thread's items
+        int32_t cr = -1;
+        float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
+        double2 gon = make_double2(0.0, 0.0);
+  #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          w[j] = 0.0;
+          gwTea[j] = 0.0;
+          double v = 0.0;
+          const double ea = interval_ea(s[j]);
+          const double T = NACC_RENDER_TPROD ? ((j > 0 && it.head[j]) ? 1.0 : Tn) : exp(-S[j]);
+          Tn = T * ea;
+          if (it.valid[j] && !(S[j] > L)) {
+            live |= 1u << j;
             if (!NACC_RENDER_RAYCACHE || it.rid[j] != cr) {
               gc = __ldg(gcv + it.rid[j]);
               gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
