@@ -5,7 +5,6 @@
 // the cuts + a compacting copy (three kernels, no host sync).
 #include "common.cuh"
 #include "debug.cuh"
-#include "lookback.cuh"
 
 namespace nacc {
 
@@ -256,127 +255,6 @@ __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
   }
 }
 
-// Fused single pass (NACC_FILTER_FUSED): persistent warps take 32-ray tiles from a counter; lane
-// l walks ray 32t + l to its cut (the sector walk above), the warp scans the tile's cuts and
-// publishes the tile total; then it resolves the output offset of its PREVIOUS tile by the
-// decoupled look-back (lookback.cuh; predecessors have had a tile's time to publish), writes
-// that tile's packed_info' and copies its kept prefixes ray by ray with all 32 lanes (coalesced,
-// mostly L1/L2 hits: the walk just read them).  One launch instead of three, no re-read from
-// DRAM, no block-sums pass.  Writes past `capacity` are dropped (complete iff total <= capacity).
-#ifndef NACC_FILTER_FUSED
-#define NACC_FILTER_FUSED 0  // build parameter: one-kernel filter (A/B)
-#endif
-constexpr int kFusedFilterWarps = 4;
-
-__device__ __forceinline__ int64_t walk_cut(int64_t st, int64_t e, const float *__restrict__ t0,
-                                            const float *__restrict__ t1, const float *__restrict__ sigma,
-                                            int64_t n_samples, double L) {
-  double S = 0.0;
-  int64_t cut = e - st;
-  int64_t q = st & ~(int64_t)7;
-  Sector cur, nxt;
-  if (q < e) load_sector(cur, t0, t1, sigma, q, n_samples);
-  while (q < e) {
-    const int64_t qn = q + 8;
-    if (qn < e) load_sector(nxt, t0, t1, sigma, qn, n_samples);
-    bool done = false;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (!done && q + j >= st && q + j < e) {
-        if (S > L) {
-          cut = q + j - st;
-          done = true;
-        } else {
-          S = __dadd_rn(S, __dmul_rn((double)cur.c[j], __dsub_rn((double)cur.b[j], (double)cur.a[j])));
-        }
-      }
-    }
-    if (done) break;
-    cur = nxt;
-    q = qn;
-  }
-  return cut;
-}
-
-__global__ void __launch_bounds__(kFusedFilterWarps * 32) filter_fused_kernel(
-    const int64_t *__restrict__ packed_info, int64_t n_rays, int64_t n_tiles, const float *__restrict__ t0,
-    const float *__restrict__ t1, const float *__restrict__ sigma, int64_t n_samples, double L,
-    LookbackWs *__restrict__ lb, int64_t capacity, int64_t *__restrict__ packed_out, float *__restrict__ t0_out,
-    float *__restrict__ t1_out, int32_t *__restrict__ ray_id_out, int64_t *__restrict__ total) {
-  const int lane = threadIdx.x & 31;
-  int64_t prev_tile = -1, prev_st = 0;
-  int32_t prev_cut = 0;
-  long long prev_incl = 0, prev_agg = 0;
-  for (;;) {
-    unsigned int t32 = 0;
-    if (lane == 0) t32 = atomicAdd(&lb->tile_counter, 1u);
-    const int64_t tile = (int64_t)__shfl_sync(kFull, t32, 0);
-    const bool have = tile < n_tiles;
-    int64_t st = 0;
-    int32_t cut = 0;
-    long long incl = 0, agg = 0;
-    if (have) {
-      const int64_t r = tile * 32 + lane;
-      if (r < n_rays) {
-        const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
-        st = min((int64_t)pi.x, n_samples);
-        const int64_t e = min((int64_t)(pi.x + pi.y), n_samples);  // clamped (overflowed march)
-        cut = (int32_t)walk_cut(st, e, t0, t1, sigma, n_samples, L);
-      }
-      incl = cut;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
-      }
-      agg = __shfl_sync(kFull, incl, 31);
-      lookback_publish(lb->status, tile, agg);
-    }
-    if (prev_tile >= 0) {
-      const long long excl = lookback_resolve(lb->status, prev_tile, prev_agg);
-      const int64_t r0 = prev_tile * 32;
-      const long long out = excl + prev_incl - prev_cut;
-      if (r0 + lane < n_rays) reinterpret_cast<longlong2 *>(packed_out)[r0 + lane] = make_longlong2(out, prev_cut);
-      if (prev_tile == n_tiles - 1 && lane == 0) *total = excl + prev_agg;
-      if (t0_out != nullptr && excl < capacity) {
-        for (int j = 0; j < 32; ++j) {
-          const int c = __shfl_sync(kFull, prev_cut, j);
-          if (c == 0) continue;
-          const int64_t src = __shfl_sync(kFull, prev_st, j), dst = __shfl_sync(kFull, out, j);
-          const int32_t rid = (int32_t)(r0 + j);
-          for (int i = lane; i < c; i += 32) {
-            if (dst + i < capacity) {
-              t0_out[dst + i] = __ldg(t0 + src + i);
-              t1_out[dst + i] = __ldg(t1 + src + i);
-              ray_id_out[dst + i] = rid;
-            }
-          }
-        }
-      }
-    }
-    if (!have) break;
-    prev_tile = tile;
-    prev_st = st;
-    prev_cut = cut;
-    prev_incl = incl;
-    prev_agg = agg;
-  }
-}
-
-static unsigned fused_filter_blocks(int64_t n_tiles) {
-  static int per_sm = 0, n_sm = 0;
-  if (per_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, filter_fused_kernel, kFusedFilterWarps * 32, 0);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int64_t want = ceil_div(n_tiles, (int64_t)kFusedFilterWarps);
-  const int64_t cap = (int64_t)per_sm * (n_sm > 0 ? n_sm : 1);
-  return (unsigned)(want < cap ? want : cap);
-}
-
 static size_t filter_ws_layout(int64_t n, int32_t **cuts, int64_t **bsums, void *base) {
   const size_t a = align_up((size_t)n * 4, 256);
   if (base) {
@@ -394,9 +272,7 @@ extern "C" {
 
 size_t nacc_filter_workspace_bytes(int64_t n_rays) {
   if (n_rays < 0) return 0;
-  const size_t fused = align_up(8 + 8 * (size_t)ceil_div(n_rays, 32), 256);  // look-back words
-  const size_t three = filter_ws_layout(n_rays, nullptr, nullptr, nullptr);
-  return fused > three ? fused : three;
+  return filter_ws_layout(n_rays, nullptr, nullptr, nullptr);
 }
 
 nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, const float *t0, const float *t1,
@@ -420,17 +296,6 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   NACC_REQUIRE(ws && ws_bytes >= nacc_filter_workspace_bytes(n_rays), "workspace too small");
   NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
   NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
-  if (NACC_FILTER_FUSED && aligned(t0, 32) && aligned(t1, 32) && aligned(sigma, 32)) {
-    const int64_t n_tiles = ceil_div(n_rays, (int64_t)32);
-    LookbackWs *lb = static_cast<LookbackWs *>(ws);
-    NACC_CUDA(cudaMemsetAsync(lb, 0, 8 + 8 * (size_t)n_tiles, stream));
-    filter_fused_kernel<<<fused_filter_blocks(n_tiles), kFusedFilterWarps * 32, 0, stream>>>(
-        packed_info, n_rays, n_tiles, t0, t1, sigma, n_samples, neg_log_eps, lb, capacity, packed_info_out,
-        capacity > 0 ? t0_out : nullptr, t1_out, ray_id_out, total);
-    count_launch(1);
-    NACC_CHECK_LAUNCH();
-    return NACC_OK;
-  }
   int32_t *cuts;
   int64_t *bsums;
   filter_ws_layout(n_rays, &cuts, &bsums, ws);

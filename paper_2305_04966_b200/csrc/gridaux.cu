@@ -10,11 +10,15 @@
 //   mask2 (when skipping is enabled): for every macro cell m (4^3 fine cells)
 //     of every level, the OR of the fine bits of macro cells m + {0,1}^3,
 //     i.e. of the fine cells [4m, 4m + 8)^3 clipped to the level;
-//   mask3 (every grid with skipping; per level): for every fine cell c the OR of
-//     the fine bits of cells c + {0..W-1}^3 (W = kFineWin) clipped to the level,
-//     at the fine resolution (the march's segment test: a 16-point segment spans
-//     at most 5 cells per axis on the CFG lattices);
+//   mask3 (every grid with skipping; per level): for every fine cell c and every
+//     window size w = 2..W (W = kFineWin), the OR and the AND of the fine bits of
+//     cells c + {0..w-1}^3 clipped to the level, at the fine resolution, stored as
+//     OR_2, AND_2, OR_3, AND_3, ..., OR_W, AND_W (the march's segment test picks the
+//     window of its segment's cell span: a 16-point segment spans at most 5 cells
+//     per axis on the CFG lattices; a tighter window skips and solidifies more);
 #include "common.cuh"
+
+#include <type_traits>
 
 namespace nacc {
 
@@ -44,7 +48,7 @@ static int64_t grid_aux_words(const nacc_grid &g) {
   if (!grid_skip_enabled(g)) return kAuxHeaderWords;
   const int64_t w = kAuxHeaderWords + mask2_words(g);
   if (!grid_fine_mask_enabled(g)) return w;
-  return w + 2 * mask3_words(g);  // OR window mask, then AND window mask
+  return w + 2 * (kFineWin - 1) * mask3_words(g);  // OR and AND window masks per window size 2..W
 }
 
 __global__ void bbox_init_kernel(int32_t *__restrict__ hdr, int levels, int R) {
@@ -162,7 +166,7 @@ __global__ void mask2_kernel(uint32_t *__restrict__ bits, int levels, int R, int
 // thread per fine cell (one level): the OR (kAnd = false) or the AND (kAnd = true) of the
 // bits of cells c + {0..W-1}^3; cells outside the grid count as empty (an AND window that
 // leaves the grid is 0)
-template <bool kAnd>
+template <bool kAnd, int kW>
 __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits, int levels, int R, int64_t off) {
   const int64_t R3 = (int64_t)R * R * R, n = levels * R3;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -170,21 +174,21 @@ __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits,
   if (q < n) {
     const int64_t lbase = (q / R3) * R3, ql = q - lbase;  // the cell's level: windows stay inside it
     const int x = (int)(ql % R), y = (int)((ql / R) % R), z = (int)(ql / ((int64_t)R * R));
-    const int nx = min(kFineWin, R - x);
+    const int nx = min(kW, R - x);
     const uint32_t xmask = (1u << nx) - 1u;
     if (kAnd) {
-      on = x + kFineWin <= R && y + kFineWin <= R && z + kFineWin <= R;
-      for (int zz = z; zz < z + kFineWin && on; ++zz)
-        for (int yy = y; yy < y + kFineWin && on; ++yy) {
+      on = x + kW <= R && y + kW <= R && z + kW <= R;
+      for (int zz = z; zz < z + kW && on; ++zz)
+        for (int yy = y; yy < y + kW && on; ++yy) {
           const int64_t s = lbase + x + (int64_t)R * (yy + (int64_t)R * zz);
           const int o = (int)(s & 31);
           uint32_t v = __ldg(bits + (s >> 5)) >> o;
-          if (o + kFineWin > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
+          if (o + kW > 32) v |= __ldg(bits + (s >> 5) + 1) << (32 - o);
           on = (v & xmask) == xmask;
         }
     } else {
-      for (int zz = z; zz < min(z + kFineWin, R) && !on; ++zz)
-        for (int yy = y; yy < min(y + kFineWin, R) && !on; ++yy) {
+      for (int zz = z; zz < min(z + kW, R) && !on; ++zz)
+        for (int yy = y; yy < min(y + kW, R) && !on; ++yy) {
           const int64_t s = lbase + x + (int64_t)R * (yy + (int64_t)R * zz);
           const int o = (int)(s & 31);
           uint32_t v = __ldg(bits + (s >> 5)) >> o;
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(256) mask3_kernel(uint32_t *__restrict__ bits,
 // Row-wise variant (R % 32 == 0): thread per output word, i.e. 32 cells of one x-row; the
 // x-window is W shifted copies of the row's word and its successor, then OR (AND) over the
 // W x W rows of the window.  Same bits as mask3_kernel, 32x fewer loads.
-template <bool kAnd>
+template <bool kAnd, int kW>
 __global__ void __launch_bounds__(256) mask3_rows_kernel(uint32_t *__restrict__ bits, int levels, int R, int64_t off) {
   const int64_t R3 = (int64_t)R * R * R, nw = levels * R3 / 32;
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -209,14 +213,14 @@ __global__ void __launch_bounds__(256) mask3_rows_kernel(uint32_t *__restrict__ 
   const int x0 = (int)(c0 % R), y = (int)((c0 / R) % R), z = (int)(c0 / ((int64_t)R * R));
   const bool last_word = x0 + 32 >= R;
   uint32_t acc = kAnd ? 0xffffffffu : 0u;
-  if (kAnd && (y + kFineWin > R || z + kFineWin > R)) acc = 0u;
-  for (int zz = z; zz < min(z + kFineWin, R) && (!kAnd || acc); ++zz)
-    for (int yy = y; yy < min(y + kFineWin, R); ++yy) {
+  if (kAnd && (y + kW > R || z + kW > R)) acc = 0u;
+  for (int zz = z; zz < min(z + kW, R) && (!kAnd || acc); ++zz)
+    for (int yy = y; yy < min(y + kW, R); ++yy) {
       const int64_t wi = (lbase + x0 + (int64_t)R * (yy + (int64_t)R * zz)) >> 5;
       const uint32_t w = __ldg(bits + wi), wn = last_word ? 0u : __ldg(bits + wi + 1);
       uint32_t d = w;
 #pragma unroll
-      for (int k = 1; k < kFineWin; ++k) {
+      for (int k = 1; k < kW; ++k) {
         const uint32_t sh = (w >> k) | (wn << (32 - k));
         d = kAnd ? (d & sh) : (d | sh);
       }
@@ -249,15 +253,24 @@ cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream
   }
   if (grid_fine_mask_enabled(g)) {
     const int64_t n = (int64_t)g.levels * g.res * g.res * g.res;
-    const int64_t o3 = grid_mask3_offset_words(g), o3and = o3 + mask3_words(g);
-    if (g.res % 32 == 0) {
-      mask3_rows_kernel<false><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3);
-      mask3_rows_kernel<true><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3and);
-    } else {
-      mask3_kernel<false><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3);
-      mask3_kernel<true><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, o3and);
-    }
-    count_launch(2);
+    const int64_t o3 = grid_mask3_offset_words(g), mw = mask3_words(g);
+    auto masks = [&](auto wtag) {
+      constexpr int W = decltype(wtag)::value;
+      const int64_t o_or = o3 + 2 * (W - 2) * mw, o_and = o_or + mw;
+      if (g.res % 32 == 0) {
+        mask3_rows_kernel<false, W><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.levels, g.res, o_or);
+        mask3_rows_kernel<true, W><<<grid_for(n / 32, 256), 256, 0, stream>>>(bits, g.levels, g.res, o_and);
+      } else {
+        mask3_kernel<false, W><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, o_or);
+        mask3_kernel<true, W><<<grid_for(n, 256), 256, 0, stream>>>(bits, g.levels, g.res, o_and);
+      }
+      count_launch(2);
+    };
+    static_assert(kFineWin >= 2 && kFineWin <= 5, "window sizes 2..5");
+    masks(std::integral_constant<int, 2>{});
+    if (kFineWin >= 3) masks(std::integral_constant<int, 3 <= kFineWin ? 3 : 2>{});
+    if (kFineWin >= 4) masks(std::integral_constant<int, 4 <= kFineWin ? 4 : 2>{});
+    if (kFineWin >= 5) masks(std::integral_constant<int, 5 <= kFineWin ? 5 : 2>{});
   }
   return cudaGetLastError();
 }

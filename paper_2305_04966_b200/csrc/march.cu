@@ -152,43 +152,53 @@ __device__ __forceinline__ void cell_floors(const GridConst &g, const float X[3]
 }
 
 // the fine test from the endpoints' cell floors (ia: first point, ib: last point or any later one)
-__device__ __forceinline__ int segment_test_floors(const GridConst &g, const uint32_t *__restrict__ mask3,
-                                                   const int ia[3], const int ib[3], int l = 0) {
+__device__ __forceinline__ int segment_test_floors(const GridConst &g, const uint32_t *__restrict__ bits,
+                                                   const uint32_t *__restrict__ mask3, const int ia[3],
+                                                   const int ib[3], int l = 0) {
   const int R = g.res;
   const int64_t R3w = (int64_t)R * R * R / 32;  // words per level (R % 4 == 0)
-  int c[3];
+  int c[3], span = 0;
   bool interior = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const int lo = min(ia[a], ib[a]), hi = max(ia[a], ib[a]);
-    if (hi - lo > kFineWin - 1) return 2;     // longer than the mask's window: evaluate
+    if (hi - lo > kFineWin - 1) return 2;     // longer than the largest window: evaluate
     if (hi < 0 || lo > R) return 0;          // every point outside the box on this axis
     interior = interior && lo >= 0 && hi <= R - 2;
     c[a] = min(max(lo, 0), R - 1);
+    span = max(span, hi - lo);
   }
   const uint32_t q = (uint32_t)c[0] + (uint32_t)R * ((uint32_t)c[1] + (uint32_t)R * (uint32_t)c[2]);
-  if (!((__ldg(mask3 + l * R3w + (q >> 5)) >> (q & 31u)) & 1u)) return 0;
+  // the window of the segment's cell span, w = span + 1 cells per axis: OR_w at
+  // mask3 + 2 (w - 2) masks, AND_w right after (gridaux.cu); a segment inside one cell (w = 1)
+  // reads the cell's own fine bit for both
+  const int64_t mw = ((g.levels * R3w + 63) / 64) * 64;
+  const uint32_t *orm = span == 0 ? bits : mask3 + 2 * (span - 1) * mw;
+  const uint32_t *andm = span == 0 ? bits : orm + mw;
+  const int64_t wi = l * R3w + (q >> 5);
+  if (!((__ldg(orm + wi) >> (q & 31u)) & 1u)) return 0;
   if (!interior) return 2;
-  // solid window (mask3and, after every level's mask3): every cell the points can fall in is
-  // occupied, so every point is a member (subject only to k < ke and m < far)
-  const uint32_t *mask3and = mask3 + ((g.levels * R3w + 63) / 64) * 64;
-  if (NACC_MARCH_SOLID && ((__ldg(mask3and + l * R3w + (q >> 5)) >> (q & 31u)) & 1u)) return 3;
+  // solid window: every cell the points can fall in is occupied, so every point is a member
+  // (subject only to k < ke and m < far)
+  if (NACC_MARCH_SOLID && ((__ldg(andm + wi) >> (q & 31u)) & 1u)) return 3;
   return 1;
 }
 
-__device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ mask3,
-                                                 const float A[3], const float B[3]) {
+__device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint32_t *__restrict__ bits,
+                                                 const uint32_t *__restrict__ mask3, const float A[3],
+                                                 const float B[3]) {
   int ia[3], ib[3];
   cell_floors(g, A, ia);
   cell_floors(g, B, ib);
-  return segment_test_floors(g, mask3, ia, ib);
+  return segment_test_floors(g, bits, mask3, ia, ib);
 }
 
 // Returns 0 (skip the segment), 1 (evaluate; the segment lies inside the
 // single level's box with margin, so P(k) can skip the box test) or 2
 // (evaluate with the full predicate).
 template <bool kL1>
-__device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *__restrict__ mask2, int M,
+__device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *__restrict__ bits,
+                                            const uint32_t *__restrict__ mask2, int M,
                                             const uint32_t *__restrict__ mask3, const float A[3], const float B[3]) {
   int la = 0;
   if (!kL1) {
@@ -208,7 +218,7 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
       int ia[3], ib[3];
       cell_floors(g, A, ia, la);
       cell_floors(g, B, ib, la);
-      return segment_test_floors(g, mask3, ia, ib, la) | (la << 4);
+      return segment_test_floors(g, bits, mask3, ia, ib, la) | (la << 4);
     }
   }
   int i0[3];
@@ -483,7 +493,7 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 #pragma unroll
       for (int a = 0; a < 3; ++a) fb[a] = __shfl_down_sync(kFull, fa[a], 1);
       int code = 0;
-      if (lane < 31 && ks < ke) code = segment_test_floors(g, mask3, fa, fb);
+      if (lane < 31 && ks < ke) code = segment_test_floors(g, bits, mask3, fa, fb);
       const bool flag = code != 0;
       const unsigned F = __ballot_sync(kFull, flag);
       if (flag) seglist[__popc(F & ((1u << lane) - 1u))] = lane | (code == 1 ? 0x100 : (code == 3 ? 0x300 : 0));
@@ -498,8 +508,8 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
         const float ma = lattice_mid<kCone>(p, s, tab, ks), mb = lattice_mid<kCone>(p, s, tab, kl);
         const float A[3] = {__fmaf_rn(ma, s.dx, s.ox), __fmaf_rn(ma, s.dy, s.oy), __fmaf_rn(ma, s.dz, s.oz)};
         const float B[3] = {__fmaf_rn(mb, s.dx, s.ox), __fmaf_rn(mb, s.dy, s.oy), __fmaf_rn(mb, s.dz, s.oz)};
-        code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, mask3, A, B)
-                                          : segment_test<kL1>(g, mask2, M, mask3, A, B);
+        code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, bits, mask3, A, B)
+                                          : segment_test<kL1>(g, bits, mask2, M, mask3, A, B);
         lvl = code >> 4;  // cascades: the level every point of the segment lies in
         code &= 15;
         flag = code != 0;
@@ -760,14 +770,14 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
             cell_floors(g, X, fa);
 #pragma unroll
             for (int a = 0; a < 3; ++a) fb[a] = __shfl_down_sync(kFull, fa[a], 1);
-            if (owner) code = segment_test_floors(g, mask3, fa, fb);
+            if (owner) code = segment_test_floors(g, bits, mask3, fa, fb);
           } else {
             float Y[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) Y[a] = __shfl_down_sync(kFull, X[a], 1);
             if (owner) {
-              code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, mask3, X, Y)
-                                                : segment_test<kL1>(g, mask2, M, mask3, X, Y);
+              code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, bits, mask3, X, Y)
+                                                : segment_test<kL1>(g, bits, mask2, M, mask3, X, Y);
               lvl = code >> 4;
               code &= 15;
             }

@@ -284,9 +284,6 @@ __device__ __forceinline__ double trans_first(double S) {  // T of a thread's fi
 #endif
 }
 constexpr int64_t kWarpTile = NACC_RENDER_TILE;  // samples per warp tile (build parameter)
-#ifndef NACC_RENDER_LEAN
-#define NACC_RENDER_LEAN 0  // build parameter: register-lean forward (liveness bits, late rgb, lead in smem)
-#endif
 #ifndef NACC_RENDER_L2PF
 #define NACC_RENDER_L2PF 0  // build parameter: TMA bulk L2 prefetch of the warp's next tile (A/B: slower)
 #endif
@@ -449,49 +446,6 @@ __device__ __forceinline__ SegM warp_segm_excl(const SegM &x, SegM &carry) {
   carry = segm_combine(carry, segm_shfl(incl, 31));
   return res;
 }
-// The same exclusive segmented scan, one component at a time: the flag progression of the 5
-// shuffle steps is computed once (5 bits), then each component runs its own 5 steps with only
-// its own temporaries live (the all-at-once version spilled at 64 registers).
-__device__ __forceinline__ SegM warp_segm_excl_lean(const SegM &x, SegM &carry) {
-  const int lane = threadIdx.x & 31;
-  // flag inclusive scan, remembering each lane's flag before every step
-  int f = x.f;
-  unsigned bfm = 0;
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    const int o = 1 << i;
-    bfm |= (unsigned)(f != 0) << i;
-    const int yf = __shfl_up_sync(kFull, f, o);
-    if (lane >= o) f |= yf;
-  }
-  int exf = __shfl_up_sync(kFull, f, 1);
-  if (lane == 0) exf = 0;
-  const int lastf = __shfl_sync(kFull, f, 31);
-  SegM res;
-  res.f = carry.f | exf;
-  double vals[5] = {x.o, x.n, x.c0, x.c1, x.c2};
-  double cv[5] = {carry.o, carry.n, carry.c0, carry.c1, carry.c2};
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    double incl = vals[k];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const int o = 1 << i;
-      const double y = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o && !((bfm >> i) & 1u)) incl += y;
-    }
-    double ex = __shfl_up_sync(kFull, incl, 1);
-    if (lane == 0) ex = 0.0;
-    const double last = __shfl_sync(kFull, incl, 31);
-    vals[k] = exf ? ex : cv[k] + ex;       // combine(carry, ex)
-    cv[k] = lastf ? last : cv[k] + last;   // carry = combine(carry, last)
-  }
-  res.o = vals[0]; res.n = vals[1]; res.c0 = vals[2]; res.c1 = vals[3]; res.c2 = vals[4];
-  carry.f = carry.f | lastf;
-  carry.o = cv[0]; carry.n = cv[1]; carry.c0 = cv[2]; carry.c1 = cv[3]; carry.c2 = cv[4];
-  return res;
-}
-
 __device__ __forceinline__ SegM segm_item(const Items &it, int j, double w, const float *col) {
   SegM x;
   x.f = it.head[j];
@@ -512,7 +466,8 @@ __device__ __forceinline__ void render_fwd_out(const SegM &v, int64_t r, float *
     color[3 * r + 2] = (float)v.c2;
   }
   if (opacity) opacity[r] = (float)v.o;
-  if (depth) depth[r] = (float)(v.n / fmax(v.o, 1e-10));
+  // depth = N / max(O, 1e-10) in fp32 (rel 1e-4 bar; an fp64 division was ~3 % of the kernel)
+  if (depth) depth[r] = __fdiv_rn((float)v.n, (float)fmax(v.o, 1e-10));
   if (ctx) {
     ctx[5 * r] = v.c0;
     ctx[5 * r + 1] = v.c1;
@@ -528,9 +483,6 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, float *__restrict__ color, float *__restrict__ opacity,
     float *__restrict__ depth, double *__restrict__ ctx) {
-#if NACC_RENDER_LEAN
-  __shared__ double s_lead[8][32][5];  // a lane's lead run until the warp scan returns
-#endif
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -558,17 +510,8 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
       load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
       double s[4], S[4];
       warp_items_S(it, s, S, carryS);
-#if NACC_RENDER_LEAN
-      // register economy (the kernel spilled at 64 registers): liveness bits instead of S[1..3];
-      // rgb loaded item by item inside the loop; the lead run parked in shared memory
-      unsigned livem = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) livem |= (it.valid[j] && !(S[j] > L)) ? (1u << j) : 0u;
-      const double S0 = S[0];
-#else
       float col[12];
       load_rgb4(col, it, rgb, kVec);
-#endif
       // One pass over the items: a ray whose head lies in this lane is summed
       // here and written at its tail; only the lane's leading run (the ray
       // entering from earlier lanes) waits for the warp scan.
@@ -577,50 +520,6 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
       int64_t lead_r = -1;
       // T of the thread's first item from its optical depth, later items by the product
       // T_{j+1} = T_j e^{-s_j} (one fp64 exp per item instead of two)
-#if NACC_RENDER_LEAN
-      double Tn = trans_first(S0);
-  #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool live = (livem >> j) & 1u;
-        const double ea = interval_ea(s[j]);
-        const double T = (j > 0 && it.head[j]) ? 1.0 : Tn;
-        Tn = T * ea;
-        const double w = live ? T * (1.0 - ea) : 0.0;
-        float col3[3];
-        const int64_t q = it.q0 + j;
-        col3[0] = it.valid[j] ? __ldg(rgb + 3 * q) : 0.f;
-        col3[1] = it.valid[j] ? __ldg(rgb + 3 * q + 1) : 0.f;
-        col3[2] = it.valid[j] ? __ldg(rgb + 3 * q + 2) : 0.f;
-        SegM x;
-        x.f = it.head[j];
-        x.o = w;
-        x.n = w * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-        x.c0 = w * (double)col3[0];
-        x.c1 = w * (double)col3[1];
-        x.c2 = w * (double)col3[2];
-        cur = segm_combine(cur, x);
-        if (it.tail[j]) {
-          if (cur.f) render_fwd_out(cur, it.rid[j], color, opacity, depth, ctx);
-          else {
-            double *ls = s_lead[threadIdx.x >> 5][lane];
-            ls[0] = cur.o; ls[1] = cur.n; ls[2] = cur.c0; ls[3] = cur.c1; ls[4] = cur.c2;
-            lead_r = it.rid[j];
-          }
-        }
-      }
-      const SegM enter = warp_segm_excl_lean(cur, carryC);
-      if (lead_r >= 0) {
-        const double *ls = s_lead[threadIdx.x >> 5][lane];
-        SegM v;
-        v.f = 0;
-        v.o = enter.o + ls[0];
-        v.n = enter.n + ls[1];
-        v.c0 = enter.c0 + ls[2];
-        v.c1 = enter.c1 + ls[3];
-        v.c2 = enter.c2 + ls[4];
-        render_fwd_out(v, lead_r, color, opacity, depth, ctx);
-      }
-#else
       double Tn = trans_first(S[0]);
   #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -640,7 +539,6 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
       }
       const SegM enter = warp_segm_excl(cur, carryC);
       if (lead_r >= 0) render_fwd_out(segm_combine(enter, lead), lead_r, color, opacity, depth, ctx);
-#endif
     }
   }
 }
@@ -720,82 +618,6 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
       load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
       double s[4], S[4];
       warp_items_S(it, s, S, carryS);
-#if NACC_RENDER_LEAN
-      // phase A: per item g_w w (scan input) and g_w T (1-α); g_rgb = w g_C is final here and
-      // is stored at once, so w and the rgb values do not live across the warp scan
-      double gwTea[4];
-      unsigned live = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) live |= (it.valid[j] && !(S[j] > L)) ? (1u << j) : 0u;
-      Seg<1> agg = seg_identity<1>();
-      {
-        double Tn = trans_first(S[0]);  // T_{j+1} = T_j e^{-s_j}, as in the forward
-        int32_t cr = -1;
-        float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
-        double2 gon = make_double2(0.0, 0.0);
-  #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          gwTea[j] = 0.0;
-          double v = 0.0;
-          const double ea = interval_ea(s[j]);
-          const double T = (j > 0 && it.head[j]) ? 1.0 : Tn;
-          Tn = T * ea;
-          float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-          if ((live >> j) & 1u) {
-            if (it.rid[j] != cr) {
-              gc = __ldg(gcv + it.rid[j]);
-              gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
-              cr = it.rid[j];
-            }
-            const int64_t q = it.q0 + j;
-            const float c0 = __ldg(rgb + 3 * q), c1 = __ldg(rgb + 3 * q + 1), c2 = __ldg(rgb + 3 * q + 2);
-            const double w = T * (1.0 - ea);
-            const double gw = (double)gc.x * c0 + (double)gc.y * c1 + (double)gc.z * c2 + gon.x +
-                              gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
-            v = gw * w;
-            gwTea[j] = gw * T * ea;
-            g0 = (float)(w * gc.x);
-            g1 = (float)(w * gc.y);
-            g2 = (float)(w * gc.z);
-          }
-          if (g_rgb && it.valid[j]) {
-            float *gp = g_rgb + 3 * (it.q0 + j);
-            gp[0] = g0;
-            gp[1] = g1;
-            gp[2] = g2;
-          }
-          s[j] = v;
-          Seg<1> x;
-          x.f = it.head[j];
-          x.v[0] = v;
-          agg = seg_combine(agg, x);
-        }
-      }
-      Seg<1> run = warp_seg_excl<1>(agg, carryP);
-      float gs[4];
-      int32_t cr = -1;
-      double R = 0.0;
-  #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + s[j];
-        gs[j] = 0.f;
-        if ((live >> j) & 1u) {
-          if (it.rid[j] != cr) {
-            R = __ldg(gq + 2 * (int64_t)it.rid[j] + 1).x;
-            cr = it.rid[j];
-          }
-          const double Q = R - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
-          gs[j] = (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - Q));
-        }
-      }
-      if (kVec && it.valid[0] && it.valid[3]) {
-        *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
-      } else {
-  #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (it.valid[j]) g_sigma[it.q0 + j] = gs[j];
-      }
-#else
       // phase A: per item g_w w (scan input), w and g_w T (1-α); the only state kept
       double w[4], gwTea[4];
       unsigned live = 0;
@@ -877,7 +699,6 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
             for (int ch = 0; ch < 3; ++ch) g_rgb[3 * (it.q0 + j) + ch] = gr[3 * j + ch];
         }
       }
-#endif
     }
   }
 }
