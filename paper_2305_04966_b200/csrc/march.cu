@@ -595,7 +595,7 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 //   point as the segment's far end (a later point: a superset by monotonicity,
 //   reading #22).  A pass advances 31 slots.
 // Flagged segments get entries, in (ray, k) order, in the warp's shared entry
-// buffer: (j << 28) | (q << 16) | mask of the segment's emitted points.  A
+// buffer: (j << (16 + kQBits)) | (q << 16) | mask of the segment's emitted points.  A
 // solid segment (every point provably a member, all < ke and < far) writes its
 // full mask at once; the others are queued and evaluated exactly, two
 // segments per 32-lane pass, filling in their masks.  Per-ray counts
@@ -621,7 +621,21 @@ constexpr int kFWarps = NACC_MARCH_WARPS, kTRays = NACC_MARCH_TRAYS, kECap = NAC
 constexpr int tile_rays(bool cone, bool l1) { return (cone || !l1) ? kTRays / 2 : kTRays; }
 constexpr int kTSeg = 16;   // lattice points per segment / entry mask bits
 constexpr int kEvCap = 64;  // queued segments awaiting evaluation
-static_assert(kTRays <= 16, "4-bit ray index in the entries");
+static_assert(kTRays <= 32, "one lane per ray of a tile");
+// entry = (j << (16 + kQBits)) | (q << 16) | 16-bit mask: ray index j, segment index q
+constexpr int kJBits = kTRays > 16 ? 5 : 4;
+constexpr int kQBits = 16 - kJBits;
+constexpr uint32_t kQMask = (1u << kQBits) - 1u;
+__device__ __forceinline__ uint32_t ent_pack(int j, int q, uint32_t mask) {
+  return ((uint32_t)j << (16 + kQBits)) | ((uint32_t)q << 16) | mask;
+}
+__device__ __forceinline__ int ent_j(uint32_t e) { return (int)(e >> (16 + kQBits)); }
+__device__ __forceinline__ int ent_k16(uint32_t e) { return (int)((e >> 12) & (kQMask << 4)); }  // 16 q
+// queued segment = slot (10 bits) | j | q | code (2 bits, at 26) | level (3 bits, at 28)
+__device__ __forceinline__ uint32_t evq_pack(int slot, int j, int q, int code, int lvl) {
+  return (uint32_t)min(slot, 1023) | ((uint32_t)j << 10) | ((uint32_t)q << (10 + kJBits)) | ((uint32_t)code << 26) |
+         ((uint32_t)lvl << 28);
+}
 static_assert(kECap <= 1024, "10-bit entry slot in the evaluation queue");
 static_assert(NACC_MARCH_SEG == kTSeg && NACC_MARCH_SEG_CASCADE == kTSeg, "16-point segments");
 
@@ -661,7 +675,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
   const int K = kCone ? (int)hdr->K : 0;
   // the previous tile, pending its phase 2 (lane j < kR: ray j)
   int64_t prev_tile = -1;
-  int prev_c = 0;
+  int prev_c = 0, prev_ne = 0;
   long long prev_agg = 0;
   bool prev_over = false;
   int buf = 0;
@@ -670,7 +684,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
     if (lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
     const int64_t tile = (int64_t)__shfl_sync(kFull, tile32, 0);
     const bool have = tile < n_tiles;
-    int cur_c = 0;
+    int cur_c = 0, cur_ne = 0;
     long long cur_agg = 0;
     bool cur_over = false;
     if (have) {
@@ -700,7 +714,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
         }
         T.kr[lane] = make_int2(kb, ke);
         T.cnt[lane] = 0;
-        longray = nseg >= 4096;
+        longray = nseg > (int)kQMask;
       }
       // flat slot list: ray j owns slots [base_j, base_j + nseg_j], every ray at least one
       const int nslot = lane < kR ? nseg + 1 : 0;
@@ -723,7 +737,8 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
         for (int e0 = 0; e0 < n_eval; e0 += 2) {
           const int idx = e0 + (lane >> 4);
           const uint32_t qe = idx < n_eval ? evq[warp][idx] : 0u;
-          const int j = (qe >> 10) & 15, q = (qe >> 14) & 4095, code = (qe >> 26) & 3, lv = (qe >> 28) & 7;
+          const int j = (qe >> 10) & ((1 << kJBits) - 1), q = (qe >> (10 + kJBits)) & kQMask, code = (qe >> 26) & 3,
+                    lv = (qe >> 28) & 7;
           const int2 kr = T.kr[j];
           const int k = kr.x + q * kTSeg + (lane & 15);
           bool pred = false;
@@ -739,7 +754,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           if ((lane & 15) == 0 && idx < n_eval) {
             const uint32_t half = (lane ? bal >> 16 : bal) & 0xFFFFu;
             const int slot = qe & 1023;
-            if (slot < kECap) T.ent[slot] = ((uint32_t)j << 28) | ((uint32_t)q << 16) | half;
+            if (slot < kECap) T.ent[slot] = ent_pack(j, q, half);
             atomicAdd(&T.cnt[j], __popc(half));
           }
         }
@@ -788,24 +803,24 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           const unsigned F = __ballot_sync(kFull, flag), Dm = __ballot_sync(kFull, direct);
           const int slot = n_ent + __popc(F & lt);
           if (direct) {
-            if (slot < kECap) T.ent[slot] = ((uint32_t)j << 28) | ((uint32_t)q << 16) | 0xFFFFu;
+            if (slot < kECap) T.ent[slot] = ent_pack(j, q, 0xFFFFu);
             atomicAdd(&T.cnt[j], kTSeg);
           } else if (flag) {
-            evq[warp][npend + __popc((F & ~Dm) & lt)] = (uint32_t)min(slot, 1023) | ((uint32_t)j << 10) |
-                                                        ((uint32_t)q << 14) | ((uint32_t)code << 26) |
-                                                        ((uint32_t)lvl << 28);
+            evq[warp][npend + __popc((F & ~Dm) & lt)] = evq_pack(slot, j, q, code, lvl);
           }
           n_ent += __popc(F);
           npend += __popc(F & ~Dm);
           __syncwarp();
-          if (npend >= 32) {  // keep the queue short: evaluate all but an odd one
-            const int ne = npend & ~1;
+          if (npend >= 32) {  // keep the queue short: evaluate whole passes, keep the remainder
+            constexpr int kPerPass = 2;
+            const int ne = npend & ~(kPerPass - 1);
             evaluate(ne);
-            if (npend & 1) {
-              if (lane == 0) evq[warp][0] = evq[warp][ne];
-              __syncwarp();
-            }
-            npend &= 1;
+            const int rest = npend - ne;
+            const uint32_t keep = lane < rest ? evq[warp][ne + lane] : 0u;
+            __syncwarp();
+            if (lane < rest) evq[warp][lane] = keep;
+            __syncwarp();
+            npend = rest;
           }
         }
         evaluate(npend);
@@ -834,8 +849,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
       for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(kFull, agg, o);
       cur_agg = agg;
       lookback_publish(lb->status, tile, cur_agg);
-      // the entry count travels in lane 31's cur_c slot (lanes >= kR hold no ray)
-      if (lane == 31) cur_c = n_ent;
+      cur_ne = n_ent;
     }
     if (prev_tile >= 0) {
       // ---------------- phase 2 of the previous tile (buffer buf ^ 1)
@@ -862,21 +876,21 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
         reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(run, c);
       if (t0 != nullptr && excl + prev_agg <= capacity) {
         if (!prev_over) {
-          const int n_ent = __shfl_sync(kFull, prev_c, 31);
-          const int b = lane & 15;
+          const int n_ent = prev_ne;
           float *__restrict__ o0 = t0 + excl;
           float *__restrict__ o1 = t1 + excl;
           int32_t *__restrict__ oid = ray_id + excl;
           int carry = 0;  // samples written so far in the tile
+          const int b = lane & 15;
           for (int e = 0; e < n_ent; e += 2) {
             const int idx = e + (lane >> 4);
             const uint32_t ent = idx < n_ent ? T.ent[idx] : 0u;
             const bool set = (ent >> b) & 1u;
             const unsigned bal = __ballot_sync(kFull, set);  // both entries' masks, in output order
             if (set) {
-              const int j = ent >> 28;
+              const int j = ent_j(ent);
               const int pos = carry + __popc(bal & lt);
-              const int k = T.kr[j].x + (int)((ent >> 12) & 0xFFF0u) + b;  // kb_j + 16 q + b
+              const int k = T.kr[j].x + ent_k16(ent) + b;  // kb_j + 16 q + b
               float ta, tb2;
               lattice_ends<kCone>(p, T.od[j][0].w, tab, k, ta, tb2);
               o0[pos] = ta;
@@ -911,6 +925,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
     if (!have) break;
     prev_tile = tile;
     prev_c = cur_c;
+    prev_ne = cur_ne;
     prev_agg = cur_agg;
     prev_over = cur_over;
     buf ^= 1;
