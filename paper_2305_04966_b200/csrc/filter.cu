@@ -255,167 +255,6 @@ __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
   }
 }
 
-// Hybrid cut (NACC_FILTER_HYBRID): the thread-per-ray walk's time is set by its longest rays
-// (one dependent sector load per 8 samples, lanes of a warp idle once their rays end).
-// Pass A: every thread reads the first two sectors of its ray at once (>= 9 samples) and sums
-// them in the definition's order; rays resolved there write their cut.  The others (their
-// exact sequential S and the next sector) go to a queue.  Pass B: one warp per queued ray,
-// 32 samples per step, fp64 warp scan continuing from the exact S; as in every parallel sum,
-// a decision within the rounding band |S_i - L| <= (cnt + 8) 2^-50 L at or before the cut
-// sends the ray to a sequential recompute (O5 order), so cuts stay bit-identical.
-#ifndef NACC_FILTER_HYBRID
-#define NACC_FILTER_HYBRID 1  // build parameter: two-pass cut (short walk + warp per long ray)
-#endif
-
-struct HybridWs {
-  int32_t *cuts;
-  int64_t *bsums;
-  unsigned long long *qcount;
-  int32_t *queue;
-  double *qS;
-  int64_t *qnext;
-};
-
-__global__ void __launch_bounds__(kCutThreads) filter_cut_short_kernel(
-    const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
-    const float *__restrict__ t1, const float *__restrict__ sigma, int64_t n_samples, double L, HybridWs w) {
-  const int64_t r = (int64_t)blockIdx.x * kCutThreads + threadIdx.x;
-  int64_t cut = 0;
-  bool queued = false;
-  if (r < n_rays) {
-    const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
-    const int64_t st = min((int64_t)pi.x, n_samples), e = min((int64_t)(pi.x + pi.y), n_samples);
-    const int64_t q0 = st & ~(int64_t)7;
-    Sector a, b;
-    if (q0 < e) load_sector(a, t0, t1, sigma, q0, n_samples);
-    if (q0 + 8 < e) load_sector(b, t0, t1, sigma, q0 + 8, n_samples);
-    double S = 0.0;
-    int64_t c = -1;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t i = q0 + j;
-      if (c < 0 && i >= st && i < e) {
-        if (S > L) c = i - st;
-        else S = __dadd_rn(S, __dmul_rn((double)a.c[j], __dsub_rn((double)a.b[j], (double)a.a[j])));
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t i = q0 + 8 + j;
-      if (c < 0 && i < e) {
-        if (S > L) c = i - st;
-        else S = __dadd_rn(S, __dmul_rn((double)b.c[j], __dsub_rn((double)b.b[j], (double)b.a[j])));
-      }
-    }
-    if (c < 0 && q0 + 16 >= e) c = e - st;  // every sample read and kept
-    if (c >= 0) {
-      cut = c;
-      w.cuts[r] = (int32_t)c;
-    } else {
-      queued = true;
-      w.qS[r] = S;
-      w.qnext[r] = q0 + 16;
-    }
-  }
-  // queue the unresolved rays (warp-aggregated append; order is irrelevant)
-  const unsigned qm = __ballot_sync(kFull, queued);
-  if (qm) {
-    unsigned long long base = 0;
-    const int lane = threadIdx.x & 31;
-    if (lane == __ffs(qm) - 1) base = atomicAdd(w.qcount, (unsigned long long)__popc(qm));
-    base = __shfl_sync(kFull, base, __ffs(qm) - 1);
-    if (queued) w.queue[base + __popc(qm & ((1u << lane) - 1u))] = (int32_t)r;
-  }
-  const int64_t tot = warp_sum_i64(cut);
-  const int64_t r_warp = r - (threadIdx.x & 31);
-  if ((threadIdx.x & 31) == 0 && tot)
-    atomicAdd(reinterpret_cast<unsigned long long *>(w.bsums + r_warp / kFiltRays), (unsigned long long)tot);
-}
-
-__global__ void __launch_bounds__(256) filter_cut_long_kernel(
-    const int64_t *__restrict__ packed_info, const float *__restrict__ t0, const float *__restrict__ t1,
-    const float *__restrict__ sigma, int64_t n_samples, double L, HybridWs w) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t nq = (int64_t)*w.qcount;
-  for (int64_t qi = gw; qi < nq; qi += nw) {
-    const int32_t r = w.queue[qi];
-    const longlong2 pi = __ldg(reinterpret_cast<const longlong2 *>(packed_info) + r);
-    const int64_t st = min((int64_t)pi.x, n_samples), e = min((int64_t)(pi.x + pi.y), n_samples);
-    const double tol = L * (double)(e - st + 8) * 0x1p-50;
-    double carry = w.qS[r];
-    int64_t cut = e - st;
-    bool amb = false;
-    for (int64_t q0 = w.qnext[r]; q0 < e; q0 += 32) {
-      const int64_t i = q0 + lane;
-      const bool in = i < e;
-      const double sv = in ? __dmul_rn((double)__ldg(sigma + i), __dsub_rn((double)__ldg(t1 + i), (double)__ldg(t0 + i)))
-                           : 0.0;
-      const double incl = warp_incl_scan(sv);
-      const double S = __dadd_rn(carry, __dsub_rn(incl, sv));  // entering optical depth of item i
-      const unsigned over = __ballot_sync(kFull, in && S > L);
-      const int first = over ? __ffs(over) - 1 : 32;
-      amb |= __any_sync(kFull, in && lane <= first && fabs(S - L) <= tol);
-      if (over) {
-        cut = q0 + first - st;
-        break;
-      }
-      carry = __dadd_rn(carry, __shfl_sync(kFull, incl, 31));
-    }
-    if (amb) {  // the definition's sequential order (O5)
-      int64_t c2 = e - st;
-      if (lane == 0) {
-        double S = 0.0;
-        for (int64_t i = st; i < e; ++i) {
-          if (S > L) {
-            c2 = i - st;
-            break;
-          }
-          S = __dadd_rn(S, __dmul_rn((double)__ldg(sigma + i), __dsub_rn((double)__ldg(t1 + i), (double)__ldg(t0 + i))));
-        }
-      }
-      cut = __shfl_sync(kFull, c2, 0);
-    }
-    if (lane == 0) {
-      w.cuts[r] = (int32_t)cut;
-      if (cut) atomicAdd(reinterpret_cast<unsigned long long *>(w.bsums + r / kFiltRays), (unsigned long long)cut);
-    }
-  }
-}
-
-static size_t hybrid_ws_layout(int64_t n, HybridWs *w, void *base) {
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    const size_t o = off;
-    off += align_up(bytes, 256);
-    return o;
-  };
-  const size_t o_cuts = take((size_t)n * 4), o_b = take(8 * (size_t)ceil_div(n, kFiltRays)), o_qc = take(8),
-               o_q = take((size_t)n * 4), o_s = take((size_t)n * 8), o_n = take((size_t)n * 8);
-  if (w && base) {
-    char *b = static_cast<char *>(base);
-    w->cuts = reinterpret_cast<int32_t *>(b + o_cuts);
-    w->bsums = reinterpret_cast<int64_t *>(b + o_b);
-    w->qcount = reinterpret_cast<unsigned long long *>(b + o_qc);
-    w->queue = reinterpret_cast<int32_t *>(b + o_q);
-    w->qS = reinterpret_cast<double *>(b + o_s);
-    w->qnext = reinterpret_cast<int64_t *>(b + o_n);
-  }
-  return off;
-}
-
-static unsigned long_blocks() {
-  static int n_sm = 0;
-  if (n_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sm <= 0) n_sm = 1;
-  }
-  return (unsigned)(n_sm * 8);  // 8 resident 256-thread blocks per SM: one persistent wave
-}
-
 static size_t filter_ws_layout(int64_t n, int32_t **cuts, int64_t **bsums, void *base) {
   const size_t a = align_up((size_t)n * 4, 256);
   if (base) {
@@ -433,8 +272,7 @@ extern "C" {
 
 size_t nacc_filter_workspace_bytes(int64_t n_rays) {
   if (n_rays < 0) return 0;
-  const size_t a = filter_ws_layout(n_rays, nullptr, nullptr, nullptr), b = hybrid_ws_layout(n_rays, nullptr, nullptr);
-  return a > b ? a : b;
+  return filter_ws_layout(n_rays, nullptr, nullptr, nullptr);
 }
 
 nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, const float *t0, const float *t1,
@@ -462,27 +300,13 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   int64_t *bsums;
   filter_ws_layout(n_rays, &cuts, &bsums, ws);
   const int64_t nb = ceil_div(n_rays, kFiltRays);
-  const bool sector = aligned(t0, 32) && aligned(t1, 32) && aligned(sigma, 32);
-  if (NACC_FILTER_HYBRID && sector) {
-    HybridWs hw;
-    hybrid_ws_layout(n_rays, &hw, ws);
-    cuts = hw.cuts;
-    bsums = hw.bsums;
-    NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)nb, stream));
-    NACC_CUDA(cudaMemsetAsync(hw.qcount, 0, 8, stream));
-    filter_cut_short_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, hw);
-    filter_cut_long_kernel<<<long_blocks(), 256, 0, stream>>>(packed_info, t0, t1, sigma, n_samples, neg_log_eps, hw);
-    count_launch(1);
-  } else {
-    NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)nb, stream));
-    if (NACC_FILTER_SECTOR && sector)
-      filter_cut_sector_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-          packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
-    else
-      filter_cut_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-          packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
-  }
+  NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)nb, stream));
+  if (NACC_FILTER_SECTOR && aligned(t0, 32) && aligned(t1, 32) && aligned(sigma, 32))
+    filter_cut_sector_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
+        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
+  else
+    filter_cut_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
+        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
   block_sums_scan_kernel<<<1, 1024, 0, stream>>>(bsums, nb, total);
   filter_copy_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, cuts, bsums, total, capacity,
                                                              packed_info_out, capacity > 0 ? t0_out : nullptr, t1_out,
