@@ -606,6 +606,9 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 // (t0, t1, ray_id) runs, 32 lattice points per pass.  A tile whose entries
 // overflow the buffer (or with a ray longer than 2^16 points) is counted and
 // written by direct traversal instead (traverse_ray).
+#ifndef NACC_MARCH_NOLOOKBACK
+#define NACC_MARCH_NOLOOKBACK 0  // timing experiment only (wrong output): no look-back
+#endif
 #ifndef NACC_MARCH_TRAYS
 #define NACC_MARCH_TRAYS 16  // build parameter: rays per tile
 #endif
@@ -669,6 +672,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
   __shared__ TileBuf tb[kFWarps][2];
   __shared__ uint32_t evq[kFWarps][kEvCap];
   __shared__ int seglist[kFWarps][32];  // direct traversal (overflowed tiles)
+  __shared__ float *obase[kFWarps][3];   // a tile's output bases (phase 2)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const bool fine = kSkip && kL1 && !kCone && mask3 != nullptr;  // single-level fine-mask test on shared floors
@@ -738,7 +742,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           const int idx = e0 + (lane >> 4);
           const uint32_t qe = idx < n_eval ? evq[warp][idx] : 0u;
           const int j = (qe >> 10) & ((1 << kJBits) - 1), q = (qe >> (10 + kJBits)) & kQMask, code = (qe >> 26) & 3,
-                    lv = (qe >> 28) & 7;
+                    lv = kL1 ? 0 : (qe >> 28) & 7;  // single level: a constant (no indexed constant loads)
           const int2 kr = T.kr[j];
           const int k = kr.x + q * kTSeg + (lane & 15);
           bool pred = false;
@@ -854,7 +858,11 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
     if (prev_tile >= 0) {
       // ---------------- phase 2 of the previous tile (buffer buf ^ 1)
       const TileBuf &T = tb[warp][buf ^ 1];
+#if NACC_MARCH_NOLOOKBACK  // timing experiment only: every tile writes at offset 0 (wrong output)
+      const long long excl = 0;
+#else
       const long long excl = lookback_resolve(lb->status, prev_tile, prev_agg);
+#endif
       if (prev_tile == n_tiles - 1 && lane == 0) {
         *total = excl + prev_agg;
         if (status_out) {
@@ -877,9 +885,17 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
       if (t0 != nullptr && excl + prev_agg <= capacity) {
         if (!prev_over) {
           const int n_ent = prev_ne;
-          float *__restrict__ o0 = t0 + excl;
-          float *__restrict__ o1 = t1 + excl;
-          int32_t *__restrict__ oid = ray_id + excl;
+          // the tile's output bases through shared memory, opaque to the optimiser, so every store
+          // is one 32-bit-offset IMAD.WIDE from a base register (the compiler otherwise re-associated
+          // excl + pos into a 64-bit add chain per store)
+          if (lane == 0) {
+            obase[warp][0] = t0 + excl;
+            obase[warp][1] = t1 + excl;
+            obase[warp][2] = reinterpret_cast<float *>(ray_id + excl);
+          }
+          __syncwarp();
+          float *const o0 = obase[warp][0], *const o1 = obase[warp][1];
+          int32_t *const oid = reinterpret_cast<int32_t *>(obase[warp][2]);
           int carry = 0;  // samples written so far in the tile
           const int b = lane & 15;
           for (int e = 0; e < n_ent; e += 2) {
