@@ -133,6 +133,9 @@ constexpr int seg_len(bool l1) { return l1 ? NACC_MARCH_SEG : NACC_MARCH_SEG_CAS
 static_assert(NACC_MARCH_SEG == 8 || NACC_MARCH_SEG == 16, "segment length");
 static_assert(NACC_MARCH_SEG_CASCADE == 8 || NACC_MARCH_SEG_CASCADE == 16, "segment length");
 constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
+// segment-test flag (cascades): every point of the segment lies in level (code >> 4) & 7 or the
+// next one, so P(k) needs at most two box tests instead of the level search
+constexpr int kTwoLevels = 0x100;
 constexpr float kSegEps = 1e-3f;
 
 // The same decision at the fine resolution (reading #22).  The points of a
@@ -202,23 +205,36 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
                                             const uint32_t *__restrict__ mask3, const float A[3], const float B[3]) {
   int la = 0;
   if (!kL1) {
-    la = level_of<false>(g, A[0], A[1], A[2]);
-    if (la < 0 || la != level_of<false>(g, B[0], B[1], B[2])) return 2;
-    if (la >= 1) {
-      bool meets = true;
+    // does the segment's bounding box (padded) reach box l?  Every point of the segment lies in
+    // that box (per-axis monotone fp32 positions), so "no" proves no point is in box l
+    auto meets = [&](int l) {
+      bool m = true;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         const float lo = fminf(A[a], B[a]), hi = fmaxf(A[a], B[a]);
-        const float pad = kSegEps * (g.hi[la - 1][a] - g.lo[la - 1][a]);
-        meets = meets && hi >= g.lo[la - 1][a] - pad && lo <= g.hi[la - 1][a] + pad;
+        const float pad = kSegEps * (g.hi[l][a] - g.lo[l][a]);
+        m = m && hi >= g.lo[l][a] - pad && lo <= g.hi[l][a] + pad;
       }
-      if (meets) return 2;
+      return m;
+    };
+    la = level_of<false>(g, A[0], A[1], A[2]);
+    const int lb = level_of<false>(g, B[0], B[1], B[2]);
+    if (la < 0 || lb < 0) return 2;
+    if (la != lb) {
+      // ends in adjacent levels and box lo - 1 out of reach: every point's level is lo or lo + 1
+      // (both ends lie in the convex box lo + 1), flagged for the two-box evaluation
+      const int lo = min(la, lb);
+      if (max(la, lb) == lo + 1 && (lo == 0 || !meets(lo - 1))) return 2 | (lo << 4) | kTwoLevels;
+      return 2;
     }
+    if (la >= 1 && meets(la - 1)) return 2;
     if (mask3 != nullptr) {  // every point lies in level la (convex box, finer box clear): its fine window
       int ia[3], ib[3];
       cell_floors(g, A, ia, la);
       cell_floors(g, B, ib, la);
-      return segment_test_floors(g, bits, mask3, ia, ib, la) | (la << 4);
+      const int code = segment_test_floors(g, bits, mask3, ia, ib, la);
+      // a non-interior window still knows the level: the two-box evaluation's first box holds
+      return code | (la << 4) | (code == 2 ? kTwoLevels : 0);
     }
   }
   int i0[3];
@@ -259,6 +275,27 @@ __device__ __forceinline__ bool occupied_interior(const GridConst &g, const uint
   const int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[l][1]), g.s[l][1]));
   const int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[l][2]), g.s[l][2]));
 #endif
+  const uint32_t q = (uint32_t)l * (uint32_t)(R * R * R) + (uint32_t)ix +
+                     (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
+  return (__ldg(bits + (q >> 5)) >> (q & 31u)) & 1u;
+}
+
+// P(k) for a point whose level is known to be lo or lo + 1 (kTwoLevels segments): the normative
+// l* is the first of the nested boxes holding x, so two box tests replace the level search
+__device__ __forceinline__ bool occupied_two(const GridConst &g, const uint32_t *__restrict__ bits, float m,
+                                             float ox, float oy, float oz, float dx, float dy, float dz, int lo) {
+  const float x = __fmaf_rn(m, dx, ox), y = __fmaf_rn(m, dy, oy), z = __fmaf_rn(m, dz, oz);
+  int l = -1;
+  if (in_level_box(g, lo, x, y, z)) l = lo;
+  else if (lo + 1 < g.levels && in_level_box(g, lo + 1, x, y, z)) l = lo + 1;
+  if (l < 0) return false;
+  const int R = g.res;
+  int ix = (int)floorf(__fmul_rn(__fsub_rn(x, g.lo[l][0]), g.s[l][0]));
+  int iy = (int)floorf(__fmul_rn(__fsub_rn(y, g.lo[l][1]), g.s[l][1]));
+  int iz = (int)floorf(__fmul_rn(__fsub_rn(z, g.lo[l][2]), g.s[l][2]));
+  ix = min(max(ix, 0), R - 1);
+  iy = min(max(iy, 0), R - 1);
+  iz = min(max(iz, 0), R - 1);
   const uint32_t q = (uint32_t)l * (uint32_t)(R * R * R) + (uint32_t)ix +
                      (uint32_t)R * ((uint32_t)iy + (uint32_t)R * (uint32_t)iz);
   return (__ldg(bits + (q >> 5)) >> (q & 31u)) & 1u;
@@ -510,7 +547,7 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
         const float B[3] = {__fmaf_rn(mb, s.dx, s.ox), __fmaf_rn(mb, s.dy, s.oy), __fmaf_rn(mb, s.dz, s.oz)};
         code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, bits, mask3, A, B)
                                           : segment_test<kL1>(g, bits, mask2, M, mask3, A, B);
-        lvl = code >> 4;  // cascades: the level every point of the segment lies in
+        lvl = (code >> 4) & 7;  // cascades: the level every point of the segment lies in
         code &= 15;
         flag = code != 0;
 #if NACC_MARCH_PREFETCH
@@ -743,6 +780,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           const uint32_t qe = idx < n_eval ? evq[warp][idx] : 0u;
           const int j = (qe >> 10) & ((1 << kJBits) - 1), q = (qe >> (10 + kJBits)) & kQMask, code = (qe >> 26) & 3,
                     lv = kL1 ? 0 : (qe >> 28) & 7;  // single level: a constant (no indexed constant loads)
+          const bool two = !kL1 && (qe >> 31);
           const int2 kr = T.kr[j];
           const int k = kr.x + q * kTSeg + (lane & 15);
           bool pred = false;
@@ -752,7 +790,8 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
             if (m < D.w)
               pred = code == 3 ? true
                                : (code == 1 ? occupied_interior(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z, lv)
-                                            : occupied<kL1>(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z));
+                                  : (two ? occupied_two(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z, lv)
+                                         : occupied<kL1>(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z)));
           }
           const unsigned bal = __ballot_sync(kFull, pred);
           if ((lane & 15) == 0 && idx < n_eval) {
@@ -782,6 +821,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           const float m = tile_mid<kCone, kW>(p, A.w, tab, kCone ? min(ks, K) : ks);
           const float X[3] = {__fmaf_rn(m, D.x, A.x), __fmaf_rn(m, D.y, A.y), __fmaf_rn(m, D.z, A.z)};
           int code = 0, lvl = 0;
+          bool two = false;
           if (!kSkip) {
             code = owner ? 2 : 0;
           } else if (fine) {
@@ -797,7 +837,8 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
             if (owner) {
               code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, bits, mask3, X, Y)
                                                 : segment_test<kL1>(g, bits, mask2, M, mask3, X, Y);
-              lvl = code >> 4;
+              two = (code & kTwoLevels) != 0;
+              lvl = (code >> 4) & 7;
               code &= 15;
             }
           }
@@ -810,7 +851,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
             if (slot < kECap) T.ent[slot] = ent_pack(j, q, 0xFFFFu);
             atomicAdd(&T.cnt[j], kTSeg);
           } else if (flag) {
-            evq[warp][npend + __popc((F & ~Dm) & lt)] = evq_pack(slot, j, q, code, lvl);
+            evq[warp][npend + __popc((F & ~Dm) & lt)] = evq_pack(slot, j, q, code, lvl) | (two ? 0x80000000u : 0u);
           }
           n_ent += __popc(F);
           npend += __popc(F & ~Dm);
