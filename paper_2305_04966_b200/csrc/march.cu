@@ -697,6 +697,91 @@ __device__ __forceinline__ float tile_mid(const MarchConst &p, float near_r, con
   return lattice_mid_u<kWide>(k, p.step, near_r);
 }
 
+// Phase 2 of a tile (the fused kernel's software pipeline, one tile behind phase 1): the
+// tile's output offset is `excl`; writes packed_info and streams its entries (or, for an
+// overflowed tile, traverses its rays again).
+template <bool kCone, bool kSkip, bool kL1>
+__device__ __forceinline__ void tile_write(const TileBuf &T, int n_ent_t, bool over, int c_lane, int64_t tile,
+                                           long long excl, long long agg, const GridConst &g, const MarchConst &p,
+                                           const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2,
+                                           int M, const uint32_t *__restrict__ mask3, const float *__restrict__ obox,
+                                           const float *__restrict__ rays_o, const float *__restrict__ rays_d,
+                                           const float *__restrict__ t_min, const float *__restrict__ t_max,
+                                           int64_t n_rays, const ConeHeader *__restrict__ hdr,
+                                           const float *__restrict__ tab, int64_t *__restrict__ packed_info,
+                                           int64_t capacity, float *__restrict__ t0, float *__restrict__ t1,
+                                           int32_t *__restrict__ ray_id, int *seglist, float **obase) {
+  constexpr int kR = tile_rays(kCone, kL1);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t r_base = tile * kR;
+  const int c = lane < kR ? c_lane : 0;
+  long long incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const long long run = excl + incl - c;
+  if (lane < kR && r_base + lane < n_rays)
+    reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(run, c);
+  if (t0 != nullptr && excl + agg <= capacity) {
+    if (!over) {
+      const int n_ent = n_ent_t;
+      // the tile's output bases through shared memory, opaque to the optimiser, so every store
+      // is one 32-bit-offset IMAD.WIDE from a base register (the compiler otherwise re-associated
+      // excl + pos into a 64-bit add chain per store)
+      if (lane == 0) {
+        obase[0] = t0 + excl;
+        obase[1] = t1 + excl;
+        obase[2] = reinterpret_cast<float *>(ray_id + excl);
+      }
+      __syncwarp();
+      float *const o0 = obase[0], *const o1 = obase[1];
+      int32_t *const oid = reinterpret_cast<int32_t *>(obase[2]);
+      int carry = 0;  // samples written so far in the tile
+      const int b = lane & 15;
+      for (int e = 0; e < n_ent; e += 2) {
+        const int idx = e + (lane >> 4);
+        const uint32_t ent = idx < n_ent ? T.ent[idx] : 0u;
+        const bool set = (ent >> b) & 1u;
+        const unsigned bal = __ballot_sync(kFull, set);  // both entries' masks, in output order
+        if (set) {
+          const int j = ent_j(ent);
+          const int pos = carry + __popc(bal & lt);
+          const int k = T.kr[j].x + ent_k16(ent) + b;  // kb_j + 16 q + b
+          float ta, tb2;
+          lattice_ends<kCone>(p, T.od[j][0].w, tab, k, ta, tb2);
+          o0[pos] = ta;
+          o1[pos] = tb2;
+          oid[pos] = (int32_t)(r_base + j);
+        }
+        carry += __popc(bal);
+      }
+    } else {  // overflowed tile: traverse again, writing directly
+      for (int jj = 0; jj < kR; ++jj) {
+        const int64_t r = r_base + jj;
+        if (r >= n_rays) break;
+        const long long rj = __shfl_sync(kFull, run, jj);
+        const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r);
+        int kb0, ke0;
+        traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist, kb0, ke0,
+                                        [&](unsigned bb, bool pred, int k, int32_t cnt) {
+                                          if (pred) {
+                                            const int64_t qq = rj + cnt + __popc(bb & lt);
+                                            float ta, tb2;
+                                            lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb2);
+                                            t0[qq] = ta;
+                                            t1[qq] = tb2;
+                                            ray_id[qq] = (int32_t)r;
+                                          }
+                                        });
+      }
+    }
+  }
+  __syncwarp();  // the buffer is refilled next
+}
+
 template <bool kCone, bool kSkip, bool kL1>
 __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
@@ -893,12 +978,11 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) agg += __shfl_xor_sync(kFull, agg, o);
       cur_agg = agg;
-      lookback_publish(lb->status, tile, cur_agg);
       cur_ne = n_ent;
+      lookback_publish(lb->status, tile, cur_agg);
     }
     if (prev_tile >= 0) {
       // ---------------- phase 2 of the previous tile (buffer buf ^ 1)
-      const TileBuf &T = tb[warp][buf ^ 1];
 #if NACC_MARCH_NOLOOKBACK  // timing experiment only: every tile writes at offset 0 (wrong output)
       const long long excl = 0;
 #else
@@ -912,72 +996,9 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           *status_out = stt;
         }
       }
-      const int64_t r_base = prev_tile * kR;
-      const int c = lane < kR ? prev_c : 0;
-      long long incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long v = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const long long run = excl + incl - c;
-      if (lane < kR && r_base + lane < n_rays)
-        reinterpret_cast<longlong2 *>(packed_info)[r_base + lane] = make_longlong2(run, c);
-      if (t0 != nullptr && excl + prev_agg <= capacity) {
-        if (!prev_over) {
-          const int n_ent = prev_ne;
-          // the tile's output bases through shared memory, opaque to the optimiser, so every store
-          // is one 32-bit-offset IMAD.WIDE from a base register (the compiler otherwise re-associated
-          // excl + pos into a 64-bit add chain per store)
-          if (lane == 0) {
-            obase[warp][0] = t0 + excl;
-            obase[warp][1] = t1 + excl;
-            obase[warp][2] = reinterpret_cast<float *>(ray_id + excl);
-          }
-          __syncwarp();
-          float *const o0 = obase[warp][0], *const o1 = obase[warp][1];
-          int32_t *const oid = reinterpret_cast<int32_t *>(obase[warp][2]);
-          int carry = 0;  // samples written so far in the tile
-          const int b = lane & 15;
-          for (int e = 0; e < n_ent; e += 2) {
-            const int idx = e + (lane >> 4);
-            const uint32_t ent = idx < n_ent ? T.ent[idx] : 0u;
-            const bool set = (ent >> b) & 1u;
-            const unsigned bal = __ballot_sync(kFull, set);  // both entries' masks, in output order
-            if (set) {
-              const int j = ent_j(ent);
-              const int pos = carry + __popc(bal & lt);
-              const int k = T.kr[j].x + ent_k16(ent) + b;  // kb_j + 16 q + b
-              float ta, tb2;
-              lattice_ends<kCone>(p, T.od[j][0].w, tab, k, ta, tb2);
-              o0[pos] = ta;
-              o1[pos] = tb2;
-              oid[pos] = (int32_t)(r_base + j);
-            }
-            carry += __popc(bal);
-          }
-        } else {  // overflowed tile: traverse again, writing directly
-          for (int jj = 0; jj < kR; ++jj) {
-            const int64_t r = r_base + jj;
-            if (r >= n_rays) break;
-            const long long rj = __shfl_sync(kFull, run, jj);
-            const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r);
-            int kb0, ke0;
-            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[warp], kb0, ke0,
-                                            [&](unsigned bb, bool pred, int k, int32_t cnt) {
-                                              if (pred) {
-                                                const int64_t qq = rj + cnt + __popc(bb & lt);
-                                                float ta, tb2;
-                                                lattice_ends<kCone>(p, s.near_r, tab, k, ta, tb2);
-                                                t0[qq] = ta;
-                                                t1[qq] = tb2;
-                                                ray_id[qq] = (int32_t)r;
-                                              }
-                                            });
-          }
-        }
-      }
-      __syncwarp();  // buffer buf ^ 1 is refilled next iteration
+      tile_write<kCone, kSkip, kL1>(tb[warp][buf ^ 1], prev_ne, prev_over, prev_c, prev_tile, excl, prev_agg, g, p,
+                                    bits, mask2, M, mask3, obox, rays_o, rays_d, t_min, t_max, n_rays, hdr, tab,
+                                    packed_info, capacity, t0, t1, ray_id, seglist[warp], obase[warp]);
     }
     if (!have) break;
     prev_tile = tile;
@@ -1217,9 +1238,9 @@ static nacc_status launch_march(int mode, const nacc_grid *grid, const uint32_t 
   } else if (mode == kModeFused) {
     const int64_t n_tiles = fused_tiles(n_rays, cone, l1);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8 + 8 * (size_t)n_tiles, stream));
-    NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits, mask2, M, mask3, obox, rays_o,
-                   rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb, packed_info, total, capacity,
-                   status_out, t0, t1, ray_id);
+    NACC_DISPATCH3(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits,
+                   mask2, M, mask3, obox, rays_o, rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb,
+                   packed_info, total, capacity, status_out, t0, t1, ray_id);
   } else {
     NACC_DISPATCH3(march_fill_kernel, (unsigned)grid_for(n_rays * 32, 256), 256, stream, g, p, bits, mask2, M, mask3,
                    obox, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, packed_info, t0, t1, ray_id);

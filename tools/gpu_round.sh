@@ -5,7 +5,7 @@ mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -4 > gpurun_out/gpu_tests.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 > gpurun_out/smoke.txt
 timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 200 -c 120 --csv --log-file gpurun_out/launches.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 110 --csv --log-file gpurun_out/launches.csv \
   python bench.py --workload cfg2 --steps 12 --warmup 3 --profile --no-cpu-baseline > /dev/null 2>&1
 for k in march_fused render_fwd_warp render_bwd_warp filter_cut filter_copy; do
   bash tools/gpu_ncu.sh $k $k 3

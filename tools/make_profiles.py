@@ -18,7 +18,7 @@ if os.path.exists(os.path.join(go, "launches.csv")):
                          capture_output=True, text=True).stdout
     open(os.path.join(out, "launches.txt"), "w").write(
         "ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches of\n"
-        "`python bench.py --workload cfg2 --steps 12 --warmup 3 --profile`): compare SHARES, not absolutes.\n\n" + txt)
+        "`python bench.py --workload cfg2 --steps 12 --warmup 3 --profile`, launches 300-410: past the 16 warm-up grid updates): compare SHARES, not absolutes.\n\n" + txt)
     import shutil
     shutil.copy(os.path.join(go, "launches.csv"), os.path.join(out, "launches.csv"))
 traffic = {}
