@@ -29,6 +29,9 @@ constexpr int kCutThreads = 64;
 #define NACC_FILTER_BATCH 4
 #endif
 constexpr int kCutBatch = NACC_FILTER_BATCH;
+#ifndef NACC_FILTER_MINB
+#define NACC_FILTER_MINB 1  // build parameter: min resident 64-thread blocks per SM of the sector walk
+#endif
 #ifndef NACC_FILTER_SECTOR
 #define NACC_FILTER_SECTOR 1  // build parameter: sector-aligned walk when the arrays are 32-byte aligned
 #endif
@@ -112,7 +115,7 @@ __device__ __forceinline__ void load_sector(Sector &v, const float *__restrict__
   }
 }
 
-__global__ void __launch_bounds__(kCutThreads) filter_cut_sector_kernel(
+__global__ void __launch_bounds__(kCutThreads, NACC_FILTER_MINB) filter_cut_sector_kernel(
     const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
     const float *__restrict__ t1, const float *__restrict__ sigma, int64_t n_samples, double L,
     int32_t *__restrict__ cut_out, int64_t *__restrict__ block_sums) {
