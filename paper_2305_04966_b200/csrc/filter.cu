@@ -31,6 +31,7 @@ constexpr int kCutThreads = 64;
 constexpr int kCutBatch = NACC_FILTER_BATCH;
 #ifndef NACC_FILTER_MINB
 #define NACC_FILTER_MINB 1  // build parameter: min resident 64-thread blocks per SM of the sector walk
+                            // (A/B 1 / 16 / 24 / 32: 67.2 / 65.9 / 115 / 144 us, within noise up to 16)
 #endif
 #ifndef NACC_FILTER_SECTOR
 #define NACC_FILTER_SECTOR 1  // build parameter: sector-aligned walk when the arrays are 32-byte aligned
