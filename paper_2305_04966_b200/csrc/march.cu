@@ -41,6 +41,7 @@ namespace nacc {
 
 struct GridConst {
   int levels, res;
+  uint32_t r3w, mw;  // bit words per level (R^3 / 32); words per window mask (levels * r3w, 64-word aligned)
   float lo[8][3], hi[8][3], s[8][3];
   float olo[3], ohi[3];  // outermost box padded by 1e-4*width + 1e-6
 };
@@ -55,6 +56,8 @@ static GridConst make_grid_const(const nacc_grid &g) {
   GridConst c{};
   c.levels = g.levels;
   c.res = g.res;
+  c.r3w = (uint32_t)((int64_t)g.res * g.res * g.res / 32);
+  c.mw = (uint32_t)((((int64_t)g.levels * c.r3w + 63) / 64) * 64);
   for (int a = 0; a < 3; ++a) {
     const double lo0 = (double)g.roi[a], hi0 = (double)g.roi[3 + a];
     const double ctr = (lo0 + hi0) / 2.0, half = (hi0 - lo0) / 2.0;
@@ -159,7 +162,6 @@ __device__ __forceinline__ int segment_test_floors(const GridConst &g, const uin
                                                    const uint32_t *__restrict__ mask3, const int ia[3],
                                                    const int ib[3], int l = 0) {
   const int R = g.res;
-  const int64_t R3w = (int64_t)R * R * R / 32;  // words per level (R % 4 == 0)
   int c[3], span = 0;
   bool interior = true;
 #pragma unroll
@@ -175,10 +177,9 @@ __device__ __forceinline__ int segment_test_floors(const GridConst &g, const uin
   // the window of the segment's cell span, w = span + 1 cells per axis: OR_w at
   // mask3 + 2 (w - 2) masks, AND_w right after (gridaux.cu); a segment inside one cell (w = 1)
   // reads the cell's own fine bit for both
-  const int64_t mw = ((g.levels * R3w + 63) / 64) * 64;
-  const uint32_t *orm = span == 0 ? bits : mask3 + 2 * (span - 1) * mw;
-  const uint32_t *andm = span == 0 ? bits : orm + mw;
-  const int64_t wi = l * R3w + (q >> 5);
+  const uint32_t *orm = span == 0 ? bits : mask3 + 2u * (uint32_t)(span - 1) * g.mw;
+  const uint32_t *andm = span == 0 ? bits : orm + g.mw;
+  const uint32_t wi = (uint32_t)l * g.r3w + (q >> 5);
   if (!((__ldg(orm + wi) >> (q & 31u)) & 1u)) return 0;
   if (!interior) return 2;
   // solid window: every cell the points can fall in is occupied, so every point is a member

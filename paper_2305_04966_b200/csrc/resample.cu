@@ -3,6 +3,8 @@
 // the CDF directly using 1 - T(t)"), piecewise linear in s (P:257,
 // readings #16-#19).  One warp per ray; the ray's normalised CDF lives in
 // shared memory, each lane inverts 1/32 of the output edges by binary search.
+#include <type_traits>
+
 #include "common.cuh"
 #include "debug.cuh"
 
@@ -46,8 +48,60 @@ __device__ __forceinline__ float one_minus_exp_neg(float S) {
 }
 
 constexpr int kResampleWarps = 4;
+#ifndef NACC_RESAMPLE_ITEMS
+#define NACC_RESAMPLE_ITEMS 1  // build parameter: sigma CDF with consecutive edges per lane (0: 32-edge windows)
+#endif
 
-template <bool kRanged>
+// The sigma CDF with kIPL consecutive intervals per lane (n_in <= 32 kIPL): each lane maps its
+// edges through Φ, forms s_j = σ_j (t_{j+1} - t_j) and their running sum in fp64, one fp64 warp
+// scan of the lane totals gives every S_{j+1}; F[j+1] = 1 - e^{-S_{j+1}} is normalised by F_m in
+// registers before it is stored (the same arithmetic as the windowed path, one scan per ray
+// instead of one per 32 edges).  Returns the total S_m (every lane).
+template <int kIPL, typename PhiE>
+__device__ __forceinline__ double cdf_items(int n_in, const float *__restrict__ er, const float *__restrict__ sr,
+                                            float *e, float *F, PhiE phi_e, bool &uniform) {
+  const int lane = threadIdx.x & 31;
+  const int j0 = lane * kIPL;
+  float ev[kIPL + 1], sv[kIPL];
+#pragma unroll
+  for (int k = 0; k < kIPL; ++k) {
+    const int j = j0 + k;
+    ev[k] = j <= n_in ? __ldg(er + j) : 0.f;
+    sv[k] = j < n_in ? __ldg(sr + j) : 0.f;
+  }
+  ev[kIPL] = j0 + kIPL <= n_in ? __ldg(er + j0 + kIPL) : 0.f;
+#pragma unroll
+  for (int k = 0; k < kIPL; ++k)
+    if (j0 + k <= n_in) e[j0 + k] = ev[k];
+  if (j0 + kIPL == n_in) e[n_in] = ev[kIPL];
+  double tk = phi_e((double)ev[0]);
+  double loc[kIPL];
+  double run = 0.0;
+#pragma unroll
+  for (int k = 0; k < kIPL; ++k) {
+    const double tk1 = phi_e((double)ev[k + 1]);
+    run += j0 + k < n_in ? (double)sv[k] * (tk1 - tk) : 0.0;
+    loc[k] = run;
+    tk = tk1;
+  }
+  const double incl = warp_incl_scan(run);
+  const double base = incl - run, total = __shfl_sync(kFull, incl, 31);
+  uniform = !(-expm1(-total) > 1e-12);
+  const float Fm = one_minus_exp_neg((float)total), rFm = __frcp_rn(Fm);
+#pragma unroll
+  for (int k = 0; k < kIPL; ++k) {
+    const int j = j0 + k;
+    if (j < n_in) {
+      const float f = one_minus_exp_neg((float)(base + loc[k]));
+      F[j + 1] = uniform ? f : (j + 1 == n_in ? 1.0f : fminf(__fmul_rn(f, rFm), 1.0f));
+    }
+  }
+  if (lane == 0) F[0] = 0.f;
+  __syncwarp();
+  return total;
+}
+
+template <bool kRanged, int kIPL>
 __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     int64_t n_rays, int n_in, const float *__restrict__ s_edges, const float *__restrict__ sigma,
     const float *__restrict__ cdf, int map, double tn, double tf, const float *__restrict__ tn_r,
@@ -73,52 +127,64 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     }
   }
   const double inv_tn = 1.0 / tn, inv_tf = isinf(tf) ? 0.0 : 1.0 / tf;
-  for (int j = lane; j <= n_in; j += 32) e[j] = __ldg(er + j);
-  __syncwarp();
-  bool uniform = false;
-  if (sigma) {
+  bool uniform = false, normal = false;
+  if constexpr (kIPL > 0) {  // sigma input, n_in <= 32 kIPL
     const float *sr = sigma + r * (int64_t)n_in;
-    double carry = 0.0;
-    // t of every edge once: lane l holds t(e[base + l]); t(e[j + 1]) comes from the next lane,
-    // and for lane 31 from lane 0 of the next window (computed one window ahead)
-    // every edge's 1/t in fp32's normal range (the common case): Φ without the range check
-    const bool normal = map == NACC_MAP_LINDISP && fmin(inv_tn, inv_tf) >= 1e-30 && fmax(inv_tn, inv_tf) <= 1e30 &&
-                        e[0] >= 0.f && e[n_in] <= 1.f;
-    auto phi_e = [&](double sv) {
-      return normal ? phi_normal(map, sv, tn, inv_tn, inv_tf, tf) : phi(map, sv, tn, inv_tn, inv_tf, tf);
-    };
-    double ta = lane <= n_in ? phi_e((double)e[lane]) : 0.0;
-    for (int base = 0; base < n_in; base += 32) {
-      const int j = base + lane;
-      const double tnext = j + 32 <= n_in ? phi_e((double)e[j + 32]) : 0.0;
-      const double dn = __shfl_down_sync(kFull, ta, 1), wn = __shfl_sync(kFull, tnext, 0);
-      const double tb = lane < 31 ? dn : wn;
-      double s = 0.0;
-      if (j < n_in) s = (double)__ldg(sr + j) * (tb - ta);
-      ta = tnext;
-      const double incl = warp_incl_scan(s);
-      if (j < n_in) F[j + 1] = one_minus_exp_neg((float)(carry + incl));
-      carry += __shfl_sync(kFull, incl, 31);
-    }
-    if (lane == 0) F[0] = 0.f;
-    uniform = !(-expm1(-carry) > 1e-12);
-    __syncwarp();
-    if (!uniform) {  // F / F_m by one reciprocal (within an ulp of the quotient); F_m / F_m = 1 exactly
-      const float Fm = F[n_in], rFm = __frcp_rn(Fm);
-      for (int j = lane; j < n_in; j += 32) F[j] = fminf(__fmul_rn(F[j], rFm), 1.0f);  // monotone, <= 1
-      __syncwarp();
-      if (lane == 0) F[n_in] = 1.0f;
-    }
+    normal = map == NACC_MAP_LINDISP && fmin(inv_tn, inv_tf) >= 1e-30 && fmax(inv_tn, inv_tf) <= 1e30 &&
+             __ldg(er) >= 0.f && __ldg(er + n_in) <= 1.f;
+    if (normal)
+      cdf_items<kIPL>(n_in, er, sr, e, F, [&](double sv) { return phi_normal(map, sv, tn, inv_tn, inv_tf, tf); },
+                      uniform);
+    else
+      cdf_items<kIPL>(n_in, er, sr, e, F, [&](double sv) { return phi(map, sv, tn, inv_tn, inv_tf, tf); }, uniform);
   } else {
-    const float *cr = cdf + r * (int64_t)(n_in + 1);
-    const float c0 = __ldg(cr), cm = __ldg(cr + n_in);
-    uniform = !((double)cm - (double)c0 > 1e-12);
-    if (!uniform) {
-      const float den = __fsub_rn(cm, c0);
-      for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(__fsub_rn(__ldg(cr + j), c0), den);
+    for (int j = lane; j <= n_in; j += 32) e[j] = __ldg(er + j);
+    __syncwarp();
+    if (sigma) {
+      const float *sr = sigma + r * (int64_t)n_in;
+      double carry = 0.0;
+      // t of every edge once: lane l holds t(e[base + l]); t(e[j + 1]) comes from the next lane,
+      // and for lane 31 from lane 0 of the next window (computed one window ahead)
+      // every edge's 1/t in fp32's normal range (the common case): Φ without the range check
+      normal = map == NACC_MAP_LINDISP && fmin(inv_tn, inv_tf) >= 1e-30 && fmax(inv_tn, inv_tf) <= 1e30 &&
+               e[0] >= 0.f && e[n_in] <= 1.f;
+      auto phi_e = [&](double sv) {
+        return normal ? phi_normal(map, sv, tn, inv_tn, inv_tf, tf) : phi(map, sv, tn, inv_tn, inv_tf, tf);
+      };
+      double ta = lane <= n_in ? phi_e((double)e[lane]) : 0.0;
+      for (int base = 0; base < n_in; base += 32) {
+        const int j = base + lane;
+        const double tnext = j + 32 <= n_in ? phi_e((double)e[j + 32]) : 0.0;
+        const double dn = __shfl_down_sync(kFull, ta, 1), wn = __shfl_sync(kFull, tnext, 0);
+        const double tb = lane < 31 ? dn : wn;
+        double s = 0.0;
+        if (j < n_in) s = (double)__ldg(sr + j) * (tb - ta);
+        ta = tnext;
+        const double incl = warp_incl_scan(s);
+        if (j < n_in) F[j + 1] = one_minus_exp_neg((float)(carry + incl));
+        carry += __shfl_sync(kFull, incl, 31);
+      }
+      if (lane == 0) F[0] = 0.f;
+      uniform = !(-expm1(-carry) > 1e-12);
+      __syncwarp();
+      if (!uniform) {  // F / F_m by one reciprocal (within an ulp of the quotient); F_m / F_m = 1 exactly
+        const float Fm = F[n_in], rFm = __frcp_rn(Fm);
+        for (int j = lane; j < n_in; j += 32) F[j] = fminf(__fmul_rn(F[j], rFm), 1.0f);  // monotone, <= 1
+        __syncwarp();
+        if (lane == 0) F[n_in] = 1.0f;
+      }
+    } else {
+      const float *cr = cdf + r * (int64_t)(n_in + 1);
+      const float c0 = __ldg(cr), cm = __ldg(cr + n_in);
+      uniform = !((double)cm - (double)c0 > 1e-12);
+      if (!uniform) {
+        const float den = __fsub_rn(cm, c0);
+        for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(__fsub_rn(__ldg(cr + j), c0), den);
+      }
     }
   }
   if (uniform) {
+    __syncwarp();
     const float e0 = e[0], den = __fsub_rn(e[n_in], e0);
     for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(__fsub_rn(e[j], e0), den);
   }
@@ -159,7 +225,8 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
       s = ej + (u - Fj) * rcp_fast(Fj1 - Fj) * (ej1 - ej);
     }
     so[i] = (float)s;
-    if (to) to[i] = (float)phi(map, s, tn, inv_tn, inv_tf, tf);
+    // s lies between two edges: with every edge's 1/t normal, so is Φ(s)'s
+    if (to) to[i] = (float)(normal ? phi_normal(map, s, tn, inv_tn, inv_tf, tf) : phi(map, s, tn, inv_tn, inv_tf, tf));
   }
 }
 
@@ -174,19 +241,39 @@ static nacc_status launch_importance(int64_t n_rays, int32_t n_in, const float *
     return NACC_ERR_UNSUPPORTED;
   }
   const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
-  if (tn_r) {
-    if (smem > 48 * 1024)
-      NACC_CUDA(cudaFuncSetAttribute(importance_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    importance_kernel<true><<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
+  const int ipl = NACC_RESAMPLE_ITEMS && sigma && n_in <= 256 ? (n_in + 31) / 32 : 0;
+  nacc_status st = NACC_OK;
+  auto go = [&](auto ranged, auto items) {
+    constexpr bool kR = decltype(ranged)::value;
+    constexpr int kI = decltype(items)::value;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(importance_kernel<kR, kI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess) {
+      set_error("nacc_importance_sample: cudaFuncSetAttribute failed");
+      st = NACC_ERR_CUDA;
+      return;
+    }
+    importance_kernel<kR, kI><<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
         n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, tn_r, tf_r, n_out, stratified, k0, k1, s_out,
         t_out);
-  } else {
-    if (smem > 48 * 1024)
-      NACC_CUDA(cudaFuncSetAttribute(importance_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    importance_kernel<false><<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
-        n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, nullptr, nullptr, n_out, stratified, k0, k1,
-        s_out, t_out);
-  }
+  };
+  auto by_items = [&](auto ranged) {
+    using I = std::integral_constant<int, 0>;
+    switch (ipl) {
+      case 1: go(ranged, std::integral_constant<int, 1>{}); break;
+      case 2: go(ranged, std::integral_constant<int, 2>{}); break;
+      case 3: go(ranged, std::integral_constant<int, 3>{}); break;
+      case 4: go(ranged, std::integral_constant<int, 4>{}); break;
+      case 5: go(ranged, std::integral_constant<int, 5>{}); break;
+      case 6: go(ranged, std::integral_constant<int, 6>{}); break;
+      case 7: go(ranged, std::integral_constant<int, 7>{}); break;
+      case 8: go(ranged, std::integral_constant<int, 8>{}); break;
+      default: go(ranged, I{});
+    }
+  };
+  if (tn_r) by_items(std::true_type{});
+  else by_items(std::false_type{});
+  if (st != NACC_OK) return st;
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;
