@@ -192,40 +192,56 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
   const double inv_n = 1.0 / (double)n_out;
   float *so = s_out + r * (int64_t)(n_out + 1);
   float *to = t_out ? t_out + r * (int64_t)(n_out + 1) : nullptr;
-  for (int i = lane; i <= n_out; i += 32) {
+  int n_search = n_out + 1;
+  if (!stratified) {
+    // u = 1 at i = n_out: the smallest j in [0, n_in-1] with F[j+1] >= 1.  {j : F[j+1] >= 1} is a
+    // suffix of the bins (F monotone, F[n_in] = 1), so scan 32-bin windows from the end and stop
+    // at the first window holding a bin below 1
+    int jl = 0;
+    for (int b0 = n_in - 32;; b0 -= 32) {
+      const int j = b0 + lane;
+      const unsigned m = __ballot_sync(kFull, j < 0 || F[j + 1] >= 1.0f);
+      if (m != kFull) {
+        jl = b0 + 32 - __clz(~m);  // one past the highest bin below 1
+        break;
+      }
+      if (b0 <= 0) break;  // every bin reaches 1: j = 0
+    }
+    if (lane == 0) {
+      const double s = (double)e[jl + 1];
+      so[n_out] = (float)s;
+      if (to) to[n_out] = (float)phi(map, s, tn, inv_tn, inv_tf, tf);
+    }
+    n_search = n_out;
+  }
+  for (int i = lane; i < n_search; i += 32) {
     double u;
     if (stratified) {
       const u32x4 rnd = philox4x32_10(u32x4{(uint32_t)(uint64_t)r, (uint32_t)((uint64_t)r >> 32), (uint32_t)i, 1u},
                                       key0, key1);
       u = ((double)i + u24(rnd.x)) / (double)(n_out + 1);
     } else {
-      u = i == n_out ? 1.0 : (double)i * inv_n;  // i / n within an ulp; exactly 1 at the end
+      u = (double)i * inv_n;  // i / n within an ulp, < 1
     }
-    double s;
-    if (u >= 1.0) {
-      // smallest j in [0, n_in-1] with F[j+1] >= 1
-      int lo = 0, hi = n_in - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (F[mid + 1] >= 1.0f) hi = mid;
-        else lo = mid + 1;
-      }
-      s = (double)e[lo + 1];
-    } else {
-      // largest j in [0, n_in-1] with F[j] <= u, i.e. F[j] <= uf, the largest float <= u (exact)
-      const float uf = __double2float_rd(u);
-      int lo = 0, hi = n_in - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (F[mid] <= uf) lo = mid;
-        else hi = mid - 1;
-      }
-      const double Fj = (double)F[lo], Fj1 = (double)F[lo + 1];
-      const double ej = (double)e[lo], ej1 = (double)e[lo + 1];
-      s = ej + (u - Fj) * rcp_fast(Fj1 - Fj) * (ej1 - ej);
+    // largest j in [0, n_in-1] with F[j] <= u, i.e. F[j] <= uf, the largest float <= u (exact)
+    const float uf = __double2float_rd(u);
+    int lo = 0, hi = n_in - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (F[mid] <= uf) lo = mid;
+      else hi = mid - 1;
     }
-    so[i] = (float)s;
+    // linear within the bin in fp32 (reading #29): F[lo] <= u < F[lo + 1], so the fraction lies in
+    // [0, 1); each step rounds once (back error ~1e-7 plus the output's own rounding), and the
+    // clamp to the bin keeps the edges non-decreasing across bins
+    const float Fj = F[lo], Fj1 = F[lo + 1], ej = e[lo], ej1 = e[lo + 1];
+    const float d = __fsub_rn(Fj1, Fj);
+    const float num = (float)(u - (double)Fj);
+    const float frac = d >= 1e-30f ? __fmul_rn(num, __frcp_rn(d)) : (float)((double)num / (double)d);
+    const float sf = fminf(__fmaf_rn(fminf(frac, 1.0f), __fsub_rn(ej1, ej), ej), ej1);
+    so[i] = sf;
     // s lies between two edges: with every edge's 1/t normal, so is Φ(s)'s
+    const double s = (double)sf;
     if (to) to[i] = (float)(normal ? phi_normal(map, s, tn, inv_tn, inv_tf, tf) : phi(map, s, tn, inv_tn, inv_tf, tf));
   }
 }
