@@ -48,6 +48,9 @@ __device__ __forceinline__ float one_minus_exp_neg(float S) {
 }
 
 constexpr int kResampleWarps = 4;
+#ifndef NACC_RESAMPLE_F32DT
+#define NACC_RESAMPLE_F32DT 1  // build parameter: interval lengths by the fp32 product identities (cdf_items)
+#endif
 #ifndef NACC_RESAMPLE_ITEMS
 #define NACC_RESAMPLE_ITEMS 1  // build parameter: sigma CDF with consecutive edges per lane (0: 32-edge windows)
 #endif
@@ -57,9 +60,22 @@ constexpr int kResampleWarps = 4;
 // scan of the lane totals gives every S_{j+1}; F[j+1] = 1 - e^{-S_{j+1}} is normalised by F_m in
 // registers before it is stored (the same arithmetic as the windowed path, one scan per ray
 // instead of one per 32 edges).  Returns the total S_m (every lane).
-template <int kIPL, typename PhiE>
+// 1/t = (1 - s)/t_n + s/t_f in fp32 from itn = 1/t_n, itf = 1/t_f: both terms >= 0, so no
+// cancellation (the form 1/t_n + s (1/t_f - 1/t_n) loses the small 1/t near s = 1)
+__device__ __forceinline__ float lin_x(float s, float itn, float itf) {
+  return __fmaf_rn(s, itf, __fmul_rn(__fsub_rn(1.0f, s), itn));
+}
+
+// kMode 0: t_j = Φ(s_j) in fp64 and s_j = σ_j (t_{j+1} - t_j) in fp64 (any map and range).
+// kMode 1 (lindisp, every t in [1e-15, 1e15]) and 2 (identity): t_{j+1} - t_j from the exact
+// identities 1/x_j - 1/x_{j+1} = (x_{j+1} - x_j) / (x_j x_{j+1}) with x = 1/t linear in s (lin_x), i.e.
+// Δt_j = Δs_j (1/t_n - 1/t_f) t_j t_{j+1}, and Δt_j = Δs_j (t_f - t_n): no cancellation, so fp32
+// gives Δt_j to a few ulps (the fp64 path needs fp64 only because it subtracts two t's); the lane's
+// running sums are fp32 (at most 8 terms), the cross-lane scan fp64 (reading #29).
+template <int kIPL, int kMode, typename PhiE>
 __device__ __forceinline__ double cdf_items(int n_in, const float *__restrict__ er, const float *__restrict__ sr,
-                                            float *e, float *F, PhiE phi_e, bool &uniform) {
+                                            float *e, float *F, PhiE phi_e, float xa, float xb, float dc,
+                                            bool &uniform) {
   const int lane = threadIdx.x & 31;
   const int j0 = lane * kIPL;
   float ev[kIPL + 1], sv[kIPL];
@@ -74,27 +90,71 @@ __device__ __forceinline__ double cdf_items(int n_in, const float *__restrict__ 
   for (int k = 0; k < kIPL; ++k)
     if (j0 + k <= n_in) e[j0 + k] = ev[k];
   if (j0 + kIPL == n_in) e[n_in] = ev[kIPL];
-  double tk = phi_e((double)ev[0]);
-  double loc[kIPL];
-  double run = 0.0;
+  float f[kIPL];  // 1 - e^{-S_{j+1}} (unnormalised)
+  double run = 0.0, incl;
+  if constexpr (kMode == 0) {
+    double tk = phi_e((double)ev[0]);
+    double loc[kIPL];
 #pragma unroll
-  for (int k = 0; k < kIPL; ++k) {
-    const double tk1 = phi_e((double)ev[k + 1]);
-    run += j0 + k < n_in ? (double)sv[k] * (tk1 - tk) : 0.0;
-    loc[k] = run;
-    tk = tk1;
+    for (int k = 0; k < kIPL; ++k) {
+      const double tk1 = phi_e((double)ev[k + 1]);
+      run += j0 + k < n_in ? (double)sv[k] * (tk1 - tk) : 0.0;
+      loc[k] = run;
+      tk = tk1;
+    }
+    incl = warp_incl_scan(run);
+    const double base = incl - run;
+#pragma unroll
+    for (int k = 0; k < kIPL; ++k) f[k] = one_minus_exp_neg((float)(base + loc[k]));
+  } else {
+    auto rcp = [](float x) {  // 1/x to 1 ulp (x normal)
+      float y;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+      return y;
+    };
+    float tk = kMode == 1 ? rcp(lin_x(ev[0], xa, xb)) : 0.f;
+    float loc[kIPL], runf = 0.f;
+#pragma unroll
+    for (int k = 0; k < kIPL; ++k) {
+      const float ds = __fsub_rn(ev[k + 1], ev[k]);
+      float dt;
+      if (kMode == 1) {
+        const float tk1 = rcp(lin_x(ev[k + 1], xa, xb));
+        dt = __fmul_rn(__fmul_rn(__fmul_rn(ds, dc), tk), tk1);
+        tk = tk1;
+      } else {
+        dt = __fmul_rn(ds, dc);
+      }
+      runf = __fadd_rn(runf, j0 + k < n_in ? __fmul_rn(sv[k], dt) : 0.f);
+      loc[k] = runf;
+    }
+    run = (double)runf;
+    incl = warp_incl_scan(run);
+    const float basef = (float)(incl - run);
+#pragma unroll
+    for (int k = 0; k < kIPL; ++k) f[k] = one_minus_exp_neg(__fadd_rn(basef, loc[k]));
   }
-  const double incl = warp_incl_scan(run);
-  const double base = incl - run, total = __shfl_sync(kFull, incl, 31);
+  // F non-decreasing edge by edge (the scan's tree-order sums and the fp32 1 - e^{-S} can each
+  // step back by an ulp): a running max within the lane, then across the lanes
+#pragma unroll
+  for (int k = 1; k < kIPL; ++k) f[k] = fmaxf(f[k], f[k - 1]);
+  float mx = f[kIPL - 1];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(kFull, mx, o);
+    if (lane >= o) mx = fmaxf(mx, y);
+  }
+  const float before = __shfl_up_sync(kFull, mx, 1);
+  if (lane > 0)
+#pragma unroll
+    for (int k = 0; k < kIPL; ++k) f[k] = fmaxf(f[k], before);
+  const double total = __shfl_sync(kFull, incl, 31);
   uniform = !(-expm1(-total) > 1e-12);
   const float Fm = one_minus_exp_neg((float)total), rFm = __frcp_rn(Fm);
 #pragma unroll
   for (int k = 0; k < kIPL; ++k) {
     const int j = j0 + k;
-    if (j < n_in) {
-      const float f = one_minus_exp_neg((float)(base + loc[k]));
-      F[j + 1] = uniform ? f : (j + 1 == n_in ? 1.0f : fminf(__fmul_rn(f, rFm), 1.0f));
-    }
+    if (j < n_in) F[j + 1] = uniform ? f[k] : (j + 1 == n_in ? 1.0f : fminf(__fmul_rn(f[k], rFm), 1.0f));
   }
   if (lane == 0) F[0] = 0.f;
   __syncwarp();
@@ -128,15 +188,28 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
   }
   const double inv_tn = 1.0 / tn, inv_tf = isinf(tf) ? 0.0 : 1.0 / tf;
   bool uniform = false, normal = false;
+  int tmode = 0;  // t_out: 0 Φ in fp64; 1 lindisp 1/lin_x(s, 1/t_n, 1/t_f) in fp32; 2 identity t_n + s w in fp32
+  float xa = 0.f, xb = 0.f;
   if constexpr (kIPL > 0) {  // sigma input, n_in <= 32 kIPL
     const float *sr = sigma + r * (int64_t)n_in;
-    normal = map == NACC_MAP_LINDISP && fmin(inv_tn, inv_tf) >= 1e-30 && fmax(inv_tn, inv_tf) <= 1e30 &&
-             __ldg(er) >= 0.f && __ldg(er + n_in) <= 1.f;
-    if (normal)
-      cdf_items<kIPL>(n_in, er, sr, e, F, [&](double sv) { return phi_normal(map, sv, tn, inv_tn, inv_tf, tf); },
-                      uniform);
+    const bool in01 = __ldg(er) >= 0.f && __ldg(er + n_in) <= 1.f;
+    normal = map == NACC_MAP_LINDISP && fmin(inv_tn, inv_tf) >= 1e-30 && fmax(inv_tn, inv_tf) <= 1e30 && in01;
+    auto phi_n = [&](double sv) { return phi_normal(map, sv, tn, inv_tn, inv_tf, tf); };
+    if (NACC_RESAMPLE_F32DT && normal && fmin(inv_tn, inv_tf) >= 1e-15 && fmax(inv_tn, inv_tf) <= 1e15) {
+      tmode = 1;
+      xa = (float)inv_tn;
+      xb = (float)inv_tf;
+      cdf_items<kIPL, 1>(n_in, er, sr, e, F, phi_n, xa, xb, (float)(inv_tn - inv_tf), uniform);
+    } else if (NACC_RESAMPLE_F32DT && map == NACC_MAP_IDENTITY && in01 && tf - tn <= 1e15) {
+      tmode = 2;
+      xa = (float)tn;
+      xb = (float)(tf - tn);
+      cdf_items<kIPL, 2>(n_in, er, sr, e, F, phi_n, 0.f, 0.f, xb, uniform);
+    } else if (normal)
+      cdf_items<kIPL, 0>(n_in, er, sr, e, F, phi_n, 0.f, 0.f, 0.f, uniform);
     else
-      cdf_items<kIPL>(n_in, er, sr, e, F, [&](double sv) { return phi(map, sv, tn, inv_tn, inv_tf, tf); }, uniform);
+      cdf_items<kIPL, 0>(n_in, er, sr, e, F, [&](double sv) { return phi(map, sv, tn, inv_tn, inv_tf, tf); }, 0.f,
+                         0.f, 0.f, uniform);
   } else {
     for (int j = lane; j <= n_in; j += 32) e[j] = __ldg(er + j);
     __syncwarp();
@@ -193,6 +266,7 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
   float *so = s_out + r * (int64_t)(n_out + 1);
   float *to = t_out ? t_out + r * (int64_t)(n_out + 1) : nullptr;
   int n_search = n_out + 1;
+  const int top = n_in > 1 ? 1 << (31 - __clz(n_in - 1)) : 0;  // binary-lifting first step
   if (!stratified) {
     // u = 1 at i = n_out: the smallest j in [0, n_in-1] with F[j+1] >= 1.  {j : F[j+1] >= 1} is a
     // suffix of the bins (F monotone, F[n_in] = 1), so scan 32-bin windows from the end and stop
@@ -224,13 +298,11 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
       u = (double)i * inv_n;  // i / n within an ulp, < 1
     }
     // largest j in [0, n_in-1] with F[j] <= u, i.e. F[j] <= uf, the largest float <= u (exact)
+    // (binary lifting from the largest power of two <= n_in - 1: a fixed, uniform trip count)
     const float uf = __double2float_rd(u);
-    int lo = 0, hi = n_in - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (F[mid] <= uf) lo = mid;
-      else hi = mid - 1;
-    }
+    int lo = 0;
+    for (int step = top; step > 0; step >>= 1)
+      if (lo + step < n_in && F[lo + step] <= uf) lo += step;
     // linear within the bin in fp32 (reading #29): F[lo] <= u < F[lo + 1], so the fraction lies in
     // [0, 1); each step rounds once (back error ~1e-7 plus the output's own rounding), and the
     // clamp to the bin keeps the edges non-decreasing across bins
@@ -241,8 +313,18 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     const float sf = fminf(__fmaf_rn(fminf(frac, 1.0f), __fsub_rn(ej1, ej), ej), ej1);
     so[i] = sf;
     // s lies between two edges: with every edge's 1/t normal, so is Φ(s)'s
-    const double s = (double)sf;
-    if (to) to[i] = (float)(normal ? phi_normal(map, s, tn, inv_tn, inv_tf, tf) : phi(map, s, tn, inv_tn, inv_tf, tf));
+    if (to) {
+      if (tmode == 1) {  // 1/x to 1 ulp (x in [1e-15, 1e15]): t to ~2 ulps, Δs-equivalent ~1e-7
+        float y;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(lin_x(sf, xa, xb)));
+        to[i] = y;
+      } else if (tmode == 2) {
+        to[i] = __fmaf_rn(sf, xb, xa);
+      } else {
+        const double s = (double)sf;
+        to[i] = (float)(normal ? phi_normal(map, s, tn, inv_tn, inv_tf, tf) : phi(map, s, tn, inv_tn, inv_tf, tf));
+      }
+    }
   }
 }
 

@@ -628,6 +628,38 @@ def test_resample_unbounded_lindisp(N):
     assert np.all(np.abs(tg - t_of_s) <= 1e-6 * t_of_s + t_of_s**2 / 0.5 * ulp)
 
 
+@pytest.mark.parametrize("map_kind", [0, 1])
+def test_resample_far_mass(N, map_kind):
+    """Mass in the far bins (s -> 1, where 1/t is small for lindisp): the kernel's fp32 interval
+    lengths (reading #29) must not lose it to cancellation; n_in 256 / 96 / 40 (8, 3, 2 edges per
+    lane) and t_out against Φ(s_out)."""
+    rng = np.random.default_rng(31)
+    for m, n_out in ((256, 96), (96, 48), (40, 17)):
+        n = 600
+        e = np.sort(rng.uniform(0, 1, (n, m + 1)), axis=1).astype(np.float32)
+        e[:, 0], e[:, -1] = 0, 1
+        mid = 0.5 * (e[:, :-1] + e[:, 1:])
+        sig = np.where(mid > 0.85, rng.uniform(0.5, 40, (n, m)), rng.uniform(0, 0.02, (n, m))).astype(np.float32)
+        tn, tf = 0.2, 1000.0
+        # rays 0..99: mass only in a middle bin and in a last bin that starts at s = 1 - 1e-4, where
+        # 1/t_n + s (1/t_f - 1/t_n) would cancel (its fp32 Δt is off by ~3e-4 there; ~4e-6 in F)
+        e[:100, -2] = np.float32(1 - 1e-4)
+        e[:100, :-1] = np.minimum(e[:100, :-1], np.float32(1 - 1e-4))
+        t64 = 1.0 / ((1.0 - e[:100].astype(np.float64)) / tn + e[:100].astype(np.float64) / tf)
+        dt = np.maximum(np.diff(t64, axis=1), 1e-12)
+        sig[:100] = 0.0
+        sig[:100, m // 2] = (0.7 / dt[:, m // 2]).astype(np.float32)
+        sig[:100, -1] = (0.7 / dt[:, -1]).astype(np.float32)
+        sg, tg = N.importance_sample(cuda(e), n_out, sigma=cuda(sig), map_kind=map_kind, t_near=tn, t_far=tf)
+        sr, _ = O.importance_sample(e, n_out, sigma=sig, map_kind=map_kind, t_near=tn, t_far=tf)
+        F = O.importance_cdf(e, sigma=sig, map_kind=map_kind, t_near=tn, t_far=tf)
+        sg, tg = sg.cpu().numpy(), tg.cpu().numpy().astype(np.float64)
+        check_resample(sg, sr, F, e, n_out)
+        s64 = sg.astype(np.float64)
+        t_ref = 1.0 / ((1.0 - s64) / tn + s64 / tf) if map_kind == 1 else tn + s64 * (tf - tn)
+        assert np.all(np.abs(tg - t_ref) <= 4e-7 * t_ref + 1e-6)
+
+
 # ============================================================================ combined estimator
 def gpu_bounds(N, occ, levels, res, roi, o, d, **kw):
     import torch
