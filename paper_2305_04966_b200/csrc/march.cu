@@ -141,6 +141,21 @@ constexpr int kMacro = kMacroCells;  // fine cells per macro cell and axis
 constexpr int kTwoLevels = 0x100;
 constexpr float kSegEps = 1e-3f;
 
+#ifndef NACC_MARCH_STATS
+#define NACC_MARCH_STATS 0  // debug build: count segment classes (nacc_debug_march_stats)
+#endif
+#if NACC_MARCH_STATS
+// [0] owner slots tested, [1] skipped, [2] solid (direct), [3] queued code 1 (interior), [4] queued code 2,
+// [5] evaluation passes, [6] writer passes, [7] tiles, [8] phase-1 passes, [9] emitted points of evaluated
+// segments; why segments are evaluated: [10] an end outside every box, [11] two adjacent levels,
+// [12] a level gap, [13] the finer box within reach, [14] span > the largest window, [15] window not
+// interior; evaluated segments that came out [16] full / [17] empty
+__device__ unsigned long long g_march_stats[18];
+#define MSTAT(i, v) atomicAdd(&g_march_stats[i], (unsigned long long)(v))
+#else
+#define MSTAT(i, v) ((void)0)
+#endif
+
 // The same decision at the fine resolution (reading #22).  The points of a
 // segment have positions x and cell coordinates u = (x - lo) * s computed by
 // the normative fp32 ops of P(k), each of which is monotone in m (RN rounding
@@ -167,7 +182,10 @@ __device__ __forceinline__ int segment_test_floors(const GridConst &g, const uin
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const int lo = min(ia[a], ib[a]), hi = max(ia[a], ib[a]);
-    if (hi - lo > kFineWin - 1) return 2;     // longer than the largest window: evaluate
+    if (hi - lo > kFineWin - 1) {  // longer than the largest window: evaluate
+      MSTAT(14, 1);
+      return 2;
+    }
     if (hi < 0 || lo > R) return 0;          // every point outside the box on this axis
     interior = interior && lo >= 0 && hi <= R - 2;
     c[a] = min(max(lo, 0), R - 1);
@@ -181,7 +199,10 @@ __device__ __forceinline__ int segment_test_floors(const GridConst &g, const uin
   const uint32_t *andm = span == 0 ? bits : orm + g.mw;
   const uint32_t wi = (uint32_t)l * g.r3w + (q >> 5);
   if (!((__ldg(orm + wi) >> (q & 31u)) & 1u)) return 0;
-  if (!interior) return 2;
+  if (!interior) {
+    MSTAT(15, 1);
+    return 2;
+  }
   // solid window: every cell the points can fall in is occupied, so every point is a member
   // (subject only to k < ke and m < far)
   if (NACC_MARCH_SOLID && ((__ldg(andm + wi) >> (q & 31u)) & 1u)) return 3;
@@ -220,15 +241,25 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
     };
     la = level_of<false>(g, A[0], A[1], A[2]);
     const int lb = level_of<false>(g, B[0], B[1], B[2]);
-    if (la < 0 || lb < 0) return 2;
+    if (la < 0 || lb < 0) {
+      MSTAT(10, 1);
+      return 2;
+    }
     if (la != lb) {
       // ends in adjacent levels and box lo - 1 out of reach: every point's level is lo or lo + 1
       // (both ends lie in the convex box lo + 1), flagged for the two-box evaluation
       const int lo = min(la, lb);
-      if (max(la, lb) == lo + 1 && (lo == 0 || !meets(lo - 1))) return 2 | (lo << 4) | kTwoLevels;
+      if (max(la, lb) == lo + 1 && (lo == 0 || !meets(lo - 1))) {
+        MSTAT(11, 1);
+        return 2 | (lo << 4) | kTwoLevels;
+      }
+      MSTAT(12, 1);
       return 2;
     }
-    if (la >= 1 && meets(la - 1)) return 2;
+    if (la >= 1 && meets(la - 1)) {
+      MSTAT(13, 1);
+      return 2;
+    }
     if (mask3 != nullptr) {  // every point lies in level la (convex box, finer box clear): its fine window
       int ia[3], ib[3];
       cell_floors(g, A, ia, la);
@@ -747,6 +778,7 @@ __device__ __forceinline__ void tile_write(const TileBuf &T, int n_ent_t, bool o
         const uint32_t ent = idx < n_ent ? T.ent[idx] : 0u;
         const bool set = (ent >> b) & 1u;
         const unsigned bal = __ballot_sync(kFull, set);  // both entries' masks, in output order
+        if (NACC_MARCH_STATS && lane == 0) MSTAT(6, 1);
         if (set) {
           const int j = ent_j(ent);
           const int pos = carry + __popc(bal & lt);
@@ -880,10 +912,18 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
                                          : occupied<kL1>(g, bits, m, A.x, A.y, A.z, D.x, D.y, D.z)));
           }
           const unsigned bal = __ballot_sync(kFull, pred);
+          if (NACC_MARCH_STATS && lane == 0) {
+            MSTAT(5, 1);
+            MSTAT(9, __popc(bal));
+          }
           if ((lane & 15) == 0 && idx < n_eval) {
             const uint32_t half = (lane ? bal >> 16 : bal) & 0xFFFFu;
             const int slot = qe & 1023;
             if (slot < kECap) T.ent[slot] = ent_pack(j, q, half);
+            if (NACC_MARCH_STATS) {
+              if (half == 0xFFFFu) MSTAT(16, 1);
+              if (half == 0u) MSTAT(17, 1);
+            }
             atomicAdd(&T.cnt[j], __popc(half));
           }
         }
@@ -932,6 +972,18 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
           bool direct = false;
           if (code == 3 && ks + kTSeg <= kej) direct = tile_mid<kCone, kW>(p, A.w, tab, ks + kTSeg - 1) < D.w;
           const unsigned F = __ballot_sync(kFull, flag), Dm = __ballot_sync(kFull, direct);
+          if (NACC_MARCH_STATS) {
+            const unsigned Ow = __ballot_sync(kFull, owner);
+            const unsigned C1 = __ballot_sync(kFull, code == 1 && !direct);
+            if (lane == 0) {
+              MSTAT(0, __popc(Ow));
+              MSTAT(1, __popc(Ow & ~F));
+              MSTAT(2, __popc(Dm));
+              MSTAT(3, __popc(C1));
+              MSTAT(4, __popc(F & ~Dm & ~C1));
+              MSTAT(8, 1);
+            }
+          }
           const int slot = n_ent + __popc(F & lt);
           if (direct) {
             if (slot < kECap) T.ent[slot] = ent_pack(j, q, 0xFFFFu);
@@ -981,6 +1033,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
       cur_agg = agg;
       cur_ne = n_ent;
       lookback_publish(lb->status, tile, cur_agg);
+      if (NACC_MARCH_STATS && lane == 0) MSTAT(7, 1);
     }
     if (prev_tile >= 0) {
       // ---------------- phase 2 of the previous tile (buffer buf ^ 1)
@@ -1315,6 +1368,16 @@ nacc_status nacc_occgrid_ray_bounds(const nacc_grid *grid, const uint32_t *bits,
   return launch_march(kModeBounds, grid, bits, params, rays_o, rays_d, t_min, t_max, n_rays, nullptr, t_near, t_far,
                       nullptr, 0, nullptr, nullptr, ws, stream, reinterpret_cast<unsigned long long *>(n_alive));
 }
+
+#if NACC_MARCH_STATS
+// debug build only: read and reset the segment counters (g_march_stats above)
+void nacc_debug_march_stats(unsigned long long *out18) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out18, g_march_stats, 18 * sizeof(unsigned long long));
+  const unsigned long long z[18] = {};
+  cudaMemcpyToSymbol(g_march_stats, z, sizeof(z));
+}
+#endif
 
 #if NACC_LB_STATS
 // debug build only: read and reset the look-back counters (resolves, polls, sleeping polls, tiles walked)

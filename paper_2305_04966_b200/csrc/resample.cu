@@ -48,6 +48,14 @@ __device__ __forceinline__ float one_minus_exp_neg(float S) {
 }
 
 constexpr int kResampleWarps = 4;
+
+// per-launch constants computed once on the host
+struct ResampleConst {
+  double inv_tn, inv_tf;  // 1/t_n, 1/t_f (0 for t_f = inf); unused with per-ray spans
+  double inv_n;           // 1/n_out
+  double s_thr;           // -log1p(-1e-12): S_m > s_thr <=> F_m = 1 - e^{-S_m} > 1e-12 (reading #16)
+  int top;                // largest power of two <= n_in - 1 (0 for n_in = 1)
+};
 #ifndef NACC_RESAMPLE_F32DT
 #define NACC_RESAMPLE_F32DT 1  // build parameter: interval lengths by the fp32 product identities (cdf_items)
 #endif
@@ -75,7 +83,7 @@ __device__ __forceinline__ float lin_x(float s, float itn, float itf) {
 template <int kIPL, int kMode, typename PhiE>
 __device__ __forceinline__ double cdf_items(int n_in, const float *__restrict__ er, const float *__restrict__ sr,
                                             float *e, float *F, PhiE phi_e, float xa, float xb, float dc,
-                                            bool &uniform) {
+                                            double s_thr, bool &uniform) {
   const int lane = threadIdx.x & 31;
   const int j0 = lane * kIPL;
   float ev[kIPL + 1], sv[kIPL];
@@ -149,7 +157,7 @@ __device__ __forceinline__ double cdf_items(int n_in, const float *__restrict__ 
 #pragma unroll
     for (int k = 0; k < kIPL; ++k) f[k] = fmaxf(f[k], before);
   const double total = __shfl_sync(kFull, incl, 31);
-  uniform = !(-expm1(-total) > 1e-12);
+  uniform = !(total > s_thr);  // F_m = 1 - e^{-S_m} > 1e-12 <=> S_m > -log1p(-1e-12) (host constant)
   const float Fm = one_minus_exp_neg((float)total), rFm = __frcp_rn(Fm);
 #pragma unroll
   for (int k = 0; k < kIPL; ++k) {
@@ -166,7 +174,7 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     int64_t n_rays, int n_in, const float *__restrict__ s_edges, const float *__restrict__ sigma,
     const float *__restrict__ cdf, int map, double tn, double tf, const float *__restrict__ tn_r,
     const float *__restrict__ tf_r, int n_out, int stratified, uint32_t key0, uint32_t key1,
-    float *__restrict__ s_out, float *__restrict__ t_out) {
+    float *__restrict__ s_out, float *__restrict__ t_out, ResampleConst rc) {
   extern __shared__ float smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t r = (int64_t)blockIdx.x * kResampleWarps + warp;
@@ -186,7 +194,8 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
       return;
     }
   }
-  const double inv_tn = 1.0 / tn, inv_tf = isinf(tf) ? 0.0 : 1.0 / tf;
+  // launch constants from the host (1/t_n, 1/t_f, 1/n, ...); per-ray spans compute their own
+  const double inv_tn = kRanged ? 1.0 / tn : rc.inv_tn, inv_tf = kRanged ? (isinf(tf) ? 0.0 : 1.0 / tf) : rc.inv_tf;
   bool uniform = false, normal = false;
   int tmode = 0;  // t_out: 0 Φ in fp64; 1 lindisp 1/lin_x(s, 1/t_n, 1/t_f) in fp32; 2 identity t_n + s w in fp32
   float xa = 0.f, xb = 0.f;
@@ -199,17 +208,17 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
       tmode = 1;
       xa = (float)inv_tn;
       xb = (float)inv_tf;
-      cdf_items<kIPL, 1>(n_in, er, sr, e, F, phi_n, xa, xb, (float)(inv_tn - inv_tf), uniform);
+      cdf_items<kIPL, 1>(n_in, er, sr, e, F, phi_n, xa, xb, (float)(inv_tn - inv_tf), rc.s_thr, uniform);
     } else if (NACC_RESAMPLE_F32DT && map == NACC_MAP_IDENTITY && in01 && tf - tn <= 1e15) {
       tmode = 2;
       xa = (float)tn;
       xb = (float)(tf - tn);
-      cdf_items<kIPL, 2>(n_in, er, sr, e, F, phi_n, 0.f, 0.f, xb, uniform);
+      cdf_items<kIPL, 2>(n_in, er, sr, e, F, phi_n, 0.f, 0.f, xb, rc.s_thr, uniform);
     } else if (normal)
-      cdf_items<kIPL, 0>(n_in, er, sr, e, F, phi_n, 0.f, 0.f, 0.f, uniform);
+      cdf_items<kIPL, 0>(n_in, er, sr, e, F, phi_n, 0.f, 0.f, 0.f, rc.s_thr, uniform);
     else
       cdf_items<kIPL, 0>(n_in, er, sr, e, F, [&](double sv) { return phi(map, sv, tn, inv_tn, inv_tf, tf); }, 0.f,
-                         0.f, 0.f, uniform);
+                         0.f, 0.f, rc.s_thr, uniform);
   } else {
     for (int j = lane; j <= n_in; j += 32) e[j] = __ldg(er + j);
     __syncwarp();
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
         carry += __shfl_sync(kFull, incl, 31);
       }
       if (lane == 0) F[0] = 0.f;
-      uniform = !(-expm1(-carry) > 1e-12);
+      uniform = !(carry > rc.s_thr);
       __syncwarp();
       if (!uniform) {  // F / F_m by one reciprocal (within an ulp of the quotient); F_m / F_m = 1 exactly
         const float Fm = F[n_in], rFm = __frcp_rn(Fm);
@@ -262,11 +271,11 @@ __global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
     for (int j = lane; j <= n_in; j += 32) F[j] = __fdiv_rn(__fsub_rn(e[j], e0), den);
   }
   __syncwarp();
-  const double inv_n = 1.0 / (double)n_out;
+  const double inv_n = rc.inv_n;
   float *so = s_out + r * (int64_t)(n_out + 1);
   float *to = t_out ? t_out + r * (int64_t)(n_out + 1) : nullptr;
   int n_search = n_out + 1;
-  const int top = n_in > 1 ? 1 << (31 - __clz(n_in - 1)) : 0;  // binary-lifting first step
+  const int top = rc.top;  // binary-lifting first step: the largest power of two <= n_in - 1
   if (!stratified) {
     // u = 1 at i = n_out: the smallest j in [0, n_in-1] with F[j+1] >= 1.  {j : F[j+1] >= 1} is a
     // suffix of the bins (F monotone, F[n_in] = 1), so scan 32-bin windows from the end and stop
@@ -333,13 +342,20 @@ static nacc_status launch_importance(int64_t n_rays, int32_t n_in, const float *
                                      const float *tn_r, const float *tf_r, int32_t n_out, int32_t stratified,
                                      uint64_t seed, float *s_out, float *t_out, cudaStream_t stream) {
   NACC_REQUIRE(s_edges && s_out, "s_edges and s_out must be non-NULL");
+  const int ipl = NACC_RESAMPLE_ITEMS && sigma && n_in <= 256 ? (n_in + 31) / 32 : 0;
   const size_t smem = (size_t)kResampleWarps * 2 * (n_in + 1) * sizeof(float);
   if (smem > 227 * 1024) {
     set_error("nacc_importance_sample: n_in too large for shared memory");
     return NACC_ERR_UNSUPPORTED;
   }
   const uint32_t k0 = (uint32_t)(seed & 0xffffffffu), k1 = (uint32_t)(seed >> 32);
-  const int ipl = NACC_RESAMPLE_ITEMS && sigma && n_in <= 256 ? (n_in + 31) / 32 : 0;
+  ResampleConst rc;
+  rc.inv_tn = tn_r ? 0.0 : 1.0 / t_near;
+  rc.inv_tf = tn_r ? 0.0 : (std::isinf(t_far) ? 0.0 : 1.0 / t_far);
+  rc.inv_n = 1.0 / (double)n_out;
+  rc.s_thr = -std::log1p(-1e-12);
+  rc.top = 0;
+  while (n_in > 1 && 2 * rc.top <= n_in - 1) rc.top = rc.top ? 2 * rc.top : 1;
   nacc_status st = NACC_OK;
   auto go = [&](auto ranged, auto items) {
     constexpr bool kR = decltype(ranged)::value;
@@ -353,7 +369,7 @@ static nacc_status launch_importance(int64_t n_rays, int32_t n_in, const float *
     }
     importance_kernel<kR, kI><<<grid_for(n_rays, kResampleWarps), kResampleWarps * 32, smem, stream>>>(
         n_rays, n_in, s_edges, sigma, cdf, (int)map, t_near, t_far, tn_r, tf_r, n_out, stratified, k0, k1, s_out,
-        t_out);
+        t_out, rc);
   };
   auto by_items = [&](auto ranged) {
     using I = std::integral_constant<int, 0>;
