@@ -115,9 +115,15 @@ inline int grid_for(int64_t work_items, int per_block, int64_t cap = (1ll << 31)
 // occupancy bitfield auxiliary skip mask (gridaux.cu)
 constexpr int kMacroCells = 4;  // fine cells per macro cell and axis
 #ifndef NACC_MARCH_WIN
-#define NACC_MARCH_WIN 5  // fine-mask window (cells per axis): 3 for 8-point segments, 5 for 16
+#define NACC_MARCH_WIN 9  // largest fine-mask window (cells per axis) of cascaded grids
+#endif
+#ifndef NACC_MARCH_WIN1
+#define NACC_MARCH_WIN1 5  // largest window of single-level grids (a 16-point segment of the CFG2 lattice spans <= 5)
 #endif
 constexpr int kFineWin = NACC_MARCH_WIN;
+// windows w = 2..grid_fine_win(g) are built: cascades (cone lattices: a 16-point segment can span up to ~9
+// cells per axis; A/B on CFG3 with 5 / 7 / 9: 2.72 / 2.39 / 2.36 ms) and single-level grids (CFG2: 5 / 9 equal)
+int grid_fine_win(const nacc_grid &g);
 bool grid_skip_enabled(const nacc_grid &g);
 int64_t grid_aux_offset_words(const nacc_grid &g);   // start of the private region (gridaux.cu)
 int64_t grid_mask2_offset_words(const nacc_grid &g);  // the macro skip mask

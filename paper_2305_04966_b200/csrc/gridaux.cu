@@ -11,7 +11,7 @@
 //     of every level, the OR of the fine bits of macro cells m + {0,1}^3,
 //     i.e. of the fine cells [4m, 4m + 8)^3 clipped to the level;
 //   mask3 (every grid with skipping; per level): for every fine cell c and every
-//     window size w = 2..W (W = kFineWin), the OR and the AND of the fine bits of
+//     window size w = 2..W (W = grid_fine_win: 9 for cascades, 5 for one level), the OR and the AND of the fine bits of
 //     cells c + {0..w-1}^3 clipped to the level, at the fine resolution, stored as
 //     OR_2, AND_2, OR_3, AND_3, ..., OR_W, AND_W (the march's segment test picks the
 //     window of its segment's cell span: a 16-point segment spans at most 5 cells
@@ -38,6 +38,8 @@ static int64_t mask2_words(const nacc_grid &g) {
 
 bool grid_fine_mask_enabled(const nacc_grid &g) { return grid_skip_enabled(g); }
 
+int grid_fine_win(const nacc_grid &g) { return g.levels > 1 ? kFineWin : (kFineWin < NACC_MARCH_WIN1 ? kFineWin : NACC_MARCH_WIN1); }
+
 int64_t grid_mask3_offset_words(const nacc_grid &g) { return grid_mask2_offset_words(g) + mask2_words(g); }
 
 static int64_t mask3_words(const nacc_grid &g) {  // one mask, every level (level-major, R^3 bits each)
@@ -48,7 +50,7 @@ static int64_t grid_aux_words(const nacc_grid &g) {
   if (!grid_skip_enabled(g)) return kAuxHeaderWords;
   const int64_t w = kAuxHeaderWords + mask2_words(g);
   if (!grid_fine_mask_enabled(g)) return w;
-  return w + 2 * (kFineWin - 1) * mask3_words(g);  // OR and AND window masks per window size 2..W
+  return w + 2 * (grid_fine_win(g) - 1) * mask3_words(g);  // OR and AND window masks per window size 2..W
 }
 
 __global__ void bbox_init_kernel(int32_t *__restrict__ hdr, int levels, int R) {
@@ -266,11 +268,16 @@ cudaError_t grid_prepare(const nacc_grid &g, uint32_t *bits, cudaStream_t stream
       }
       count_launch(2);
     };
-    static_assert(kFineWin >= 2 && kFineWin <= 5, "window sizes 2..5");
+    static_assert(kFineWin >= 2 && kFineWin <= 9, "window sizes 2..9");
     masks(std::integral_constant<int, 2>{});
-    if (kFineWin >= 3) masks(std::integral_constant<int, 3 <= kFineWin ? 3 : 2>{});
-    if (kFineWin >= 4) masks(std::integral_constant<int, 4 <= kFineWin ? 4 : 2>{});
-    if (kFineWin >= 5) masks(std::integral_constant<int, 5 <= kFineWin ? 5 : 2>{});
+    const int W = grid_fine_win(g);
+    if (W >= 3) masks(std::integral_constant<int, 3 <= kFineWin ? 3 : 2>{});
+    if (W >= 4) masks(std::integral_constant<int, 4 <= kFineWin ? 4 : 2>{});
+    if (W >= 5) masks(std::integral_constant<int, 5 <= kFineWin ? 5 : 2>{});
+    if (W >= 6) masks(std::integral_constant<int, 6 <= kFineWin ? 6 : 2>{});
+    if (W >= 7) masks(std::integral_constant<int, 7 <= kFineWin ? 7 : 2>{});
+    if (W >= 8) masks(std::integral_constant<int, 8 <= kFineWin ? 8 : 2>{});
+    if (W >= 9) masks(std::integral_constant<int, 9 <= kFineWin ? 9 : 2>{});
   }
   return cudaGetLastError();
 }

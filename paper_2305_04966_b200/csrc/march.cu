@@ -42,6 +42,7 @@ namespace nacc {
 struct GridConst {
   int levels, res;
   uint32_t r3w, mw;  // bit words per level (R^3 / 32); words per window mask (levels * r3w, 64-word aligned)
+  int win;           // largest window mask (cells per axis, grid_fine_win)
   float lo[8][3], hi[8][3], s[8][3];
   float olo[3], ohi[3];  // outermost box padded by 1e-4*width + 1e-6
 };
@@ -58,6 +59,7 @@ static GridConst make_grid_const(const nacc_grid &g) {
   c.res = g.res;
   c.r3w = (uint32_t)((int64_t)g.res * g.res * g.res / 32);
   c.mw = (uint32_t)((((int64_t)g.levels * c.r3w + 63) / 64) * 64);
+  c.win = grid_fine_win(g);
   for (int a = 0; a < 3; ++a) {
     const double lo0 = (double)g.roi[a], hi0 = (double)g.roi[3 + a];
     const double ctr = (lo0 + hi0) / 2.0, half = (hi0 - lo0) / 2.0;
@@ -160,7 +162,7 @@ __device__ unsigned long long g_march_stats[18];
 // segment have positions x and cell coordinates u = (x - lo) * s computed by
 // the normative fp32 ops of P(k), each of which is monotone in m (RN rounding
 // is monotone), so every point's floor(u) lies between the endpoints' floors,
-// exactly, per axis.  With at most W = kFineWin cells per axis that range lies
+// exactly, per axis.  With at most W = g.win cells per axis that range lies
 // in c + {0..W-1}^3, c = the clamped low corner, and mask3[c] (the OR of those
 // W^3 fine bits) being 0 proves no point is emitted.  A segment whose floors lie
 // in [0, R-2] on every axis is inside the box (u >= 0 <=> x >= lo exactly;
@@ -182,7 +184,7 @@ __device__ __forceinline__ int segment_test_floors(const GridConst &g, const uin
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const int lo = min(ia[a], ib[a]), hi = max(ia[a], ib[a]);
-    if (hi - lo > kFineWin - 1) {  // longer than the largest window: evaluate
+    if (hi - lo > g.win - 1) {  // longer than the largest window: evaluate
       MSTAT(14, 1);
       return 2;
     }
