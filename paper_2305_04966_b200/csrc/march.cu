@@ -223,10 +223,12 @@ __device__ __forceinline__ int segment_test_fine(const GridConst &g, const uint3
 // Returns 0 (skip the segment), 1 (evaluate; the segment lies inside the
 // single level's box with margin, so P(k) can skip the box test) or 2
 // (evaluate with the full predicate).
+// la_in / lb_in: the ends' levels when the caller has them (level_of), else -2
 template <bool kL1>
 __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *__restrict__ bits,
                                             const uint32_t *__restrict__ mask2, int M,
-                                            const uint32_t *__restrict__ mask3, const float A[3], const float B[3]) {
+                                            const uint32_t *__restrict__ mask3, const float A[3], const float B[3],
+                                            int la_in = -2, int lb_in = -2) {
   int la = 0;
   if (!kL1) {
     // does the segment's bounding box (padded) reach box l?  Every point of the segment lies in
@@ -241,8 +243,8 @@ __device__ __forceinline__ int segment_test(const GridConst &g, const uint32_t *
       }
       return m;
     };
-    la = level_of<false>(g, A[0], A[1], A[2]);
-    const int lb = level_of<false>(g, B[0], B[1], B[2]);
+    la = la_in != -2 ? la_in : level_of<false>(g, A[0], A[1], A[2]);
+    const int lb = lb_in != -2 ? lb_in : level_of<false>(g, B[0], B[1], B[2]);
     if (la < 0 || lb < 0) {
       MSTAT(10, 1);
       return 2;
@@ -962,9 +964,16 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
             float Y[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) Y[a] = __shfl_down_sync(kFull, X[a], 1);
+            // cascades: every slot's first point gets its level once; the segment's far end is
+            // the next slot's first point, so its level comes from the next lane
+            int la = -2, lb = -2;
+            if (!kL1) {
+              la = level_of<false>(g, X[0], X[1], X[2]);
+              lb = __shfl_down_sync(kFull, la, 1);
+            }
             if (owner) {
               code = (kL1 && mask3 != nullptr) ? segment_test_fine(g, bits, mask3, X, Y)
-                                                : segment_test<kL1>(g, bits, mask2, M, mask3, X, Y);
+                                                : segment_test<kL1>(g, bits, mask2, M, mask3, X, Y, la, lb);
               two = (code & kTwoLevels) != 0;
               lvl = (code >> 4) & 7;
               code &= 15;
