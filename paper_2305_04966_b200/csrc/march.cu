@@ -679,6 +679,10 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 // (t0, t1, ray_id) runs, 32 lattice points per pass.  A tile whose entries
 // overflow the buffer (or with a ray longer than 2^16 points) is counted and
 // written by direct traversal instead (traverse_ray).
+#ifndef NACC_MARCH_WPAIR
+#define NACC_MARCH_WPAIR 1  // build parameter: writer with two consecutive lattice points per lane (0 off,
+                            // 1 cones / cascades: CFG3 2.236 -> 2.182 ms; 2 every grid: CFG2 161.5 -> 163.1 us)
+#endif
 #ifndef NACC_MARCH_NOLOOKBACK
 #define NACC_MARCH_NOLOOKBACK 0  // timing experiment only (wrong output): no look-back
 #endif
@@ -776,6 +780,48 @@ __device__ __forceinline__ void tile_write(const TileBuf &T, int n_ent_t, bool o
       float *const o0 = obase[0], *const o1 = obase[1];
       int32_t *const oid = reinterpret_cast<int32_t *>(obase[2]);
       int carry = 0;  // samples written so far in the tile
+      if constexpr (NACC_MARCH_WPAIR == 2 || (NACC_MARCH_WPAIR == 1 && (kCone || !kL1))) {
+      // two consecutive lattice points per lane, four entries per pass: one entry decode, one
+      // k, three lattice ends and one output position per two samples; the points' output slots
+      // come from two ballots (a lane's two samples are consecutive in the output)
+      const int b2 = (lane & 7) * 2;
+      for (int e = 0; e < n_ent; e += 4) {
+        const int idx = e + (lane >> 3);
+        const uint32_t ent = idx < n_ent ? T.ent[idx] : 0u;
+        const bool s0 = (ent >> b2) & 1u, s1 = (ent >> (b2 + 1)) & 1u;
+        const unsigned B0 = __ballot_sync(kFull, s0), B1 = __ballot_sync(kFull, s1);
+        if (NACC_MARCH_STATS && lane == 0) MSTAT(6, 1);
+        if (s0 || s1) {
+          const int j = ent_j(ent);
+          const int pos = carry + __popc(B0 & lt) + __popc(B1 & lt);
+          const int k = T.kr[j].x + ent_k16(ent) + b2;  // kb_j + 16 q + b2
+          const int32_t rid = (int32_t)(r_base + j);
+          float ta, tb, tc;
+          if (kCone) {
+            ta = __ldg(tab + k);
+            tb = __ldg(tab + k + 1);
+            tc = s1 ? __ldg(tab + k + 2) : 0.f;
+          } else {
+            const float nr = T.od[j][0].w;
+            ta = __fmaf_rn((float)k, p.step, nr);
+            tb = __fmaf_rn((float)(k + 1), p.step, nr);
+            tc = __fmaf_rn((float)(k + 2), p.step, nr);
+          }
+          if (s0) {
+            o0[pos] = ta;
+            o1[pos] = tb;
+            oid[pos] = rid;
+          }
+          if (s1) {
+            const int p1 = pos + (s0 ? 1 : 0);
+            o0[p1] = tb;
+            o1[p1] = tc;
+            oid[p1] = rid;
+          }
+        }
+        carry += __popc(B0) + __popc(B1);
+      }
+      } else {
       const int b = lane & 15;
       for (int e = 0; e < n_ent; e += 2) {
         const int idx = e + (lane >> 4);
@@ -794,6 +840,7 @@ __device__ __forceinline__ void tile_write(const TileBuf &T, int n_ent_t, bool o
           oid[pos] = (int32_t)(r_base + j);
         }
         carry += __popc(bal);
+      }
       }
     } else {  // overflowed tile: traverse again, writing directly
       for (int jj = 0; jj < kR; ++jj) {
