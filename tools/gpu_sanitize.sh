@@ -8,6 +8,7 @@ SUB='tests/test_gpu_parity.py::test_march_cfg1 tests/test_gpu_parity.py::test_ma
  tests/test_gpu_parity.py::test_render_flat_unaligned tests/test_gpu_parity.py::test_render_degenerate
  tests/test_gpu_parity.py::test_render_cfg1 tests/test_gpu_parity.py::test_weights_and_accumulate
  tests/test_gpu_parity.py::test_weights_alpha tests/test_gpu_parity.py::test_resample_cdf_input_stratified_and_degenerate
+ tests/test_gpu_parity.py::test_resample_unbounded_lindisp tests/test_gpu_parity.py::test_resample_far_mass
  tests/test_gpu_parity.py::test_occgrid_points_bit_exact tests/test_gpu_parity.py::test_occgrid_update_bit_exact
  tests/test_gpu_parity.py::test_pdf_loss tests/test_gpu_parity.py::test_dynamic_grid_times_and_max_merge'
 for tool in memcheck racecheck synccheck initcheck; do
