@@ -119,16 +119,17 @@ NCU_KERNELS_OF_STAGE = {"march": ["march_fused"], "render_fwd": ["render_fwd_war
                         "field_sigma_rgb": ["field_samples"]}
 
 
-def ncu_traffic():
+def ncu_traffic(suffix=""):
     """dram read+write bytes per launch per stage, from the newest committed `ncu --set full` capture
-    (profiles/<round>/ncu_traffic_bytes.json, written by tools/make_profiles.py)."""
+    (profiles/<round>/ncu_traffic_bytes.json, written by tools/make_profiles.py); suffix "_cfg5"
+    selects the captures taken at the CFG5 launch shape (2^21 rays per launch)."""
     rounds = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic_bytes.json")))
     if not rounds:
         return {}
     with open(rounds[-1]) as f:
         by_kernel = json.load(f)
-    return {st: sum(by_kernel[k] for k in ks) for st, ks in NCU_KERNELS_OF_STAGE.items()
-            if all(k in by_kernel for k in ks)}
+    return {st: sum(by_kernel[k + suffix] for k in ks) for st, ks in NCU_KERNELS_OF_STAGE.items()
+            if all(k + suffix in by_kernel for k in ks)}
 
 
 def ncu_warp_instructions(kernel="march_fused"):
@@ -968,16 +969,24 @@ def run_nacc(args):
             byts = algorithmic_bytes(dom, pre_pc, post_pc, rays_pc)
             ms_launch = lib_stages[dom] / n_chunks
             achieved = byts / (ms_launch / 1e3) / 1e9
-            tr = ncu_traffic().get(dom)
+            # traffic from a capture at this launch shape when one is committed (CFG5: 2^21 rays)
+            shape = "_cfg5" if rays_pc == (1 << 21) else ""
+            tr = ncu_traffic(shape).get(dom) if shape else None
+            note = ("ncu dram bytes of one launch at this shape (profiles/, CFG5 chunk of 2^21 rays)"
+                    if tr else None)
+            if tr is None:
+                shape = ""
+                tr = ncu_traffic().get(dom)
+                note = "ncu dram bytes per launch of the committed CFG2 capture (profiles/), the same kernel at " \
+                       "2^18 rays" if tr else None
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                     "traffic": tr, "kernel": dom, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": byts,
-                    "ms_per_launch": ms_launch, "traffic_note": "ncu dram bytes per launch of the committed CFG2 "
-                    "capture (profiles/), the same kernel at 2^18 rays" if tr else None}
+                    "ms_per_launch": ms_launch, "traffic_note": note}
             # the march is bound by instruction issue, not HBM (DESIGN.md §6/§10): its warp
             # instructions per launch (committed ncu capture, CFG2 shape) over the issue peak of
             # 148 SMs x 4 schedulers x 1 warp-instruction per cycle at the sampled SM clock
-            winst = ncu_warp_instructions() if dom == "march" else None
-            if winst and rays_pc == (1 << 18):
+            winst = ncu_warp_instructions("march_fused" + shape) if dom == "march" else None
+            if winst and rays_pc == (1 << (21 if shape else 18)):
                 sm_mhz = clk.summary().get("sm_mhz") or 1965.0
                 n_sm = torch.cuda.get_device_properties(device).multi_processor_count
                 issue_peak = n_sm * 4 * sm_mhz * 1e6

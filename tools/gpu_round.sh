@@ -7,6 +7,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2 > 
 timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 300 -c 110 --csv --log-file gpurun_out/launches.csv \
   python bench.py --workload cfg2 --steps 12 --warmup 3 --profile --no-cpu-baseline > /dev/null 2>&1
+bash tools/gpu_ncu.sh march_fused march_fused_cfg5 2 --workload cfg5 --steps 1 --warmup 2 --profile --no-cpu-baseline
 for k in march_fused render_fwd_warp render_bwd_warp filter_cut filter_copy; do
   bash tools/gpu_ncu.sh $k $k 3
 done
