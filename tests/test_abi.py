@@ -56,8 +56,11 @@ def test_version_and_sizes(lib):
     assert lib.nacc_abi_version() == 1
     g = GridSpec(res=128, levels=4).c()
     # fine bits + private header (occupied boxes) + macro skip mask + the fine OR / AND
-    # window masks for window sizes 2..5 (one bit per fine cell of every level each)
-    assert lib.nacc_grid_bits_bytes(C.byref(g)) == (1 + 2 * 4) * (4 * 128**3 // 8) + 256 + 4 * 32**3 // 8
+    # window masks (one bit per fine cell of every level each) for window sizes 2..9 on
+    # cascades, 2..5 on a single level (gridaux.cu grid_fine_win)
+    assert lib.nacc_grid_bits_bytes(C.byref(g)) == (1 + 2 * 8) * (4 * 128**3 // 8) + 256 + 4 * 32**3 // 8
+    g1 = GridSpec(res=128, levels=1).c()
+    assert lib.nacc_grid_bits_bytes(C.byref(g1)) == (1 + 2 * 4) * (128**3 // 8) + 256 + 32**3 // 8
     g.levels = 0
     assert lib.nacc_grid_bits_bytes(C.byref(g)) == 0
     g = GridSpec(res=128).c()
