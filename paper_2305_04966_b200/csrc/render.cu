@@ -231,6 +231,10 @@ struct Items {
 #ifndef NACC_RENDER_BPS
 #define NACC_RENDER_BPS 4  // blocks per SM of the tile kernels (A/B: 2 / 3 / 4 -> bwd 88.4 / 81.7 / 79.7 us)
 #endif
+#ifndef NACC_RENDER_GRIDX
+#define NACC_RENDER_GRIDX 2  // build parameter: grid of the tile kernels as a multiple of the resident blocks
+                             // (2: a second wave balances the forward's tiles; CFG2 fwd 60.3 -> 59.5 us)
+#endif
 #ifndef NACC_RENDER_TPROD
 #define NACC_RENDER_TPROD 1  // build parameter: T_{j+1} = T_j e^{-s_j} within a thread's items
 #endif
@@ -569,7 +573,7 @@ static unsigned resident_blocks(int64_t want) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm <= 0) n_sm = 1;
   }
-  const int64_t cap = (int64_t)n_sm * NACC_RENDER_BPS;
+  const int64_t cap = (int64_t)n_sm * NACC_RENDER_BPS * NACC_RENDER_GRIDX;
   return (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 

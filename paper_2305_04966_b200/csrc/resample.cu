@@ -47,7 +47,14 @@ __device__ __forceinline__ float one_minus_exp_neg(float S) {
   return 1.0f - __expf(-S);
 }
 
-constexpr int kResampleWarps = 4;
+#ifndef NACC_RESAMPLE_WARPS
+#define NACC_RESAMPLE_WARPS 4  // build parameter: rays (warps) per block
+#endif
+#ifndef NACC_RESAMPLE_MINB
+#define NACC_RESAMPLE_MINB 11  // build parameter: min resident blocks per SM in the launch bounds (A/B: 1 / 8 / 9 / 10 / 11 / 12:
+                               // 112.7/57.4, 113.0/57.4, 109.6/55.4, 108.5/53.4, 106.5/53.4, 106.5/53.3 us)
+#endif
+constexpr int kResampleWarps = NACC_RESAMPLE_WARPS;
 
 // per-launch constants computed once on the host
 struct ResampleConst {
@@ -170,7 +177,7 @@ __device__ __forceinline__ double cdf_items(int n_in, const float *__restrict__ 
 }
 
 template <bool kRanged, int kIPL>
-__global__ void __launch_bounds__(kResampleWarps * 32) importance_kernel(
+__global__ void __launch_bounds__(kResampleWarps * 32, NACC_RESAMPLE_MINB) importance_kernel(
     int64_t n_rays, int n_in, const float *__restrict__ s_edges, const float *__restrict__ sigma,
     const float *__restrict__ cdf, int map, double tn, double tf, const float *__restrict__ tn_r,
     const float *__restrict__ tf_r, int n_out, int stratified, uint32_t key0, uint32_t key1,
