@@ -231,6 +231,9 @@ struct Items {
 #ifndef NACC_RENDER_BPS
 #define NACC_RENDER_BPS 4  // blocks per SM of the tile kernels (A/B: 2 / 3 / 4 -> bwd 88.4 / 81.7 / 79.7 us)
 #endif
+#ifndef NACC_RENDER_COLORONLY
+#define NACC_RENDER_COLORONLY 1  // build parameter: colour-loss backward without the per-ray constants kernel
+#endif
 #ifndef NACC_RENDER_GRIDX
 #define NACC_RENDER_GRIDX 2  // build parameter: grid of the tile kernels as a multiple of the resident blocks
                              // (2: a second wave balances the forward's tiles; CFG2 fwd 60.3 -> 59.5 us)
@@ -618,12 +621,30 @@ __global__ void __launch_bounds__(256) ray_grad_kernel(int64_t n_rays, const dou
   gq[2 * r + 1] = make_double2(q.R, 0.0);
 }
 
-template <bool kVec>
+// kColorOnly (g_opacity = g_depth = NULL, the colour-loss case): g_O' = g_N = 0, so the per-ray
+// constants are g_C itself and R = <g_C, C>, read directly (g_color, ctx) instead of from the
+// ray_grad_kernel workspace, whose launch and 100 B per ray are skipped; the arithmetic is the same
+// (the zero terms add +0).
+template <bool kVec, bool kColorOnly = false>
 __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
     const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
     const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma,
     const float *__restrict__ rgb, double L, const float4 *__restrict__ gcv, const double2 *__restrict__ gq,
-    float *__restrict__ g_sigma, float *__restrict__ g_rgb) {
+    float *__restrict__ g_sigma, float *__restrict__ g_rgb, const float *__restrict__ g_color = nullptr,
+    const double *__restrict__ ctx = nullptr) {
+  auto ray_gc = [&](int32_t r) {
+    if (kColorOnly)
+      return make_float4(__ldg(g_color + 3 * (int64_t)r), __ldg(g_color + 3 * (int64_t)r + 1),
+                         __ldg(g_color + 3 * (int64_t)r + 2), 0.f);
+    return __ldg(gcv + r);
+  };
+  auto ray_R = [&](int32_t r, const float4 &gc) {
+    if (kColorOnly) {
+      const double *cx = ctx + 5 * (int64_t)r;
+      return (double)gc.x * __ldg(cx) + (double)gc.y * __ldg(cx + 1) + (double)gc.z * __ldg(cx + 2);
+    }
+    return __ldg(gq + 2 * (int64_t)r + 1).x;
+  };
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t N = min(packed_end(packed_info, n_rays), n_samples);  // in bounds after an overflowed march
@@ -662,13 +683,15 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
           if (it.valid[j] && !(S[j] > L)) {
             live |= 1u << j;
             if (!NACC_RENDER_RAYCACHE || it.rid[j] != cr) {
-              gc = __ldg(gcv + it.rid[j]);
-              gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
+              gc = ray_gc(it.rid[j]);
+              if (!kColorOnly) gon = __ldg(gq + 2 * (int64_t)it.rid[j]);
               cr = it.rid[j];
             }
             w[j] = T * (1.0 - ea);
-            const double gw = (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2] +
-                              gon.x + gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
+            const double gw =
+                kColorOnly ? (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2]
+                           : (double)gc.x * col[3 * j] + (double)gc.y * col[3 * j + 1] + (double)gc.z * col[3 * j + 2] +
+                                 gon.x + gon.y * (0.5 * ((double)it.t0[j] + (double)it.t1[j]));
             v = gw * w[j];
             gwTea[j] = gw * T * ea;
           }
@@ -691,8 +714,8 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_bwd_warp_kernel(
         gr[3 * j] = gr[3 * j + 1] = gr[3 * j + 2] = 0.f;
         if (live & (1u << j)) {
           if (!NACC_RENDER_RAYCACHE || it.rid[j] != cr) {
-            gc = __ldg(gcv + it.rid[j]);
-            R = __ldg(gq + 2 * (int64_t)it.rid[j] + 1).x;
+            gc = ray_gc(it.rid[j]);
+            R = ray_R(it.rid[j], gc);
             cr = it.rid[j];
           }
           const double Q = R - run.v[0];  // Σ_{i>j} g_w_i w_i of the ray
@@ -1016,18 +1039,28 @@ nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, i
     NACC_REQUIRE(ws && ws_bytes >= nacc_render_bwd_workspace_bytes(n_rays), "workspace too small");
     float4 *gcv = static_cast<float4 *>(ws);
     double2 *gq = reinterpret_cast<double2 *>(static_cast<char *>(ws) + align_up((size_t)n_rays * 16, 256));
-    ray_grad_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(n_rays, ctx, g_color, g_opacity, g_depth, gcv, gq);
+    const bool color_only = NACC_RENDER_COLORONLY && g_color && !g_opacity && !g_depth;
+    if (!color_only)
+      ray_grad_kernel<<<grid_for(n_rays, 256), 256, 0, stream>>>(n_rays, ctx, g_color, g_opacity, g_depth, gcv, gq);
     const int64_t n_wtiles = ceil_div(n_samples, kWarpTileBwd);
     const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(rgb, 16) &&
                      aligned(ray_id, 16) && aligned(g_sigma, 16) && (!g_rgb || aligned(g_rgb, 16));
     const unsigned blocks = resident_blocks(ceil_div(n_wtiles * 32, 256));
-    if (vec)
+    if (color_only && vec)
+      render_bwd_warp_kernel<true, true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1,
+                                                                     sigma, rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb,
+                                                                     g_color, ctx);
+    else if (color_only)
+      render_bwd_warp_kernel<false, true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1,
+                                                                      sigma, rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb,
+                                                                      g_color, ctx);
+    else if (vec)
       render_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
                                                                rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb);
     else
       render_bwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
                                                                 rgb, neg_log_eps, gcv, gq, g_sigma, g_rgb);
-    count_launch(1);
+    if (!color_only) count_launch(1);
   } else {
     render_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma, rgb,
                                                                        neg_log_eps, ctx, g_color, g_opacity, g_depth,

@@ -359,7 +359,9 @@ def gpu_render(N, pk, t0, t1, sig, rgb, g_color, g_opacity, g_depth, eps=None, f
     sg = cuda(sig).requires_grad_()
     cg = cuda(rgb).requires_grad_()
     color, opacity, depth = N.rendering(s, sg, cg, eps=eps)
-    loss = (color * cuda(g_color)).sum() + (opacity * cuda(g_opacity)).sum() + (depth * cuda(g_depth)).sum()
+    loss = (color * cuda(g_color)).sum()
+    if g_opacity is not None:  # None: opacity / depth unused -> NULL gradients (the colour-only backward)
+        loss = loss + (opacity * cuda(g_opacity)).sum() + (depth * cuda(g_depth)).sum()
     loss.backward()
     torch.cuda.synchronize()
     return (color.detach().cpu().numpy(), opacity.detach().cpu().numpy(), depth.detach().cpu().numpy(),
@@ -380,13 +382,15 @@ def grad_ok(got, ref, pk, comps=1):
     return np.abs(got - ref) <= 1e-3 * (np.abs(ref) + 1e-3 * ray_max[:, None])
 
 
-def run_render_parity(N, pk, t0, t1, sig, rgb, seed, eps=None, flat=True):
+def run_render_parity(N, pk, t0, t1, sig, rgb, seed, eps=None, flat=True, color_only=False):
     rng = np.random.default_rng(seed)
     n = len(pk)
     gC, gO, gD = rng.normal(size=(n, 3)).astype(np.float32), rng.normal(size=n).astype(np.float32), \
         rng.normal(size=n).astype(np.float32)
+    if color_only:  # a colour loss only: the backward gets NULL opacity / depth gradients
+        gO, gD = np.zeros(n, np.float32), np.zeros(n, np.float32)
     L = math.inf if eps is None else -math.log(float(np.float32(eps)))
-    got = gpu_render(N, pk, t0, t1, sig, rgb, gC, gO, gD, eps, flat)
+    got = gpu_render(N, pk, t0, t1, sig, rgb, gC, None if color_only else gO, None if color_only else gD, eps, flat)
     ref = O.render_fwd(pk, t0, t1, sig, rgb, neg_log_eps=L)
     gs, grgb = O.render_bwd(pk, t0, t1, sig, rgb, gC, gO, gD, neg_log_eps=L)
     ok_rays = np.ones(n, bool)
@@ -407,6 +411,14 @@ def test_render_ragged(N, eps, flat):
     """flat = the ray-aligned-tile kernels (ray_id given); False = one warp per ray"""
     pk, t0, t1, _, sig, rgb = W.ragged_samples(2000, seed=3, long_rays=(0, 9, 1500, 1999), long_count=5000)
     run_render_parity(N, pk, t0, t1, sig, rgb, seed=4, eps=eps, flat=flat)
+
+
+@pytest.mark.parametrize("eps", [None, 1e-4])
+def test_render_color_only_backward(N, eps):
+    """colour loss only (opacity / depth unused): the backward skips the per-ray constants kernel
+    and reads g_C and the forward's colour sums directly (render.cu kColorOnly)"""
+    pk, t0, t1, _, sig, rgb = W.ragged_samples(2000, seed=23, long_rays=(0, 9, 1500, 1999), long_count=5000)
+    run_render_parity(N, pk, t0, t1, sig, rgb, seed=24, eps=eps, color_only=True)
 
 
 def test_render_flat_unaligned(N):
