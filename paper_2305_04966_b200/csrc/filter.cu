@@ -2,7 +2,7 @@
 // transmittance is below ε are dropped before the differentiable pass.
 // Per ray the kept set is a prefix (S_i never decreases; reading #9), so the
 // filter is a per-ray cut (sequential fp64 sum, early exit) + exclusive scan of
-// the cuts + a compacting copy (three kernels, no host sync).
+// the cuts + a compacting copy (two kernels after a memset, no host sync).
 #include "common.cuh"
 #include "debug.cuh"
 
@@ -37,12 +37,19 @@ constexpr int kCutBatch = NACC_FILTER_BATCH;
 #define NACC_FILTER_SECTOR 1  // build parameter: sector-aligned walk when the arrays are 32-byte aligned
 #endif
 
+// a warp's cut total into its 256-ray group sum and into the sum of the group's 32-group super
+// group (block_sums + nb), from which the copy kernel forms every group's offset directly
+__device__ __forceinline__ void add_group_sum(int64_t *block_sums, int64_t nb, int64_t g, int64_t v) {
+  atomicAdd(reinterpret_cast<unsigned long long *>(block_sums + g), (unsigned long long)v);
+  atomicAdd(reinterpret_cast<unsigned long long *>(block_sums + nb + (g >> 5)), (unsigned long long)v);
+}
+
 __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *__restrict__ packed_info, int64_t n_rays,
                                                                  const float *__restrict__ t0,
                                                                  const float *__restrict__ t1,
                                                                  const float *__restrict__ sigma, int64_t n_samples,
                                                                  double L, int32_t *__restrict__ cut_out,
-                                                                 int64_t *__restrict__ block_sums) {
+                                                                 int64_t *__restrict__ block_sums, int64_t nb) {
   const int64_t r = (int64_t)blockIdx.x * kCutThreads + threadIdx.x;
   int64_t cut = 0;
   if (r < n_rays) {
@@ -81,7 +88,7 @@ __global__ void __launch_bounds__(kCutThreads) filter_cut_kernel(const int64_t *
   const int64_t tot = warp_sum_i64(cut);
   const int64_t r_warp = r - (threadIdx.x & 31);
   if ((threadIdx.x & 31) == 0 && tot)
-    atomicAdd(reinterpret_cast<unsigned long long *>(block_sums + r_warp / kFiltRays), (unsigned long long)tot);
+    add_group_sum(block_sums, nb, r_warp / kFiltRays, tot);
 }
 
 // Pass 1, sector-aligned variant: the walk reads whole 32-byte sectors (8 floats, two
@@ -119,7 +126,7 @@ __device__ __forceinline__ void load_sector(Sector &v, const float *__restrict__
 __global__ void __launch_bounds__(kCutThreads, NACC_FILTER_MINB) filter_cut_sector_kernel(
     const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
     const float *__restrict__ t1, const float *__restrict__ sigma, int64_t n_samples, double L,
-    int32_t *__restrict__ cut_out, int64_t *__restrict__ block_sums) {
+    int32_t *__restrict__ cut_out, int64_t *__restrict__ block_sums, int64_t nb) {
   const int64_t r = (int64_t)blockIdx.x * kCutThreads + threadIdx.x;
   int64_t cut = 0;
   if (r < n_rays) {
@@ -156,43 +163,18 @@ __global__ void __launch_bounds__(kCutThreads, NACC_FILTER_MINB) filter_cut_sect
   const int64_t tot = warp_sum_i64(cut);
   const int64_t r_warp = r - (threadIdx.x & 31);
   if ((threadIdx.x & 31) == 0 && tot)
-    atomicAdd(reinterpret_cast<unsigned long long *>(block_sums + r_warp / kFiltRays), (unsigned long long)tot);
+    add_group_sum(block_sums, nb, r_warp / kFiltRays, tot);
 }
 
-// Pass 2 (one block): exclusive scan of the block sums in place; *total.
-__global__ void __launch_bounds__(1024) block_sums_scan_kernel(int64_t *__restrict__ sums, int64_t nb,
-                                                               int64_t *__restrict__ total) {
-  __shared__ int64_t sm[33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t carry = 0;
-  for (int64_t base = 0; base < nb; base += 1024) {
-    const int64_t i = base + threadIdx.x;
-    const int64_t v = i < nb ? sums[i] : 0;
-    const int64_t incl = warp_incl_scan_i64(v);
-    if (lane == 31) sm[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const int64_t w = sm[lane];
-      const int64_t wi = warp_incl_scan_i64(w);
-      sm[lane] = wi - w;
-      if (lane == 31) sm[32] = wi;
-    }
-    __syncthreads();
-    if (i < nb) sums[i] = carry + sm[warp] + incl - v;
-    carry += sm[32];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *total = carry;
-}
-
-// Pass 3: blocks of 256 consecutive rays scan their cuts (+ the block offset)
+// Pass 2: blocks of 256 consecutive rays scan their cuts (+ the group's offset, from the group and
+// super-group sums of pass 1; block 0 writes the total)
 // into packed_info', then copy the kept prefixes, which are contiguous in the
 // output; each thread locates its ray by binary search over the block's output
 // starts in shared memory, so stores are coalesced.
 __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
     const int64_t *__restrict__ packed_info, int64_t n_rays, const float *__restrict__ t0,
     const float *__restrict__ t1, const int32_t *__restrict__ cuts, const int64_t *__restrict__ block_off,
-    const int64_t *__restrict__ total, int64_t capacity, int64_t *__restrict__ packed_out,
+    int64_t nb, int64_t *__restrict__ total, int64_t capacity, int64_t *__restrict__ packed_out,
     float *__restrict__ t0_out, float *__restrict__ t1_out, int32_t *__restrict__ ray_id_out, int vec) {
   __shared__ int64_t s_out[kFiltRays + 1];
   __shared__ int64_t s_in[kFiltRays];
@@ -200,11 +182,31 @@ __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
   const int64_t r0 = (int64_t)blockIdx.x * kFiltRays;
   const int nr = (int)min((int64_t)kFiltRays, n_rays - r0);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ int64_t s_pre[2];  // this group's output offset, the grand total
+  if (warp == 0) {
+    // offset = the super groups before this one + the groups before this one in its super group
+    const int64_t b = blockIdx.x, sb = b >> 5, nsb = (nb + 31) >> 5;
+    int64_t pre = 0, tot = 0;
+    for (int64_t k = lane; k < nsb; k += 32) {
+      const int64_t v = block_off[nb + k];
+      tot += v;
+      if (k < sb) pre += v;
+    }
+    const int64_t gq = (sb << 5) + lane;
+    if (gq < b) pre += block_off[gq];
+    pre = warp_sum_i64(pre);
+    tot = warp_sum_i64(tot);
+    if (lane == 0) {
+      s_pre[0] = pre;
+      s_pre[1] = tot;
+      if (b == 0) *total = tot;
+    }
+  }
   const int64_t c = t < nr ? (int64_t)cuts[r0 + t] : 0;
   const int64_t incl = warp_incl_scan_i64(c);
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
-  int64_t wbase = block_off[blockIdx.x];
+  int64_t wbase = s_pre[0];
   for (int w = 0; w < warp; ++w) wbase += s_w[w];
   const int64_t out = wbase + incl - c;
   if (t < nr) {
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kFiltRays) filter_copy_kernel(
     if (t == nr - 1) s_out[nr] = out + c;
   }
   __syncthreads();
-  if (t0_out == nullptr || *total > capacity) return;
+  if (t0_out == nullptr || s_pre[1] > capacity) return;
   const int64_t p0 = s_out[0], p1 = s_out[nr];
   // four consecutive outputs per thread: one binary search, then a forward walk; the
   // stores of a full aligned quad are float4 / int4
@@ -265,7 +267,8 @@ static size_t filter_ws_layout(int64_t n, int32_t **cuts, int64_t **bsums, void 
     *cuts = static_cast<int32_t *>(base);
     *bsums = reinterpret_cast<int64_t *>(static_cast<char *>(base) + a);
   }
-  return a + align_up(8 * (size_t)ceil_div(n, kFiltRays), 256);
+  const int64_t nb = ceil_div(n, kFiltRays);
+  return a + align_up(8 * (size_t)(nb + ceil_div(nb, 32)), 256);  // group sums, then super-group sums
 }
 
 }  // namespace nacc
@@ -304,21 +307,19 @@ nacc_status nacc_filter_early_stop(const int64_t *packed_info, int64_t n_rays, c
   int64_t *bsums;
   filter_ws_layout(n_rays, &cuts, &bsums, ws);
   const int64_t nb = ceil_div(n_rays, kFiltRays);
-  NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)nb, stream));
+  NACC_CUDA(cudaMemsetAsync(bsums, 0, 8 * (size_t)(nb + ceil_div(nb, 32)), stream));
   if (NACC_FILTER_SECTOR && aligned(t0, 32) && aligned(t1, 32) && aligned(sigma, 32))
     filter_cut_sector_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
+        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums, nb);
   else
     filter_cut_kernel<<<(unsigned)ceil_div(n_rays, kCutThreads), kCutThreads, 0, stream>>>(
-        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums);
-  block_sums_scan_kernel<<<1, 1024, 0, stream>>>(bsums, nb, total);
-  filter_copy_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, cuts, bsums, total, capacity,
+        packed_info, n_rays, t0, t1, sigma, n_samples, neg_log_eps, cuts, bsums, nb);
+  filter_copy_kernel<<<(unsigned)nb, kFiltRays, 0, stream>>>(packed_info, n_rays, t0, t1, cuts, bsums, nb, total, capacity,
                                                              packed_info_out, capacity > 0 ? t0_out : nullptr, t1_out,
                                                              ray_id_out,
                                                              aligned(t0_out, 16) && aligned(t1_out, 16) &&
                                                                  aligned(ray_id_out, 16));
   count_launch(2);
-  count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;
 }
