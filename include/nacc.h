@@ -90,7 +90,9 @@ typedef struct {
 /* Bytes of the bitfield buffer for `grid` (0 if invalid): the public fine bits
  * (4*ceil(levels*res^3/32) bytes, rounded up to 256) followed by a
  * library-private region: a 256-byte header (the boxes enclosing the occupied
- * cells) and a skip mask (1 bit per 4^3 macro cell, when res % 4 == 0). */
+ * cells), a skip mask (1 bit per 4^3 macro cell, when res % 4 == 0) and, with
+ * it, the OR / AND window masks of w^3 fine cells (1 bit per fine cell each)
+ * for w = 2..9 on cascades (levels > 1) and w = 2..5 on a single level. */
 size_t nacc_grid_bits_bytes(const nacc_grid *grid);
 
 /* Rebuild the private region of `bits` (occupied-cell boxes, skip mask) from
@@ -232,7 +234,8 @@ nacc_status nacc_render_fwd(const int64_t *packed_info, const int32_t *ray_id, i
  * g_sigma [N] and g_rgb [N][3].  ctx from the forward (NULL = recompute, one
  * warp per ray); with ray_id and ctx the flat kernel runs and needs a
  * workspace of nacc_render_bwd_workspace_bytes(n_rays) bytes (per-ray
- * gradient constants). */
+ * gradient constants; unused when g_opacity and g_depth are both NULL, a
+ * colour-only loss, whose constants the kernel forms itself). */
 size_t nacc_render_bwd_workspace_bytes(int64_t n_rays);
 nacc_status nacc_render_bwd(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
                             const float *t0,
