@@ -174,6 +174,16 @@ nacc_status nacc_render_weights_fwd(const int64_t *packed_info, int64_t n_rays, 
                                     const float *t1, const float *sigma, int64_t n_samples,
                                     double neg_log_eps, float *weights, float *trans,
                                     float *alphas, cudaStream_t stream);
+/* The same outputs on ray-aligned flat tiles (the fused forward's layout: fp64
+ * warp segmented scans, float4 runs), for packed samples from the sampling
+ * calls: needs ray_id [n_samples] and the contiguous packing (start_0 = 0,
+ * start_{r+1} = start_r + count_r).  Same arithmetic as nacc_render_weights_fwd
+ * up to summation order (T by the product T_{j+1} = T_j e^{-s_j}). */
+nacc_status nacc_render_weights_fwd_flat(const int64_t *packed_info, const int32_t *ray_id,
+                                         int64_t n_rays, const float *t0, const float *t1,
+                                         const float *sigma, int64_t n_samples, double neg_log_eps,
+                                         float *weights, float *trans, float *alphas,
+                                         cudaStream_t stream);
 /* g_sigma_i = δ_i (g_w_i T_i (1-α_i)[live] - Σ_{j>i} g_w_j w_j - Σ_{j>i} g_T_j T_j);
  * g_trans may be NULL (= 0). */
 nacc_status nacc_render_weights_bwd(const int64_t *packed_info, int64_t n_rays, const float *t0,

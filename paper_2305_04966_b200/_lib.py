@@ -61,6 +61,7 @@ SIGNATURES = {
     "nacc_filter_workspace_bytes": (SZ, [I64]),
     "nacc_filter_early_stop": (C.c_int, [P, I64, P, P, P, I64, D, P, P, P, P, I64, P, P, SZ, P]),
     "nacc_render_weights_fwd": (C.c_int, [P, I64, P, P, P, I64, D, P, P, P, P]),
+    "nacc_render_weights_fwd_flat": (C.c_int, [P, P, I64, P, P, P, I64, D, P, P, P, P]),
     "nacc_render_weights_bwd": (C.c_int, [P, I64, P, P, P, I64, D, P, P, P, P]),
     "nacc_render_weights_alpha_fwd": (C.c_int, [P, I64, P, I64, D, P, P, P]),
     "nacc_render_weights_alpha_bwd_workspace_bytes": (SZ, [I64]),

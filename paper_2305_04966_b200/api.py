@@ -290,13 +290,18 @@ def render_bwd(samples: PackedSamples, sigma: torch.Tensor, rgb: torch.Tensor, c
 
 class _WeightsFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, packed_info, t0, t1, sigma, nle):
+    def forward(ctx, packed_info, t0, t1, sigma, nle, ray_id):
         n, N = packed_info.shape[0], t0.numel()
         w = torch.empty_like(sigma)
         T = torch.empty_like(sigma)
         a = torch.empty_like(sigma)
-        check(L.lib().nacc_render_weights_fwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, nle,
-                                              _ptr(w), _ptr(T), _ptr(a), _stream()), "nacc_render_weights_fwd")
+        if ray_id is not None:  # samples from the sampling calls: the flat-tile kernel
+            check(L.lib().nacc_render_weights_fwd_flat(_ptr(packed_info), _ptr(ray_id), n, _ptr(t0), _ptr(t1),
+                                                       _ptr(sigma), N, nle, _ptr(w), _ptr(T), _ptr(a), _stream()),
+                  "nacc_render_weights_fwd_flat")
+        else:
+            check(L.lib().nacc_render_weights_fwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, nle,
+                                                  _ptr(w), _ptr(T), _ptr(a), _stream()), "nacc_render_weights_fwd")
         ctx.save_for_backward(packed_info, t0, t1, sigma)
         ctx.nle = nle
         ctx.mark_non_differentiable(a)
@@ -312,13 +317,16 @@ class _WeightsFn(torch.autograd.Function):
         check(L.lib().nacc_render_weights_bwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, ctx.nle,
                                               _ptr(gw), _ptr(gT), _ptr(g_sigma), _stream()),
               "nacc_render_weights_bwd")
-        return None, None, None, g_sigma, None
+        return None, None, None, g_sigma, None, None
 
 
 def render_weights(samples: PackedSamples, sigma: torch.Tensor, eps: Optional[float] = None):
-    """Transmittance estimator (Eq. 2): returns (weights, trans, alphas) per sample."""
+    """Transmittance estimator (Eq. 2): returns (weights, trans, alphas) per sample.  Samples
+    carrying ray_id (the sampling calls' output: contiguous packing) take the flat-tile forward;
+    a PackedSamples with an empty ray_id takes the one-warp-per-ray kernel (any packing)."""
     sigma = _req(sigma, torch.float32, "sigma", samples.n_samples)
-    return _WeightsFn.apply(samples.packed_info, samples.t0, samples.t1, sigma, neg_log_eps(eps))
+    rid = samples.ray_id if samples.ray_id is not None and samples.ray_id.numel() == samples.n_samples else None
+    return _WeightsFn.apply(samples.packed_info, samples.t0, samples.t1, sigma, neg_log_eps(eps), rid)
 
 
 class _AlphaWeightsFn(torch.autograd.Function):

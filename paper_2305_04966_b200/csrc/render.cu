@@ -567,6 +567,59 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) render_fwd_warp_kernel(
   }
 }
 
+// Granular weights (render_weights) on the same ray-aligned warp tiles as the fused forward:
+// the fp64 segmented scan of σδ gives each item's entering S, T by the product chain from one
+// e^{-S} per thread, α = 1 - e^{-s}, w = T α (0 past the early stop); 12 B/sample out as float4
+// runs.  Needs ray_id and the contiguous packing (nacc_render_weights_fwd_flat).
+template <bool kVec>
+__global__ void __launch_bounds__(256, NACC_RENDER_BPS) weights_fwd_warp_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
+    const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma, double L,
+    float *__restrict__ weights, float *__restrict__ trans, float *__restrict__ alphas) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t N = min(packed_end(packed_info, n_rays), n_samples);
+  for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
+    const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+    const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+    if (B >= E) continue;
+    Seg<1> carryS = seg_identity<1>();
+    int32_t carry_rid = -1;
+    for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+      Items it;
+      load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
+      double s[4], S[4];
+      warp_items_S(it, s, S, carryS);
+      float wv[4], tv[4], av[4];
+      double Tn = trans_first(S[0]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double ea = interval_ea(s[j]);
+        const double T = (j > 0 && it.head[j]) ? 1.0 : Tn;
+        Tn = T * ea;
+        const double a = 1.0 - ea;
+        const bool live = it.valid[j] && !(S[j] > L);
+        wv[j] = live ? (float)(T * a) : 0.f;
+        tv[j] = (float)T;
+        av[j] = (float)a;
+      }
+      if (kVec && it.valid[0] && it.valid[3]) {
+        *reinterpret_cast<float4 *>(weights + it.q0) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+        if (trans) *reinterpret_cast<float4 *>(trans + it.q0) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+        if (alphas) *reinterpret_cast<float4 *>(alphas + it.q0) = make_float4(av[0], av[1], av[2], av[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!it.valid[j]) continue;
+          weights[it.q0 + j] = wv[j];
+          if (trans) trans[it.q0 + j] = tv[j];
+          if (alphas) alphas[it.q0 + j] = av[j];
+        }
+      }
+    }
+  }
+}
+
 // persistent grid for the tile kernels: all resident at once (3 blocks of 256 per SM)
 static unsigned resident_blocks(int64_t want) {
   static int n_sm = 0;
@@ -1109,6 +1162,33 @@ nacc_status nacc_render_weights_bwd(const int64_t *packed_info, int64_t n_rays, 
   NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
   weights_bwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma,
                                                                       neg_log_eps, g_weights, g_trans, g_sigma);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+nacc_status nacc_render_weights_fwd_flat(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
+                                         const float *t0, const float *t1, const float *sigma, int64_t n_samples,
+                                         double neg_log_eps, float *weights, float *trans, float *alphas,
+                                         cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_packed(packed_info, n_rays, n_samples);
+  if (s != NACC_OK) return s;
+  NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
+  if (n_rays == 0 || n_samples == 0) return NACC_OK;
+  NACC_REQUIRE(ray_id && t0 && t1 && sigma && weights, "ray_id, t0, t1, sigma, weights must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
+  const int64_t n_wtiles = ceil_div(n_samples, kWarpTile);
+  const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(ray_id, 16) &&
+                   aligned(weights, 16) && (!trans || aligned(trans, 16)) && (!alphas || aligned(alphas, 16));
+  const unsigned blocks = resident_blocks(ceil_div(n_wtiles * 32, 256));
+  if (vec)
+    weights_fwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
+                                                              neg_log_eps, weights, trans, alphas);
+  else
+    weights_fwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
+                                                               neg_log_eps, weights, trans, alphas);
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;

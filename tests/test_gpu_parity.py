@@ -479,9 +479,11 @@ def test_weights_and_accumulate(N):
     import torch
 
     pk, t0, t1, _, sig, rgb = W.ragged_samples(1500, seed=8, long_rays=(3,))
-    for eps in (None, 1e-4):
+    # flat = ray_id given (the flat-tile forward); else an empty ray_id (one warp per ray)
+    for eps, flat in ((None, True), (1e-4, True), (None, False), (1e-4, False)):
         L = math.inf if eps is None else -math.log(float(np.float32(eps)))
-        s = N.PackedSamples(cuda(pk), cuda(t0), cuda(t1), cuda(np.zeros(len(t0), np.int32)))
+        rid = cuda(ray_ids(pk)) if flat else cuda(np.zeros(0, np.int32))
+        s = N.PackedSamples(cuda(pk), cuda(t0), cuda(t1), rid)
         sg = cuda(sig).requires_grad_()
         w, T, a = N.render_weights(s, sg, eps=eps)
         ref = O.render_fwd(pk, t0, t1, sig, None, neg_log_eps=L)

@@ -39,3 +39,9 @@ def timed(fn, n=40, batches=7):
 ms_f, (col, _, _, cx) = timed(lambda: N.render_fwd(S, sg, rgb, 1e-4))
 ms_b, _ = timed(lambda: N.render_bwd(S, sg, rgb, cx, g, None, None, 1e-4))
 print(f"samples {len(a0)} render fwd {ms_f * 1e3:.1f} us bwd {ms_b * 1e3:.1f} us")
+# granular render_weights forward: flat tiles (ray_id given) vs one warp per ray (empty ray_id)
+with torch.no_grad():
+    S0 = N.PackedSamples(S.packed_info, S.t0, S.t1, torch.zeros(0, dtype=torch.int32, device="cuda"))
+    ms_wf, _ = timed(lambda: N.render_weights(S, sg, 1e-4))
+    ms_ww, _ = timed(lambda: N.render_weights(S0, sg, 1e-4))
+print(f"render_weights fwd flat {ms_wf * 1e3:.1f} us, warp per ray {ms_ww * 1e3:.1f} us")
