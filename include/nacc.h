@@ -216,12 +216,26 @@ nacc_status nacc_render_weights_alpha_bwd(const int64_t *packed_info, int64_t n_
 nacc_status nacc_accumulate_along_rays(const int64_t *packed_info, int64_t n_rays,
                                        const float *weights, const float *values, int32_t C,
                                        int64_t n_samples, float *out, cudaStream_t stream);
+/* The same sums on ray-aligned flat tiles (fp64 lane sums and warp segmented
+ * scans) for packed samples from the sampling calls: needs ray_id [n_samples]
+ * and the contiguous packing; C > 4 runs the one-warp-per-ray kernel. */
+nacc_status nacc_accumulate_along_rays_flat(const int64_t *packed_info, const int32_t *ray_id,
+                                            int64_t n_rays, const float *weights,
+                                            const float *values, int32_t C, int64_t n_samples,
+                                            float *out, cudaStream_t stream);
 /* g_weights_i = Σ_c g_out[r][c] v_i[c]; g_values_i = w_i g_out[r] (NULL = skip). */
 nacc_status nacc_accumulate_along_rays_bwd(const int64_t *packed_info, int64_t n_rays,
                                            const float *weights, const float *values, int32_t C,
                                            int64_t n_samples, const float *g_out,
                                            float *g_weights, float *g_values,
                                            cudaStream_t stream);
+/* The same gradients, one thread per sample with its ray from ray_id [n_samples]
+ * (any packing; ray_id must be the packed tensor's ray of every sample). */
+nacc_status nacc_accumulate_along_rays_bwd_flat(const int32_t *ray_id, int64_t n_rays,
+                                                const float *weights, const float *values,
+                                                int32_t C, int64_t n_samples, const float *g_out,
+                                                float *g_weights, float *g_values,
+                                                cudaStream_t stream);
 
 /* Fused render (Alg. 1 nerfacc.rendering(t0, t1, r_id, ...)).  On the
  * flat path n_samples is the arrays' length (a capacity); the samples in use

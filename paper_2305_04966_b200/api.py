@@ -365,39 +365,53 @@ def render_weights_alpha(samples: PackedSamples, alphas: torch.Tensor, eps: Opti
 
 class _AccumFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, packed_info, weights, values, C_):
+    def forward(ctx, packed_info, weights, values, C_, ray_id):
         n, N = packed_info.shape[0], weights.numel()
         out = torch.empty((n, C_), dtype=torch.float32, device=weights.device)
-        check(L.lib().nacc_accumulate_along_rays(_ptr(packed_info), n, _ptr(weights), _ptr(values), C_, N, _ptr(out),
-                                                 _stream()), "nacc_accumulate_along_rays")
-        ctx.save_for_backward(packed_info, weights, values)
+        if ray_id is not None:  # samples from the sampling calls: the flat-tile kernel
+            check(L.lib().nacc_accumulate_along_rays_flat(_ptr(packed_info), _ptr(ray_id), n, _ptr(weights),
+                                                          _ptr(values), C_, N, _ptr(out), _stream()),
+                  "nacc_accumulate_along_rays_flat")
+        else:
+            check(L.lib().nacc_accumulate_along_rays(_ptr(packed_info), n, _ptr(weights), _ptr(values), C_, N,
+                                                     _ptr(out), _stream()), "nacc_accumulate_along_rays")
+        ctx.save_for_backward(packed_info, weights, values, ray_id)
         ctx.C = C_
         ctx.has_values = values is not None
         return out
 
     @staticmethod
     def backward(ctx, g_out):
-        packed_info, weights, values = ctx.saved_tensors
+        packed_info, weights, values, ray_id = ctx.saved_tensors
         n, N = packed_info.shape[0], weights.numel()
         g_w = torch.empty_like(weights)
         g_v = torch.empty_like(values) if ctx.has_values else None
         g_out = g_out.contiguous().float()
-        check(L.lib().nacc_accumulate_along_rays_bwd(_ptr(packed_info), n, _ptr(weights),
-                                                     _ptr(values if ctx.has_values else None), ctx.C, N,
-                                                     _ptr(g_out), _ptr(g_w), _ptr(g_v), _stream()),
-              "nacc_accumulate_along_rays_bwd")
-        return None, g_w, g_v, None
+        if ray_id is not None:  # one thread per sample
+            check(L.lib().nacc_accumulate_along_rays_bwd_flat(_ptr(ray_id), n, _ptr(weights),
+                                                              _ptr(values if ctx.has_values else None), ctx.C, N,
+                                                              _ptr(g_out), _ptr(g_w), _ptr(g_v), _stream()),
+                  "nacc_accumulate_along_rays_bwd_flat")
+        else:
+            check(L.lib().nacc_accumulate_along_rays_bwd(_ptr(packed_info), n, _ptr(weights),
+                                                         _ptr(values if ctx.has_values else None), ctx.C, N,
+                                                         _ptr(g_out), _ptr(g_w), _ptr(g_v), _stream()),
+                  "nacc_accumulate_along_rays_bwd")
+        return None, g_w, g_v, None, None
 
 
 def accumulate_along_rays(samples: PackedSamples, weights: torch.Tensor, values: Optional[torch.Tensor] = None):
-    """Segmented sums out[r] = Σ_i w_i v_i (values None = ones, i.e. opacity)."""
+    """Segmented sums out[r] = Σ_i w_i v_i (values None = ones, i.e. opacity).  Samples carrying
+    ray_id (the sampling calls' output: contiguous packing) take the flat-tile kernels; an empty
+    ray_id takes the one-warp-per-ray kernels (any packing)."""
     N = samples.n_samples
     weights = _req(weights, torch.float32, "weights", N)
+    rid = samples.ray_id if samples.ray_id is not None and samples.ray_id.numel() == N and N else None
     if values is None:
-        return _AccumFn.apply(samples.packed_info, weights, None, 1)
+        return _AccumFn.apply(samples.packed_info, weights, None, 1, rid)
     values = _req(values, torch.float32, "values")
     C_ = values.numel() // max(N, 1) if N else (values.shape[-1] if values.dim() > 1 else 1)
-    return _AccumFn.apply(samples.packed_info, weights, values.view(N, C_) if N else values, C_)
+    return _AccumFn.apply(samples.packed_info, weights, values.view(N, C_) if N else values, C_, rid)
 
 
 # ----------------------------------------------------------------------------- proposal resampling

@@ -620,6 +620,104 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) weights_fwd_warp_kernel(
   }
 }
 
+// accumulate_along_rays on the ray-aligned flat tiles (kC = 1..4 channels): lane-sequential fp64
+// sums of w v over 4 consecutive samples, rays written at their tails when their head is in the
+// lane, the leading run through the fp64 warp segmented scan (Seg<kC>).  Needs ray_id and the
+// contiguous packing (nacc_accumulate_along_rays_flat).
+template <int kC>
+__global__ void __launch_bounds__(256, NACC_RENDER_BPS) accumulate_warp_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
+    const float *__restrict__ weights, const float *__restrict__ values, float *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = gw * 32 + lane; r < n_rays; r += nw * 32)  // rays without samples
+    if (packed_info[2 * r + 1] == 0)
+#pragma unroll
+      for (int c = 0; c < kC; ++c) out[r * kC + c] = 0.f;
+  const int64_t N = min(packed_end(packed_info, n_rays), n_samples);
+  for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
+    const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+    const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+    if (B >= E) continue;
+    Seg<kC> carry = seg_identity<kC>();
+    int32_t carry_rid = -1;
+    for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+      const int64_t q0 = c0 + (int64_t)lane * 4;
+      bool valid[4], head[4], tail[4];
+      int32_t rid[4];
+      float w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t q = q0 + j;
+        valid[j] = q >= B && q < E;
+        w[j] = valid[j] ? __ldg(weights + q) : 0.f;
+        rid[j] = valid[j] ? __ldg(ray_id + q) : -1;
+      }
+      int32_t prev = __shfl_up_sync(kFull, rid[3], 1);
+      if (lane == 0) prev = carry_rid;
+      int32_t next = __shfl_down_sync(kFull, rid[0], 1);
+      if (lane == 31) next = (q0 + 4 < E) ? __ldg(ray_id + q0 + 4) : -2;
+      carry_rid = __shfl_sync(kFull, rid[3], 31);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int32_t pr = j == 0 ? prev : rid[j - 1];
+        const int32_t nx = j == 3 ? next : (valid[j + 1] ? rid[j + 1] : -2);
+        head[j] = valid[j] && (q0 + j == B || rid[j] != pr);
+        tail[j] = valid[j] && (q0 + j + 1 == E || rid[j] != nx);
+      }
+      Seg<kC> cur = seg_identity<kC>(), lead;
+      int32_t lead_r = -1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        Seg<kC> x;
+        x.f = head[j];
+#pragma unroll
+        for (int c = 0; c < kC; ++c)
+          x.v[c] = valid[j] ? (double)w[j] * (values ? (double)__ldg(values + (q0 + j) * kC + c) : 1.0) : 0.0;
+        cur = seg_combine(cur, x);
+        if (tail[j]) {
+          if (cur.f) {
+#pragma unroll
+            for (int c = 0; c < kC; ++c) out[(int64_t)rid[j] * kC + c] = (float)cur.v[c];
+          } else {
+            lead = cur;
+            lead_r = rid[j];
+          }
+        }
+      }
+      const Seg<kC> enter = warp_seg_excl<kC>(cur, carry);
+      if (lead_r >= 0) {
+        const Seg<kC> t = seg_combine(enter, lead);
+#pragma unroll
+        for (int c = 0; c < kC; ++c) out[(int64_t)lead_r * kC + c] = (float)t.v[c];
+      }
+    }
+  }
+}
+
+// its backward needs no scan: g_w_i = Σ_c g_out[r_i][c] v_i[c], g_v_i = w_i g_out[r_i], one
+// thread per sample with the sample's ray from ray_id
+__global__ void __launch_bounds__(256) accumulate_bwd_flat_kernel(const int32_t *__restrict__ ray_id,
+                                                                  int64_t n_samples, const float *__restrict__ weights,
+                                                                  const float *__restrict__ values, int C,
+                                                                  const float *__restrict__ g_out,
+                                                                  float *__restrict__ g_weights,
+                                                                  float *__restrict__ g_values) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n_samples;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = __ldg(ray_id + q);
+    const float w = __ldg(weights + q);
+    double gw = 0.0;
+    for (int c = 0; c < C; ++c) {
+      const float g = __ldg(g_out + r * C + c);
+      gw += (double)g * (values ? (double)__ldg(values + q * C + c) : 1.0);
+      if (g_values) g_values[q * C + c] = w * g;
+    }
+    if (g_weights) g_weights[q] = (float)gw;
+  }
+}
+
 // persistent grid for the tile kernels: all resident at once (3 blocks of 256 per SM)
 static unsigned resident_blocks(int64_t want) {
   static int n_sm = 0;
@@ -1261,6 +1359,49 @@ nacc_status nacc_accumulate_along_rays(const int64_t *packed_info, int64_t n_ray
     case 4: accumulate_kernel<4><<<blocks, 256, 0, stream>>>(packed_info, n_rays, weights, values, C, out); break;
     default: accumulate_kernel<0><<<blocks, 256, 0, stream>>>(packed_info, n_rays, weights, values, C, out); break;
   }
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+nacc_status nacc_accumulate_along_rays_flat(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
+                                            const float *weights, const float *values, int32_t C, int64_t n_samples,
+                                            float *out, cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_packed(packed_info, n_rays, n_samples);
+  if (s != NACC_OK) return s;
+  NACC_REQUIRE(C >= 1 && C <= 64, "C must be in 1..64");
+  NACC_REQUIRE(values || C == 1, "values == NULL requires C == 1");
+  if (n_rays == 0) return NACC_OK;
+  NACC_REQUIRE(out && (n_samples == 0 || (weights && ray_id)), "weights, ray_id and out must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, nullptr, nullptr, n_samples, stream));
+  if (C > 4 || n_samples == 0) return nacc_accumulate_along_rays(packed_info, n_rays, weights, values, C, n_samples,
+                                                                 out, stream);
+  const unsigned blocks = resident_blocks(std::max(ceil_div(n_samples, kWarpTile), ceil_div(n_rays, 32)) * 32 / 256 + 1);
+  switch (C) {
+    case 1: accumulate_warp_kernel<1><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, weights, values, out); break;
+    case 2: accumulate_warp_kernel<2><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, weights, values, out); break;
+    case 3: accumulate_warp_kernel<3><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, weights, values, out); break;
+    default: accumulate_warp_kernel<4><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, weights, values, out); break;
+  }
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+nacc_status nacc_accumulate_along_rays_bwd_flat(const int32_t *ray_id, int64_t n_rays, const float *weights,
+                                                const float *values, int32_t C, int64_t n_samples,
+                                                const float *g_out, float *g_weights, float *g_values,
+                                                cudaStream_t stream) {
+  clear_error();
+  NACC_REQUIRE(n_rays >= 0 && n_rays < (1ll << 31) && n_samples >= 0, "sizes must be >= 0 (n_rays < 2^31)");
+  NACC_REQUIRE(C >= 1 && C <= 64, "C must be in 1..64");
+  NACC_REQUIRE(values || (C == 1 && !g_values), "values == NULL requires C == 1 and g_values == NULL");
+  if (n_rays == 0 || n_samples == 0) return NACC_OK;
+  NACC_REQUIRE(ray_id && weights && g_out, "ray_id, weights and g_out must be non-NULL");
+  const int64_t blocks = std::min(ceil_div(n_samples, (int64_t)256), (int64_t)148 * 16);
+  accumulate_bwd_flat_kernel<<<(unsigned)blocks, 256, 0, stream>>>(ray_id, n_samples, weights, values, C, g_out,
+                                                                   g_weights, g_values);
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;

@@ -497,9 +497,10 @@ def test_weights_and_accumulate(N):
         (w * cuda(gw)).sum().add_((T * cuda(gT)).sum()).backward()
         gs = O.weights_bwd(pk, t0, t1, sig, gw, gT, neg_log_eps=L)
         assert np.all(grad_ok(sg.grad.cpu().numpy(), gs, pk)[ok])
-    # accumulate fwd/bwd with C = 1 (opacity), 3 (rgb) and 5
+    # accumulate fwd/bwd with C = 1 (opacity), 3 (rgb) and 5, flat (ray_id) and one warp per ray
     w = torch.rand(len(t0), device="cuda", requires_grad=True)
-    for C_ in (None, 3, 5):
+    s_flat = N.PackedSamples(cuda(pk), cuda(t0), cuda(t1), cuda(ray_ids(pk)))
+    for C_, s in [(c, sx) for sx in (s, s_flat) for c in (None, 2, 3, 4, 5)]:
         vals = None if C_ is None else torch.rand(len(t0), C_, device="cuda", requires_grad=True)
         out = N.accumulate_along_rays(s, w, vals)
         g = torch.randn_like(out)

@@ -45,3 +45,13 @@ with torch.no_grad():
     ms_wf, _ = timed(lambda: N.render_weights(S, sg, 1e-4))
     ms_ww, _ = timed(lambda: N.render_weights(S0, sg, 1e-4))
 print(f"render_weights fwd flat {ms_wf * 1e3:.1f} us, warp per ray {ms_ww * 1e3:.1f} us")
+# accumulate_along_rays (rgb, C = 3) forward + backward: flat vs one warp per ray
+wq = torch.rand(len(a0), device="cuda", requires_grad=True)
+vq = torch.rand(len(a0), 3, device="cuda", requires_grad=True)
+def acc(Sx):
+    o = N.accumulate_along_rays(Sx, wq, vq)
+    o.backward(torch.ones_like(o))
+    return o
+ms_af, _ = timed(lambda: acc(S))
+ms_aw, _ = timed(lambda: acc(S0))
+print(f"accumulate C=3 fwd+bwd (incl. autograd) flat {ms_af * 1e3:.1f} us, warp per ray {ms_aw * 1e3:.1f} us")
