@@ -201,6 +201,13 @@ nacc_status nacc_render_weights_alpha_fwd(const int64_t *packed_info, int64_t n_
                                           const float *alphas, int64_t n_samples,
                                           double neg_log_eps, float *weights, float *trans,
                                           cudaStream_t stream);
+/* The same on ray-aligned flat tiles (an fp64 segmented product scan of 1 - α)
+ * for packed samples from the sampling calls: needs ray_id [n_samples] and the
+ * contiguous packing. */
+nacc_status nacc_render_weights_alpha_fwd_flat(const int64_t *packed_info, const int32_t *ray_id,
+                                               int64_t n_rays, const float *alphas,
+                                               int64_t n_samples, double neg_log_eps,
+                                               float *weights, float *trans, cudaStream_t stream);
 /* Workspace for the alpha backward: 8 bytes per sample (fp64 T). */
 size_t nacc_render_weights_alpha_bwd_workspace_bytes(int64_t n_samples);
 /* g_α_k = [live_k] g_w_k T_k − T_k Λ_k,  Λ_k = Σ_{i>k} ([live_i] g_w_i α_i + g_T_i)

@@ -331,12 +331,17 @@ def render_weights(samples: PackedSamples, sigma: torch.Tensor, eps: Optional[fl
 
 class _AlphaWeightsFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, packed_info, alphas, nle):
+    def forward(ctx, packed_info, alphas, nle, ray_id):
         n, N = packed_info.shape[0], alphas.numel()
         w = torch.empty_like(alphas)
         T = torch.empty_like(alphas)
-        check(L.lib().nacc_render_weights_alpha_fwd(_ptr(packed_info), n, _ptr(alphas), N, nle, _ptr(w), _ptr(T),
-                                                    _stream()), "nacc_render_weights_alpha_fwd")
+        if ray_id is not None:  # samples from the sampling calls: the flat-tile kernel
+            check(L.lib().nacc_render_weights_alpha_fwd_flat(_ptr(packed_info), _ptr(ray_id), n, _ptr(alphas), N, nle,
+                                                             _ptr(w), _ptr(T), _stream()),
+                  "nacc_render_weights_alpha_fwd_flat")
+        else:
+            check(L.lib().nacc_render_weights_alpha_fwd(_ptr(packed_info), n, _ptr(alphas), N, nle, _ptr(w), _ptr(T),
+                                                        _stream()), "nacc_render_weights_alpha_fwd")
         ctx.save_for_backward(packed_info, alphas)
         ctx.nle = nle
         ctx.set_materialize_grads(False)
@@ -353,14 +358,16 @@ class _AlphaWeightsFn(torch.autograd.Function):
         check(L.lib().nacc_render_weights_alpha_bwd(_ptr(packed_info), n, _ptr(alphas), N, ctx.nle, _ptr(gw), _ptr(gT),
                                                     _ptr(g_a), _ptr(ws), ws.numel(), _stream()),
               "nacc_render_weights_alpha_bwd")
-        return None, g_a, None
+        return None, g_a, None, None
 
 
 def render_weights_alpha(samples: PackedSamples, alphas: torch.Tensor, eps: Optional[float] = None):
     """Alpha compositing for fields that return α per interval (SDF-based
     fields): returns (weights, trans), differentiable w.r.t. α."""
     alphas = _req(alphas, torch.float32, "alphas", samples.n_samples)
-    return _AlphaWeightsFn.apply(samples.packed_info, alphas, neg_log_eps(eps))
+    N = samples.n_samples
+    rid = samples.ray_id if samples.ray_id is not None and samples.ray_id.numel() == N and N else None
+    return _AlphaWeightsFn.apply(samples.packed_info, alphas, neg_log_eps(eps), rid)
 
 
 class _AccumFn(torch.autograd.Function):

@@ -718,6 +718,102 @@ __global__ void __launch_bounds__(256) accumulate_bwd_flat_kernel(const int32_t 
   }
 }
 
+// Alpha compositing forward on the ray-aligned flat tiles: an fp64 segmented exclusive product
+// scan of (1 - α) (lane-sequential over 4 samples, then across the warp with the chunk carry);
+// w = T α unless T < ε_T.  Needs ray_id and the contiguous packing.
+struct SegP {
+  int f;
+  double v;
+};
+__device__ __forceinline__ SegP segp_combine(const SegP &a, const SegP &b) {
+  return SegP{a.f | b.f, b.f ? b.v : a.v * b.v};
+}
+__device__ __forceinline__ SegP warp_segp_excl(const SegP &x, SegP &carry) {
+  const int lane = threadIdx.x & 31;
+  SegP incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    SegP y;
+    y.f = __shfl_up_sync(kFull, incl.f, o);
+    y.v = __shfl_up_sync(kFull, incl.v, o);
+    if (lane >= o) incl = segp_combine(y, incl);
+  }
+  SegP ex{__shfl_up_sync(kFull, incl.f, 1), __shfl_up_sync(kFull, incl.v, 1)};
+  if (lane == 0) ex = SegP{0, 1.0};
+  const SegP res = segp_combine(carry, ex);
+  carry = segp_combine(carry, SegP{__shfl_sync(kFull, incl.f, 31), __shfl_sync(kFull, incl.v, 31)});
+  return res;
+}
+
+template <bool kVec>
+__global__ void __launch_bounds__(256, NACC_RENDER_BPS) weights_alpha_fwd_warp_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
+    const float *__restrict__ alphas, double eps_T, float *__restrict__ weights, float *__restrict__ trans) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t N = min(packed_end(packed_info, n_rays), n_samples);
+  for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
+    const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+    const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+    if (B >= E) continue;
+    SegP carry{0, 1.0};
+    int32_t carry_rid = -1;
+    for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+      const int64_t q0 = c0 + (int64_t)lane * 4;
+      bool valid[4], head[4];
+      int32_t rid[4];
+      float a[4];
+      const bool full = kVec && q0 >= B && q0 + 3 < E;
+      if (full) {
+        const float4 av = __ldg(reinterpret_cast<const float4 *>(alphas + q0));
+        const int4 rv = __ldg(reinterpret_cast<const int4 *>(ray_id + q0));
+        a[0] = av.x; a[1] = av.y; a[2] = av.z; a[3] = av.w;
+        rid[0] = rv.x; rid[1] = rv.y; rid[2] = rv.z; rid[3] = rv.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) valid[j] = true;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int64_t q = q0 + j;
+          valid[j] = q >= B && q < E;
+          a[j] = valid[j] ? __ldg(alphas + q) : 0.f;
+          rid[j] = valid[j] ? __ldg(ray_id + q) : -1;
+        }
+      }
+      int32_t prev = __shfl_up_sync(kFull, rid[3], 1);
+      if (lane == 0) prev = carry_rid;
+      carry_rid = __shfl_sync(kFull, rid[3], 31);
+      SegP agg{0, 1.0};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        head[j] = valid[j] && (q0 + j == B || rid[j] != (j == 0 ? prev : rid[j - 1]));
+        agg = segp_combine(agg, SegP{head[j], 1.0 - (double)a[j]});
+      }
+      SegP run = warp_segp_excl(agg, carry);
+      float wv[4], tv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double T = head[j] ? 1.0 : run.v;
+        run.v = T * (1.0 - (double)a[j]);
+        wv[j] = !(T < eps_T) ? (float)(T * (double)a[j]) : 0.f;
+        tv[j] = (float)T;
+      }
+      if (full) {
+        *reinterpret_cast<float4 *>(weights + q0) = make_float4(wv[0], wv[1], wv[2], wv[3]);
+        if (trans) *reinterpret_cast<float4 *>(trans + q0) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!valid[j]) continue;
+          weights[q0 + j] = wv[j];
+          if (trans) trans[q0 + j] = tv[j];
+        }
+      }
+    }
+  }
+}
+
 // persistent grid for the tile kernels: all resident at once (3 blocks of 256 per SM)
 static unsigned resident_blocks(int64_t want) {
   static int n_sm = 0;
@@ -1287,6 +1383,30 @@ nacc_status nacc_render_weights_fwd_flat(const int64_t *packed_info, const int32
   else
     weights_fwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
                                                                neg_log_eps, weights, trans, alphas);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+nacc_status nacc_render_weights_alpha_fwd_flat(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
+                                               const float *alphas, int64_t n_samples, double neg_log_eps,
+                                               float *weights, float *trans, cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_packed(packed_info, n_rays, n_samples);
+  if (s != NACC_OK) return s;
+  NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
+  if (n_rays == 0 || n_samples == 0) return NACC_OK;
+  NACC_REQUIRE(ray_id && alphas && weights, "ray_id, alphas and weights must be non-NULL");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, nullptr, nullptr, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_alpha(alphas, n_samples, stream));
+  const bool vec = aligned(alphas, 16) && aligned(ray_id, 16) && aligned(weights, 16) && (!trans || aligned(trans, 16));
+  const unsigned blocks = resident_blocks(ceil_div(ceil_div(n_samples, kWarpTile) * 32, 256));
+  if (vec)
+    weights_alpha_fwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, alphas,
+                                                                     std::exp(-neg_log_eps), weights, trans);
+  else
+    weights_alpha_fwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, alphas,
+                                                                      std::exp(-neg_log_eps), weights, trans);
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;

@@ -517,7 +517,8 @@ def test_weights_and_accumulate(N):
 
 
 @pytest.mark.parametrize("eps", [None, 1e-4])
-def test_weights_alpha(N, eps):
+@pytest.mark.parametrize("flat", [True, False])
+def test_weights_alpha(N, eps, flat):
     """Alpha compositing (readings #16-#17) vs the oracle: ragged rays incl.
     5000-sample ones, α with exact 0s and 1s (opaque samples), early stop."""
     import torch
@@ -528,8 +529,9 @@ def test_weights_alpha(N, eps):
     a = rng.choice([0.0, 1.0, 0.02, 0.3], n_s, p=[0.3, 0.01, 0.5, 0.19]).astype(np.float32)
     a *= rng.uniform(0.5, 1.0, n_s).astype(np.float32) ** (a < 1)
     L = math.inf if eps is None else -math.log(float(np.float32(eps)))
+    # flat: ray_id given (the flat-tile forward); else an empty ray_id (one warp per ray)
     s = N.PackedSamples(cuda(pk), cuda(np.zeros(n_s, np.float32)), cuda(np.zeros(n_s, np.float32)),
-                        cuda(np.zeros(n_s, np.int32)))
+                        cuda(ray_ids(pk)) if flat else cuda(np.zeros(0, np.int32)))
     ag = cuda(a).requires_grad_()
     w, T = N.render_weights_alpha(s, ag, eps=eps)
     w_ref, T_ref = O.weights_alpha_fwd(pk, a, L)

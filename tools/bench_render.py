@@ -55,3 +55,9 @@ def acc(Sx):
 ms_af, _ = timed(lambda: acc(S))
 ms_aw, _ = timed(lambda: acc(S0))
 print(f"accumulate C=3 fwd+bwd (incl. autograd) flat {ms_af * 1e3:.1f} us, warp per ray {ms_aw * 1e3:.1f} us")
+# alpha compositing forward (SDF-style α): flat vs one warp per ray
+aq = torch.rand(len(a0), device="cuda") * 0.2
+with torch.no_grad():
+    ms_pf, _ = timed(lambda: N.render_weights_alpha(S, aq, 1e-4))
+    ms_pw, _ = timed(lambda: N.render_weights_alpha(S0, aq, 1e-4))
+print(f"render_weights_alpha fwd flat {ms_pf * 1e3:.1f} us, warp per ray {ms_pw * 1e3:.1f} us")
