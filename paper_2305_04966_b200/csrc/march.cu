@@ -866,15 +866,20 @@ __device__ __forceinline__ void tile_write(const TileBuf &T, int n_ent_t, bool o
   __syncwarp();  // the buffer is refilled next
 }
 
-template <bool kCone, bool kSkip, bool kL1>
+// kBounds: the combined estimator's per-ray span (nacc_occgrid_ray_bounds) from the same phase 1 --
+// the first and the last emitted point of each ray from its first and last entries with a set bit
+// -- with no look-back and no writer (t0 / t1 carry t_near / t_far).
+template <bool kCone, bool kSkip, bool kL1, bool kBounds = false>
 __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_kernel(
     GridConst g, MarchConst p, const uint32_t *__restrict__ bits, const uint32_t *__restrict__ mask2, int M,
     const uint32_t *__restrict__ mask3, const float *__restrict__ obox, const float *__restrict__ rays_o,
     const float *__restrict__ rays_d, const float *__restrict__ t_min, const float *__restrict__ t_max,
     int64_t n_rays, int64_t n_tiles, const ConeHeader *__restrict__ hdr, const float *__restrict__ tab,
     LookbackWs *__restrict__ lb, int64_t *__restrict__ packed_info, int64_t *__restrict__ total, int64_t capacity,
-    int32_t *__restrict__ status_out, float *__restrict__ t0, float *__restrict__ t1, int32_t *__restrict__ ray_id) {
+    int32_t *__restrict__ status_out, float *__restrict__ t0, float *__restrict__ t1, int32_t *__restrict__ ray_id,
+    unsigned long long *__restrict__ n_alive = nullptr) {
   constexpr int kR = tile_rays(kCone, kL1);  // rays per tile
+  __shared__ int s_efirst[kBounds ? kFWarps : 1][kTRays], s_elast[kBounds ? kFWarps : 1][kTRays];
   __shared__ TileBuf tb[kFWarps][2];
   __shared__ uint32_t evq[kFWarps][kEvCap];
   __shared__ int seglist[kFWarps][32];  // direct traversal (overflowed tiles)
@@ -894,6 +899,7 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
     if (lane == 0) tile32 = atomicAdd(&lb->tile_counter, 1u);
     const int64_t tile = (int64_t)__shfl_sync(kFull, tile32, 0);
     const bool have = tile < n_tiles;
+    if (kBounds && !have) break;
     int cur_c = 0, cur_ne = 0;
     long long cur_agg = 0;
     bool cur_over = false;
@@ -1071,6 +1077,66 @@ __global__ void __launch_bounds__(kFWarps * 32, NACC_MARCH_MINB) march_fused_ker
         if (wide) phase1(std::true_type{});
         else phase1(std::false_type{});
         cur_over = n_ent > kECap;
+      }
+      if constexpr (kBounds) {
+        if (!cur_over) {  // each ray's first / last entry with a set bit, by shared atomics
+          if (lane < kR) {
+            s_efirst[warp][lane] = 0x7fffffff;
+            s_elast[warp][lane] = -1;
+          }
+          __syncwarp();
+          for (int e0 = 0; e0 < n_ent; e0 += 32) {
+            const int e = e0 + lane;
+            const uint32_t ent = e < n_ent ? T.ent[e] : 0u;
+            if (ent & 0xFFFFu) {
+              atomicMin(&s_efirst[warp][ent_j(ent)], e);
+              atomicMax(&s_elast[warp][ent_j(ent)], e);
+            }
+          }
+          __syncwarp();
+          if (lane < kR && r_base + lane < n_rays) {
+            float ta = 0.f, tb = 0.f;
+            const int el = s_elast[warp][lane];
+            if (el >= 0) {
+              const uint32_t eF = T.ent[s_efirst[warp][lane]], eL = T.ent[el];
+              const int kf = T.kr[lane].x + ent_k16(eF) + (__ffs(eF & 0xFFFFu) - 1);
+              const int kl = T.kr[lane].x + ent_k16(eL) + (31 - __clz(eL & 0xFFFFu));
+              float x, y;
+              lattice_ends<kCone>(p, T.od[lane][0].w, tab, kf, ta, x);
+              lattice_ends<kCone>(p, T.od[lane][0].w, tab, kl, y, tb);
+              if (n_alive) atomicAdd(n_alive, 1ull);
+            }
+            t0[r_base + lane] = ta;
+            t1[r_base + lane] = tb;
+          }
+        } else {  // an overflowed tile: traverse its rays
+          for (int jj = 0; jj < kR; ++jj) {
+            if (r_base + jj >= n_rays) break;
+            const RaySetup s = ray_setup(g, p, obox, rays_o, rays_d, t_min, t_max, r_base + jj);
+            int kfirst = -1, klast = -1, kb0, ke0;
+            traverse_ray<kCone, kSkip, kL1>(g, p, bits, mask2, M, mask3, s, hdr, tab, seglist[warp], kb0, ke0,
+                                            [&](unsigned b, bool pred, int k, int32_t cnt) {
+                                              if (b) {
+                                                const int kf = __shfl_sync(kFull, k, __ffs(b) - 1);
+                                                klast = __shfl_sync(kFull, k, 31 - __clz(b));
+                                                if (kfirst < 0) kfirst = kf;
+                                              }
+                                            });
+            if (lane == 0) {
+              float ta = 0.f, tb = 0.f;
+              if (klast >= 0) {
+                float x, y;
+                lattice_ends<kCone>(p, s.near_r, tab, kfirst, ta, x);
+                lattice_ends<kCone>(p, s.near_r, tab, klast, y, tb);
+                if (n_alive) atomicAdd(n_alive, 1ull);
+              }
+              t0[r_base + jj] = ta;
+              t1[r_base + jj] = tb;
+            }
+          }
+        }
+        __syncwarp();
+        continue;  // no look-back, no writer
       }
       if (cur_over) {  // count by direct traversal (phase 2 writes the same way)
         for (int jj = 0; jj < kR; ++jj) {
@@ -1314,6 +1380,22 @@ static MarchConst make_march_const(const nacc_march &p) {
     else KERNEL<false, false, false><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);                     \
   } while (0)
 
+// the fused kernel in bounds mode
+#define NACC_DISPATCH3B(KERNEL, GRID, BLOCK, STREAM, ...)                                              \
+  do {                                                                                                 \
+    if (cone && skip && l1) KERNEL<true, true, true, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);     \
+    else if (cone && skip) KERNEL<true, true, false, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);     \
+    else if (cone && l1) KERNEL<true, false, true, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);       \
+    else if (cone) KERNEL<true, false, false, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);            \
+    else if (skip && l1) KERNEL<false, true, true, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);       \
+    else if (skip) KERNEL<false, true, false, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);            \
+    else if (l1) KERNEL<false, false, true, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);              \
+    else KERNEL<false, false, false, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);                     \
+  } while (0)
+#ifndef NACC_MARCH_FUSED_BOUNDS
+#define NACC_MARCH_FUSED_BOUNDS 1  // build parameter: ray bounds from the fused kernel's phase 1 (0: one warp per ray)
+#endif
+
 enum MarchMode { kModeFused = 0, kModeFill = 1, kModeBounds = 2 };
 
 static nacc_status launch_march(int mode, const nacc_grid *grid, const uint32_t *bits,
@@ -1343,7 +1425,16 @@ static nacc_status launch_march(int mode, const nacc_grid *grid, const uint32_t 
     count_launch(2);
     NACC_CHECK_LAUNCH();
   }
-  if (mode == kModeBounds) {  // t0 / t1 carry t_near / t_far
+  // single-level grids: the fused kernel's phase 1 (CFG2 182.7 -> 117.7 us); cascades keep one warp
+  // per ray (CFG3 1956 vs 2040 us fused)
+  if (mode == kModeBounds && NACC_MARCH_FUSED_BOUNDS && l1) {  // t0 / t1 carry t_near / t_far
+    if (n_alive) NACC_CUDA(cudaMemsetAsync(n_alive, 0, sizeof(unsigned long long), stream));
+    const int64_t n_tiles = fused_tiles(n_rays, cone, l1);
+    NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8, stream));  // the tile counter
+    NACC_DISPATCH3B(march_fused_kernel, fused_blocks(n_tiles, cone, skip, l1), kFWarps * 32, stream, g, p, bits,
+                    mask2, M, mask3, obox, rays_o, rays_d, t_min, t_max, n_rays, n_tiles, w.hdr, w.tab, w.lb,
+                    nullptr, nullptr, 0, nullptr, t0, t1, nullptr, n_alive);
+  } else if (mode == kModeBounds) {  // t0 / t1 carry t_near / t_far
     if (n_alive) NACC_CUDA(cudaMemsetAsync(n_alive, 0, sizeof(unsigned long long), stream));
     NACC_DISPATCH3(march_bounds_kernel, (unsigned)grid_for(n_rays * 32, 128), 128, stream, g, p, bits, mask2, M, mask3,
                    obox, rays_o, rays_d, t_min, t_max, n_rays, w.hdr, w.tab, t0, t1, n_alive);
