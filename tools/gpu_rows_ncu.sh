@@ -16,7 +16,7 @@ cap alpha_fwd weights_alpha_fwd 2 python tools/prof_rows.py alpha
 cap alpha_bwd weights_alpha_bwd 1 python tools/prof_rows.py alpha
 cap pdf_loss pdf_loss_kernel 1 python tools/prof_rows.py pdf
 cap pdf_loss_bwd pdf_loss_bwd 1 python tools/prof_rows.py pdf
-cap march_bounds march_bounds 1 python tools/prof_rows.py bounds
+cap march_bounds march_fused 1 python tools/prof_rows.py bounds  # single level: the fused kernel in bounds mode
 cap weights_fwd weights_fwd 1 python tools/prof_rows.py accum
-cap accumulate accumulate_kernel 1 python tools/prof_rows.py accum
+cap accumulate accumulate_warp 1 python tools/prof_rows.py accum
 ls gpurun_out | grep prof_
