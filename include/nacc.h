@@ -191,6 +191,18 @@ nacc_status nacc_render_weights_bwd(const int64_t *packed_info, int64_t n_rays, 
                                     double neg_log_eps, const float *g_weights,
                                     const float *g_trans, float *g_sigma, cudaStream_t stream);
 
+/* The same gradient on ray-aligned flat tiles for packed samples from the sampling
+ * calls (ray_id [n_samples], contiguous packing): pass 1 writes each ray's
+ * R = Σ (g_w w + g_T T) to the workspace (8 bytes per ray,
+ * nacc_render_weights_bwd_flat_workspace_bytes), pass 2 forms Σ_{j>i} = R - prefix. */
+size_t nacc_render_weights_bwd_flat_workspace_bytes(int64_t n_rays);
+nacc_status nacc_render_weights_bwd_flat(const int64_t *packed_info, const int32_t *ray_id,
+                                         int64_t n_rays, const float *t0, const float *t1,
+                                         const float *sigma, int64_t n_samples, double neg_log_eps,
+                                         const float *g_weights, const float *g_trans,
+                                         float *g_sigma, void *ws, size_t ws_bytes,
+                                         cudaStream_t stream);
+
 /* Alpha compositing for fields that supply α per interval (SDF-based fields,
  * P:61; "accumulating them through alpha-composition"; DESIGN.md
  * readings #16-#17):  T_i = Π_{j<i} (1 − α_j),  w_i = T_i α_i, and w_i = 0

@@ -62,6 +62,8 @@ SIGNATURES = {
     "nacc_filter_early_stop": (C.c_int, [P, I64, P, P, P, I64, D, P, P, P, P, I64, P, P, SZ, P]),
     "nacc_render_weights_fwd": (C.c_int, [P, I64, P, P, P, I64, D, P, P, P, P]),
     "nacc_render_weights_fwd_flat": (C.c_int, [P, P, I64, P, P, P, I64, D, P, P, P, P]),
+    "nacc_render_weights_bwd_flat_workspace_bytes": (C.c_size_t, [I64]),
+    "nacc_render_weights_bwd_flat": (C.c_int, [P, P, I64, P, P, P, I64, D, P, P, P, P, C.c_size_t, P]),
     "nacc_render_weights_bwd": (C.c_int, [P, I64, P, P, P, I64, D, P, P, P, P]),
     "nacc_render_weights_alpha_fwd": (C.c_int, [P, I64, P, I64, D, P, P, P]),
     "nacc_render_weights_alpha_fwd_flat": (C.c_int, [P, P, I64, P, I64, D, P, P, P]),

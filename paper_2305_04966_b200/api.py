@@ -302,21 +302,27 @@ class _WeightsFn(torch.autograd.Function):
         else:
             check(L.lib().nacc_render_weights_fwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, nle,
                                                   _ptr(w), _ptr(T), _ptr(a), _stream()), "nacc_render_weights_fwd")
-        ctx.save_for_backward(packed_info, t0, t1, sigma)
+        ctx.save_for_backward(packed_info, t0, t1, sigma, ray_id)
         ctx.nle = nle
         ctx.mark_non_differentiable(a)
         return w, T, a
 
     @staticmethod
     def backward(ctx, g_w, g_T, g_a):
-        packed_info, t0, t1, sigma = ctx.saved_tensors
+        packed_info, t0, t1, sigma, ray_id = ctx.saved_tensors
         n, N = packed_info.shape[0], t0.numel()
         g_sigma = torch.empty_like(sigma)
         gw = torch.zeros_like(sigma) if g_w is None else g_w.contiguous().float()
         gT = None if g_T is None else g_T.contiguous().float()
-        check(L.lib().nacc_render_weights_bwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, ctx.nle,
-                                              _ptr(gw), _ptr(gT), _ptr(g_sigma), _stream()),
-              "nacc_render_weights_bwd")
+        if ray_id is not None:  # the flat-tile backward (per-ray totals in a workspace)
+            ws = _ws(L.lib().nacc_render_weights_bwd_flat_workspace_bytes(n), t0.device)
+            check(L.lib().nacc_render_weights_bwd_flat(_ptr(packed_info), _ptr(ray_id), n, _ptr(t0), _ptr(t1),
+                                                       _ptr(sigma), N, ctx.nle, _ptr(gw), _ptr(gT), _ptr(g_sigma),
+                                                       _ptr(ws), ws.numel(), _stream()), "nacc_render_weights_bwd_flat")
+        else:
+            check(L.lib().nacc_render_weights_bwd(_ptr(packed_info), n, _ptr(t0), _ptr(t1), _ptr(sigma), N, ctx.nle,
+                                                  _ptr(gw), _ptr(gT), _ptr(g_sigma), _stream()),
+                  "nacc_render_weights_bwd")
         return None, None, None, g_sigma, None, None
 
 

@@ -814,6 +814,114 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) weights_alpha_fwd_warp_k
   }
 }
 
+// Granular weights backward on the flat tiles (samples with ray_id): pass 1 over the warp's tile
+// sums v = g_w w + g_T T per ray (lane sums, the leading run through the warp scan) into the
+// workspace R[ray]; pass 2 recomputes S, T, w and the inclusive prefix P of v, Q = R - P is
+// Σ_{j>i} v_j, g_σ = δ (g_w T (1 - α)[live] - Q).  The tile owns whole rays, so a warp reads only
+// the R it wrote.
+template <bool kVec>
+__global__ void __launch_bounds__(256, NACC_RENDER_BPS) weights_bwd_warp_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
+    const float *__restrict__ t0, const float *__restrict__ t1, const float *__restrict__ sigma, double L,
+    const float *__restrict__ g_weights, const float *__restrict__ g_trans, float *__restrict__ g_sigma,
+    double *__restrict__ Rws) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t N = min(packed_end(packed_info, n_rays), n_samples);
+  auto gload4 = [&](const float *__restrict__ a, const Items &it, float o[4]) {
+    if (kVec && it.valid[0] && it.valid[3]) {
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(a + it.q0));
+      o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = it.valid[j] ? __ldg(a + it.q0 + j) : 0.f;
+    }
+  };
+  for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
+    const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+    const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+    if (B >= E) continue;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      Seg<1> carryS = seg_identity<1>(), carryV = seg_identity<1>();
+      int32_t carry_rid = -1;
+      for (int64_t c0 = B & ~(int64_t)3; c0 < E; c0 += kWarpChunk) {
+        Items it;
+        load_items_warp<kVec>(it, c0, B, E, t0, t1, sigma, ray_id, carry_rid);
+        double s[4], S[4];
+        warp_items_S(it, s, S, carryS);
+        float gwv[4], gtv[4] = {0.f, 0.f, 0.f, 0.f};
+        gload4(g_weights, it, gwv);
+        if (g_trans) gload4(g_trans, it, gtv);
+        double v[4], gwTea[4];
+        double Tn = trans_first(S[0]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double ea = interval_ea(s[j]);
+          const double T = (j > 0 && it.head[j]) ? 1.0 : Tn;
+          Tn = T * ea;
+          const bool live = it.valid[j] && !(S[j] > L);
+          v[j] = it.valid[j] ? (live ? (double)gwv[j] * (T * (1.0 - ea)) : 0.0) + (double)gtv[j] * T : 0.0;
+          gwTea[j] = live ? (double)gwv[j] * T * ea : 0.0;
+        }
+        if (pass == 0) {  // per-ray totals R into the workspace
+          Seg<1> cur = seg_identity<1>(), lead;
+          int32_t lead_r = -1;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            Seg<1> x;
+            x.f = it.head[j];
+            x.v[0] = v[j];
+            cur = seg_combine(cur, x);
+            if (it.tail[j]) {
+              if (cur.f) Rws[it.rid[j]] = cur.v[0];
+              else {
+                lead = cur;
+                lead_r = it.rid[j];
+              }
+            }
+          }
+          const Seg<1> enter = warp_seg_excl<1>(cur, carryV);
+          if (lead_r >= 0) Rws[lead_r] = seg_combine(enter, lead).v[0];
+        } else {  // gradients from Q = R - P (inclusive prefix of v)
+          Seg<1> agg = seg_identity<1>();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            Seg<1> x;
+            x.f = it.head[j];
+            x.v[0] = v[j];
+            agg = seg_combine(agg, x);
+          }
+          Seg<1> run = warp_seg_excl<1>(agg, carryV);
+          float gs[4];
+          int32_t cr = -1;
+          double R = 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            run.v[0] = (it.head[j] ? 0.0 : run.v[0]) + v[j];
+            gs[j] = 0.f;
+            if (it.valid[j]) {
+              if (it.rid[j] != cr) {
+                R = Rws[it.rid[j]];
+                cr = it.rid[j];
+              }
+              gs[j] = (float)(((double)it.t1[j] - (double)it.t0[j]) * (gwTea[j] - (R - run.v[0])));
+            }
+          }
+          if (kVec && it.valid[0] && it.valid[3]) {
+            *reinterpret_cast<float4 *>(g_sigma + it.q0) = make_float4(gs[0], gs[1], gs[2], gs[3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (it.valid[j]) g_sigma[it.q0 + j] = gs[j];
+          }
+        }
+      }
+      __syncwarp();  // pass 2 reads the totals this warp wrote in pass 1
+    }
+  }
+}
+
 // persistent grid for the tile kernels: all resident at once (3 blocks of 256 per SM)
 static unsigned resident_blocks(int64_t want) {
   static int n_sm = 0;
@@ -1336,6 +1444,40 @@ nacc_status nacc_render_weights_fwd(const int64_t *packed_info, int64_t n_rays, 
   NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
   weights_fwd_kernel<<<grid_for(n_rays * 32, 256), 256, 0, stream>>>(packed_info, n_rays, t0, t1, sigma,
                                                                       neg_log_eps, weights, trans, alphas);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
+}
+
+size_t nacc_render_weights_bwd_flat_workspace_bytes(int64_t n_rays) {
+  return n_rays < 0 ? 0 : (size_t)n_rays * sizeof(double);
+}
+
+nacc_status nacc_render_weights_bwd_flat(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
+                                         const float *t0, const float *t1, const float *sigma, int64_t n_samples,
+                                         double neg_log_eps, const float *g_weights, const float *g_trans,
+                                         float *g_sigma, void *ws, size_t ws_bytes, cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_packed(packed_info, n_rays, n_samples);
+  if (s != NACC_OK) return s;
+  NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
+  if (n_rays == 0 || n_samples == 0) return NACC_OK;
+  NACC_REQUIRE(ray_id && t0 && t1 && sigma && g_weights && g_sigma,
+               "ray_id, t0, t1, sigma, g_weights, g_sigma must be non-NULL");
+  NACC_REQUIRE(ws && ws_bytes >= nacc_render_weights_bwd_flat_workspace_bytes(n_rays) && aligned(ws, 8),
+               "workspace too small");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, t0, t1, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_sigma(sigma, n_samples, "sigma must be >= 0 and finite", stream));
+  const bool vec = aligned(t0, 16) && aligned(t1, 16) && aligned(sigma, 16) && aligned(ray_id, 16) &&
+                   aligned(g_weights, 16) && (!g_trans || aligned(g_trans, 16)) && aligned(g_sigma, 16);
+  const unsigned blocks = resident_blocks(ceil_div(ceil_div(n_samples, kWarpTile) * 32, 256));
+  double *R = static_cast<double *>(ws);
+  if (vec)
+    weights_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
+                                                              neg_log_eps, g_weights, g_trans, g_sigma, R);
+  else
+    weights_bwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, t0, t1, sigma,
+                                                               neg_log_eps, g_weights, g_trans, g_sigma, R);
   count_launch(1);
   NACC_CHECK_LAUNCH();
   return NACC_OK;

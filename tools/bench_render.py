@@ -61,3 +61,12 @@ with torch.no_grad():
     ms_pf, _ = timed(lambda: N.render_weights_alpha(S, aq, 1e-4))
     ms_pw, _ = timed(lambda: N.render_weights_alpha(S0, aq, 1e-4))
 print(f"render_weights_alpha fwd flat {ms_pf * 1e3:.1f} us, warp per ray {ms_pw * 1e3:.1f} us")
+# granular render_weights forward + backward (flat vs one warp per ray)
+sgq = sg.clone().requires_grad_()
+def wfb(Sx):
+    w, T, _ = N.render_weights(Sx, sgq, 1e-4)
+    (w.sum() + T.sum()).backward()
+    return w
+ms_bf, _ = timed(lambda: wfb(S))
+ms_bw, _ = timed(lambda: wfb(S0))
+print(f"render_weights fwd+bwd (incl. autograd) flat {ms_bf * 1e3:.1f} us, warp per ray {ms_bw * 1e3:.1f} us")
