@@ -229,6 +229,14 @@ nacc_status nacc_render_weights_alpha_bwd(const int64_t *packed_info, int64_t n_
                                           double neg_log_eps, const float *g_weights,
                                           const float *g_trans, float *g_alphas, void *ws,
                                           size_t ws_bytes, cudaStream_t stream);
+/* The same gradient on ray-aligned flat tiles for packed samples from the
+ * sampling calls (ray_id [n_samples], contiguous packing); same workspace. */
+nacc_status nacc_render_weights_alpha_bwd_flat(const int64_t *packed_info, const int32_t *ray_id,
+                                               int64_t n_rays, const float *alphas,
+                                               int64_t n_samples, double neg_log_eps,
+                                               const float *g_weights, const float *g_trans,
+                                               float *g_alphas, void *ws, size_t ws_bytes,
+                                               cudaStream_t stream);
 
 /* accumulate_along_rays: out[r][c] = Σ_i w_i v_i[c]; values == NULL means ones
  * (opacity, C must be 1).  1 <= C <= 64. */

@@ -69,6 +69,7 @@ SIGNATURES = {
     "nacc_render_weights_alpha_fwd_flat": (C.c_int, [P, P, I64, P, I64, D, P, P, P]),
     "nacc_render_weights_alpha_bwd_workspace_bytes": (SZ, [I64]),
     "nacc_render_weights_alpha_bwd": (C.c_int, [P, I64, P, I64, D, P, P, P, P, SZ, P]),
+    "nacc_render_weights_alpha_bwd_flat": (C.c_int, [P, P, I64, P, I64, D, P, P, P, P, SZ, P]),
     "nacc_accumulate_along_rays": (C.c_int, [P, I64, P, P, I32, I64, P, P]),
     "nacc_accumulate_along_rays_bwd": (C.c_int, [P, I64, P, P, I32, I64, P, P, P, P]),
     "nacc_accumulate_along_rays_flat": (C.c_int, [P, P, I64, P, P, I32, I64, P, P]),

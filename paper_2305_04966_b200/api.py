@@ -348,22 +348,27 @@ class _AlphaWeightsFn(torch.autograd.Function):
         else:
             check(L.lib().nacc_render_weights_alpha_fwd(_ptr(packed_info), n, _ptr(alphas), N, nle, _ptr(w), _ptr(T),
                                                         _stream()), "nacc_render_weights_alpha_fwd")
-        ctx.save_for_backward(packed_info, alphas)
+        ctx.save_for_backward(packed_info, alphas, ray_id)
         ctx.nle = nle
         ctx.set_materialize_grads(False)
         return w, T
 
     @staticmethod
     def backward(ctx, g_w, g_T):
-        packed_info, alphas = ctx.saved_tensors
+        packed_info, alphas, ray_id = ctx.saved_tensors
         n, N = packed_info.shape[0], alphas.numel()
         g_a = torch.empty_like(alphas)
         gw = torch.zeros_like(alphas) if g_w is None else g_w.contiguous().float()
         gT = None if g_T is None else g_T.contiguous().float()
         ws = _ws(L.lib().nacc_render_weights_alpha_bwd_workspace_bytes(N), alphas.device)
-        check(L.lib().nacc_render_weights_alpha_bwd(_ptr(packed_info), n, _ptr(alphas), N, ctx.nle, _ptr(gw), _ptr(gT),
-                                                    _ptr(g_a), _ptr(ws), ws.numel(), _stream()),
-              "nacc_render_weights_alpha_bwd")
+        if ray_id is not None:  # the flat-tile backward
+            check(L.lib().nacc_render_weights_alpha_bwd_flat(_ptr(packed_info), _ptr(ray_id), n, _ptr(alphas), N,
+                                                             ctx.nle, _ptr(gw), _ptr(gT), _ptr(g_a), _ptr(ws),
+                                                             ws.numel(), _stream()), "nacc_render_weights_alpha_bwd_flat")
+        else:
+            check(L.lib().nacc_render_weights_alpha_bwd(_ptr(packed_info), n, _ptr(alphas), N, ctx.nle, _ptr(gw),
+                                                        _ptr(gT), _ptr(g_a), _ptr(ws), ws.numel(), _stream()),
+                  "nacc_render_weights_alpha_bwd")
         return None, g_a, None, None
 
 

@@ -922,6 +922,146 @@ __global__ void __launch_bounds__(256, NACC_RENDER_BPS) weights_bwd_warp_kernel(
   }
 }
 
+// Alpha compositing backward on the flat tiles (samples with ray_id).  Per warp tile: a forward
+// pass stores T (fp64 segmented product scan of 1 - α) to the workspace; a reverse pass over the
+// tile's chunks forms Λ_k = Σ_{i>k} ([live_i] g_w_i α_i + g_T_i) Π_{k<j<i} (1 - α_j) by suffix
+// composition of the affine maps x -> c + (1 - α) x (division-free, α = 1 safe), a ray's head
+// resetting the map to the constant 0 (so no segment flags are needed across lanes), and
+// g_α = [live] g_w T - T Λ.  T is read back through L2 (__ldcg): another warp's reverse pass may
+// have cached a shared line in L1 before this warp wrote it.
+template <bool kVec>
+__global__ void __launch_bounds__(256, NACC_RENDER_BPS) weights_alpha_bwd_warp_kernel(
+    const int64_t *__restrict__ packed_info, const int32_t *__restrict__ ray_id, int64_t n_rays, int64_t n_samples,
+    const float *__restrict__ alphas, double eps_T, const float *__restrict__ g_weights,
+    const float *__restrict__ g_trans, double *__restrict__ T64, float *__restrict__ g_alphas) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t N = min(packed_end(packed_info, n_rays), n_samples);
+  auto load4 = [&](const int32_t *ri, const float *a, int64_t q0, int64_t B, int64_t E, float av[4], int32_t rid[4],
+                   bool valid[4]) {
+    if (kVec && q0 >= B && q0 + 3 < E) {
+      const float4 x = __ldg(reinterpret_cast<const float4 *>(a + q0));
+      const int4 y = __ldg(reinterpret_cast<const int4 *>(ri + q0));
+      av[0] = x.x; av[1] = x.y; av[2] = x.z; av[3] = x.w;
+      rid[0] = y.x; rid[1] = y.y; rid[2] = y.z; rid[3] = y.w;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) valid[j] = true;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        valid[j] = q0 + j >= B && q0 + j < E;
+        av[j] = valid[j] ? __ldg(a + q0 + j) : 0.f;
+        rid[j] = valid[j] ? __ldg(ri + q0 + j) : -1;
+      }
+    }
+  };
+  for (int64_t wt = gw; wt * kWarpTile < N; wt += nw) {
+    const int64_t B = snap_to_ray(packed_info, ray_id, wt * kWarpTile, N);
+    const int64_t E = snap_to_ray(packed_info, ray_id, (wt + 1) * kWarpTile, N);
+    if (B >= E) continue;
+    const int64_t cfirst = B & ~(int64_t)3;
+    // forward: T of every sample of the tile
+    SegP carry{0, 1.0};
+    int32_t carry_rid = -1;
+    for (int64_t c0 = cfirst; c0 < E; c0 += kWarpChunk) {
+      const int64_t q0 = c0 + (int64_t)lane * 4;
+      float a[4];
+      int32_t rid[4];
+      bool valid[4];
+      load4(ray_id, alphas, q0, B, E, a, rid, valid);
+      int32_t prev = __shfl_up_sync(kFull, rid[3], 1);
+      if (lane == 0) prev = carry_rid;
+      carry_rid = __shfl_sync(kFull, rid[3], 31);
+      bool head[4];
+      SegP agg{0, 1.0};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        head[j] = valid[j] && (q0 + j == B || rid[j] != (j == 0 ? prev : rid[j - 1]));
+        agg = segp_combine(agg, SegP{head[j], 1.0 - (double)a[j]});
+      }
+      SegP run = warp_segp_excl(agg, carry);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double T = head[j] ? 1.0 : run.v;
+        run.v = T * (1.0 - (double)a[j]);
+        if (valid[j]) T64[q0 + j] = T;
+      }
+    }
+    __syncwarp();
+    // reverse: Λ by suffix composition, chunk by chunk from the tile's end
+    double lam_carry = 0.0;  // Λ entering the chunk from its right (0 at the tile's end: a ray ends there)
+    const int64_t clast = cfirst + ((E - 1 - cfirst) / kWarpChunk) * kWarpChunk;
+    for (int64_t c0 = clast; c0 >= cfirst; c0 -= kWarpChunk) {
+      const int64_t q0 = c0 + (int64_t)lane * 4;
+      float a[4];
+      int32_t rid[4];
+      bool valid[4];
+      load4(ray_id, alphas, q0, B, E, a, rid, valid);
+      // the previous sample's ray (for the heads): item q0 - 1, from the left lane or memory
+      int32_t prev = __shfl_up_sync(kFull, rid[3], 1);
+      if (lane == 0) prev = (q0 > B && q0 - 1 < E) ? __ldg(ray_id + q0 - 1) : -1;
+      double T[4], c[4], am[4];
+      bool head[4], live[4];
+      float gwv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        head[j] = valid[j] && (q0 + j == B || rid[j] != (j == 0 ? prev : rid[j - 1]));
+        T[j] = valid[j] ? __ldcg(T64 + q0 + j) : 0.0;
+        live[j] = valid[j] && !(T[j] < eps_T);
+        gwv[j] = valid[j] ? __ldg(g_weights + q0 + j) : 0.f;
+        const double gt = (valid[j] && g_trans) ? (double)__ldg(g_trans + q0 + j) : 0.0;
+        am[j] = valid[j] ? 1.0 - (double)a[j] : 1.0;  // identity past the tile's end
+        c[j] = (live[j] ? (double)gwv[j] * (double)a[j] : 0.0) + gt;
+      }
+      // the lane's map from Λ of its last item to Λ of the sample before its first: through items
+      // 3..0, x -> head ? 0 : c + am x
+      double A = 1.0, Bv = 0.0;
+#pragma unroll
+      for (int j = 3; j >= 0; --j) {
+        if (head[j]) {
+          A = 0.0;
+          Bv = 0.0;
+        } else {
+          Bv = c[j] + am[j] * Bv;
+          A = am[j] * A;
+        }
+      }
+      // exclusive suffix composition over the lanes to the right: X = Λ of the lane's last item
+      double SA = A, SB = Bv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double a2 = __shfl_down_sync(kFull, SA, o), b2 = __shfl_down_sync(kFull, SB, o);
+        if (lane + o < 32) {
+          SB = SB + SA * b2;
+          SA = SA * a2;
+        }
+      }
+      double Ae = __shfl_down_sync(kFull, SA, 1), Be = __shfl_down_sync(kFull, SB, 1);
+      if (lane == 31) {
+        Ae = 1.0;
+        Be = 0.0;
+      }
+      double lam = Be + Ae * lam_carry;  // Λ of item 3
+      float ga[4];
+#pragma unroll
+      for (int j = 3; j >= 0; --j) {
+        ga[j] = valid[j] ? (float)((live[j] ? (double)gwv[j] * T[j] : 0.0) - T[j] * lam) : 0.f;
+        lam = head[j] ? 0.0 : c[j] + am[j] * lam;  // Λ of item j - 1
+      }
+      if (kVec && q0 >= B && q0 + 3 < E) {
+        *reinterpret_cast<float4 *>(g_alphas + q0) = make_float4(ga[0], ga[1], ga[2], ga[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (valid[j]) g_alphas[q0 + j] = ga[j];
+      }
+      const double A0 = __shfl_sync(kFull, SA, 0), B0 = __shfl_sync(kFull, SB, 0);
+      lam_carry = B0 + A0 * lam_carry;
+    }
+  }
+}
+
 // persistent grid for the tile kernels: all resident at once (3 blocks of 256 per SM)
 static unsigned resident_blocks(int64_t want) {
   static int n_sm = 0;
@@ -1575,6 +1715,35 @@ nacc_status nacc_render_weights_alpha_fwd(const int64_t *packed_info, int64_t n_
 
 size_t nacc_render_weights_alpha_bwd_workspace_bytes(int64_t n_samples) {
   return n_samples > 0 ? align_up((size_t)n_samples * 8, 256) : 256;
+}
+
+nacc_status nacc_render_weights_alpha_bwd_flat(const int64_t *packed_info, const int32_t *ray_id, int64_t n_rays,
+                                               const float *alphas, int64_t n_samples, double neg_log_eps,
+                                               const float *g_weights, const float *g_trans, float *g_alphas,
+                                               void *ws, size_t ws_bytes, cudaStream_t stream) {
+  clear_error();
+  nacc_status s = check_packed(packed_info, n_rays, n_samples);
+  if (s != NACC_OK) return s;
+  NACC_REQUIRE(!std::isnan(neg_log_eps), "neg_log_eps must not be NaN");
+  if (n_rays == 0 || n_samples == 0) return NACC_OK;
+  NACC_REQUIRE(ray_id && alphas && g_weights && g_alphas, "ray_id, alphas, g_weights, g_alphas must be non-NULL");
+  NACC_REQUIRE(ws && ws_bytes >= nacc_render_weights_alpha_bwd_workspace_bytes(n_samples) && aligned(ws, 8),
+               "workspace too small");
+  NACC_DEBUG_CHECK(debug_check_packed(packed_info, n_rays, nullptr, nullptr, n_samples, stream));
+  NACC_DEBUG_CHECK(debug_check_alpha(alphas, n_samples, stream));
+  const double eps_T = std::exp(-neg_log_eps);
+  const bool vec = aligned(alphas, 16) && aligned(ray_id, 16) && aligned(g_alphas, 16);
+  const unsigned blocks = resident_blocks(ceil_div(ceil_div(n_samples, kWarpTile) * 32, 256));
+  double *T64 = static_cast<double *>(ws);
+  if (vec)
+    weights_alpha_bwd_warp_kernel<true><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, alphas,
+                                                                     eps_T, g_weights, g_trans, T64, g_alphas);
+  else
+    weights_alpha_bwd_warp_kernel<false><<<blocks, 256, 0, stream>>>(packed_info, ray_id, n_rays, n_samples, alphas,
+                                                                      eps_T, g_weights, g_trans, T64, g_alphas);
+  count_launch(1);
+  NACC_CHECK_LAUNCH();
+  return NACC_OK;
 }
 
 nacc_status nacc_render_weights_alpha_bwd(const int64_t *packed_info, int64_t n_rays, const float *alphas,

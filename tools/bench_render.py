@@ -70,3 +70,12 @@ def wfb(Sx):
 ms_bf, _ = timed(lambda: wfb(S))
 ms_bw, _ = timed(lambda: wfb(S0))
 print(f"render_weights fwd+bwd (incl. autograd) flat {ms_bf * 1e3:.1f} us, warp per ray {ms_bw * 1e3:.1f} us")
+# alpha compositing forward + backward (flat vs one warp per ray)
+aqg = aq.clone().requires_grad_()
+def afb(Sx):
+    w, T = N.render_weights_alpha(Sx, aqg, 1e-4)
+    (w.sum() + T.sum()).backward()
+    return w
+ms_qf, _ = timed(lambda: afb(S))
+ms_qw, _ = timed(lambda: afb(S0))
+print(f"render_weights_alpha fwd+bwd (incl. autograd) flat {ms_qf * 1e3:.1f} us, warp per ray {ms_qw * 1e3:.1f} us")
