@@ -690,7 +690,8 @@ __device__ __forceinline__ int32_t traverse_ray(const GridConst &g, const MarchC
 #define NACC_MARCH_TRAYS 16  // build parameter: rays per tile
 #endif
 #ifndef NACC_MARCH_ECAP
-#define NACC_MARCH_ECAP 512  // build parameter: entries (flagged 16-point segments) per tile buffer
+#define NACC_MARCH_ECAP 384  // build parameter: entries (flagged 16-point segments) per tile buffer (A/B 256 / 320 /
+                             // 384 / 512 / 768: CFG3 5.76 / 2.21 / 2.12 / 2.19 / 2.51 ms, CFG2 161 us at <= 512)
 #endif
 #ifndef NACC_MARCH_WARPS
 #define NACC_MARCH_WARPS 4  // build parameter: warps per block of the fused march
