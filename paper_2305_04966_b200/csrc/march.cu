@@ -1394,7 +1394,8 @@ static MarchConst make_march_const(const nacc_march &p) {
     else KERNEL<false, false, false, true><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__);                     \
   } while (0)
 #ifndef NACC_MARCH_FUSED_BOUNDS
-#define NACC_MARCH_FUSED_BOUNDS 1  // build parameter: ray bounds from the fused kernel's phase 1 (0: one warp per ray)
+#define NACC_MARCH_FUSED_BOUNDS 2  // build parameter: ray bounds from the fused kernel's phase 1 (0: one warp per ray,
+                                   // 1: single-level grids, 2: every grid)
 #endif
 
 enum MarchMode { kModeFused = 0, kModeFill = 1, kModeBounds = 2 };
@@ -1426,9 +1427,8 @@ static nacc_status launch_march(int mode, const nacc_grid *grid, const uint32_t 
     count_launch(2);
     NACC_CHECK_LAUNCH();
   }
-  // single-level grids: the fused kernel's phase 1 (CFG2 182.7 -> 117.7 us); cascades keep one warp
-  // per ray (CFG3 1956 vs 2040 us fused)
-  if (mode == kModeBounds && NACC_MARCH_FUSED_BOUNDS && l1) {  // t0 / t1 carry t_near / t_far
+  // the fused kernel's phase 1 (CFG2 182.7 -> 117.7 us, CFG3 1.96 -> 1.89 ms with 384-entry buffers)
+  if (mode == kModeBounds && NACC_MARCH_FUSED_BOUNDS && (l1 || NACC_MARCH_FUSED_BOUNDS == 2)) {  // t0/t1: t_near/t_far
     if (n_alive) NACC_CUDA(cudaMemsetAsync(n_alive, 0, sizeof(unsigned long long), stream));
     const int64_t n_tiles = fused_tiles(n_rays, cone, l1);
     NACC_CUDA(cudaMemsetAsync(w.lb, 0, 8, stream));  // the tile counter

@@ -265,6 +265,16 @@ def test_march_cfg3_full(N):
                     cone_angle=c.cone_angle, max_step=c.max_step, capacity=len(ref[1]))
     assert_march_equal(got, ref)
     assert ref[0][:, 1].mean() > 100
+    # the combined estimator's spans on the cascade (the fused kernel in bounds mode): the first t0
+    # and the last t1 each ray emits (reading #18), (0, 0) for rays that emit nothing
+    pk, t0, t1 = ref[0], ref[1], ref[2]
+    has = pk[:, 1] > 0
+    tn_ref = np.where(has, t0[np.minimum(pk[:, 0], len(t0) - 1)], 0).astype(np.float32)
+    tf_ref = np.where(has, t1[np.minimum(pk[:, 0] + pk[:, 1] - 1, len(t1) - 1)], 0).astype(np.float32)
+    tn, tf, alive = gpu_bounds(N, c.occ, 4, 128, c.roi, c.rays_o, c.rays_d, near_plane=c.near, step=c.step,
+                               cone_angle=c.cone_angle, max_step=c.max_step)
+    assert np.array_equal(tn, tn_ref) and np.array_equal(tf, tf_ref)
+    assert alive == int(has.sum())
 
 
 # ============================================================================ filter
